@@ -1,0 +1,159 @@
+/*
+ * ffst.h — C ABI of the B200-native Fast Finite Shearlet Transform (FFST,
+ * arxiv 1202.1773; citations "P:Lnnn" are lines of the paper's PAPER.md).
+ *
+ * The library computes, on one CUDA device (sm_100a), the data-parallel hot
+ * path of the paper: the forward transform
+ *     SH(f)(i) = ifft2( psi_hat_i * fft2(f) ),  i = 1..eta          (eq:shearletTransform)
+ * and its adjoint / inverse
+ *     f = Re ifft2( sum_i psi_hat_i * fft2(c_i) )                  (eq:inverseShearletTransform)
+ * with the cone-adapted Meyer shearlet spectra psi_hat_i of Sec. 2-3.5
+ * evaluated on the fly inside the kernels (never stored).
+ *
+ * Conventions (all functions):
+ *  - Images are real, square, row-major [batch][n][n]: element (r, c) is the
+ *    sample at m2 = r (row), m1 = c (column).
+ *  - Coefficient cubes are complex, interleaved (re, im), row-major
+ *    [batch][eta_local][n][n], planes in the flat-index order of Sec. 3.5.1
+ *    (P:L2076-2097).  Coefficients are complex: for even n the finest-scale
+ *    planes carry an imaginary part (reading A8).
+ *  - Element precision is the plan's dtype (float or double) for images and
+ *    for each of re/im of coefficients.
+ *  - Flat indices in this ABI are 0-based (the paper's i = index + 1).
+ *  - Ownership: the caller owns every image / coefficient / spectra buffer it
+ *    passes (device memory unless the function name ends in _host).  The plan
+ *    owns its tables and workspace, allocated once in ffst_plan_create; no call
+ *    allocates device memory and the library never frees caller memory.
+ *  - Streams: `stream` is a cudaStream_t (0 = legacy default stream).  All
+ *    device-buffer calls are asynchronous on that stream; a plan serves one
+ *    stream at a time (calls on one plan must not overlap).
+ *  - Errors: every function returns an ffst_status (never aborts, never throws).
+ *    Arguments are validated before anything is launched.  CUDA failures map to
+ *    FFST_ERR_CUDA with a detail string (ffst_last_error_detail, thread-local);
+ *    asynchronous kernel faults surface at a later call or synchronisation.
+ *  - Buffers must be 16-byte aligned and contiguous.
+ *  - Multi-GPU (eta-sharding): a plan created with shard_count = G > 1 owns the
+ *    planes i with (i mod G) == shard_rank; its cube holds only those planes and
+ *    its inverse returns the partial image of those planes (the caller reduces the
+ *    partials across ranks, e.g. with an NCCL reduce: the inverse is linear in the
+ *    planes, eq:inverseShearletTransform).
+ */
+#ifndef FFST_H
+#define FFST_H
+
+#include <stddef.h>
+
+#ifdef __cplusplus
+extern "C" {
+#endif
+
+typedef enum {
+  FFST_OK = 0,
+  FFST_ERR_INVALID_SIZE = 1,   /* n < 4 (no scale fits) or n > 4096 */
+  FFST_ERR_INVALID_ARG = 2,    /* null pointer, bad batch / shard / option */
+  FFST_ERR_INDEX = 3,          /* flat index or (kind, j, k) outside the system */
+  FFST_ERR_DTYPE = 4,          /* unknown dtype */
+  FFST_ERR_ALIGNMENT = 5,      /* buffer not 16-byte aligned */
+  FFST_ERR_OOM = 6,            /* workspace allocation failed at plan creation */
+  FFST_ERR_CUDA = 7,           /* CUDA runtime error (see ffst_last_error_detail) */
+  FFST_ERR_NCCL = 8,           /* reserved */
+  FFST_ERR_UNSUPPORTED = 9     /* n not a power of two, or variant not built */
+} ffst_status;
+
+typedef enum { FFST_F32 = 0, FFST_F64 = 1 } ffst_dtype;
+
+/* FFST_CLASSIC: meyerShearletSpect, eq:Psi1/eq:Psi2. */
+typedef enum { FFST_CLASSIC = 0, FFST_SMOOTH = 1 } ffst_variant;
+
+/* Shearlet kinds of the flat index (Sec. 3.5.1): low-pass, horizontal cone,
+ * vertical cone, glued seam ("h x v", |k| = 2^j). */
+typedef enum { FFST_KIND_LOWPASS = 0, FFST_KIND_H = 1, FFST_KIND_V = 2, FFST_KIND_X = 3 } ffst_kind;
+
+typedef struct ffst_plan ffst_plan;   /* opaque */
+
+typedef struct {
+  int n;              /* image side, power of two, 4 <= n <= 4096 */
+  int j0;             /* number of scales; 0 = default floor(log2(n)/2) */
+  int batch;          /* maximum images per call, >= 1 */
+  ffst_dtype dtype;   /* FFST_F32 or FFST_F64 */
+  ffst_variant variant;
+  int device;         /* CUDA device ordinal */
+  int shard_rank;     /* 0 <= shard_rank < shard_count */
+  int shard_count;    /* >= 1; planes i (0-based) with i % shard_count == shard_rank are local */
+} ffst_plan_desc;
+
+/* ---- host-only queries (no device needed) ------------------------------ */
+
+/* j0 = floor(1/2 log2 n).  n < 4 -> FFST_ERR_INVALID_SIZE. */
+ffst_status ffst_scales_for_size(int n, int* j0);
+
+/* eta = 2^(j0+2) - 3 (eq:numberOfScalesAndShears); -1 if j0 < 1. */
+int ffst_num_shearlets(int j0);
+
+/* Flat index (0-based) <-> (kind, j, k), order of Sec. 3.5.1:
+ * per band j: (h,0), (h,-1..-(2^j-1)), (x,-2^j), (v,-2^j+1..2^j-1), (x,2^j), (h,2^j-1..1).
+ * The low-pass (index 0) reports kind 0, j = 0, k = 0. */
+ffst_status ffst_index_to_params(int j0, int index, int* kind, int* j, int* k);
+ffst_status ffst_params_to_index(int j0, int kind, int j, int k, int* index);
+
+/* Column range [*col_lo, *col_hi] (0 <= col <= n/2, column c <-> |omega_1| = c on the
+ * Delta-scaled grid) outside which plane `index` is identically zero
+ * (used for pruning the first FFT pass; a superset of the true support). */
+ffst_status ffst_plane_support(int n, int j0, int index, int* col_lo, int* col_hi);
+
+/* 1 if plane `index` is not point-symmetric on the even grid (non-zero
+ * anti-symmetric part on the Nyquist row/column), else 0. */
+ffst_status ffst_plane_is_nyquist(int n, int j0, int index, int* is_nyquist);
+
+/* ---- plans ------------------------------------------------------------- */
+
+ffst_status ffst_plan_create(ffst_plan** out, const ffst_plan_desc* desc);
+ffst_status ffst_plan_destroy(ffst_plan* plan);
+
+/* Number of local planes and (if global_indices != NULL) their 0-based global indices. */
+ffst_status ffst_plan_local_planes(const ffst_plan* plan, int* count, int* global_indices);
+ffst_status ffst_plan_workspace_bytes(const ffst_plan* plan, size_t* bytes);
+ffst_status ffst_plan_info(const ffst_plan* plan, int* n, int* j0, int* eta, int* eta_local, int* batch);
+
+/* ---- transforms (device buffers) ---------------------------------------- */
+
+/* Materialise the local spectra psi_hat_i (tests / diagnostics only; the
+ * transforms never store them): psi is [eta_local][n][n] real; centred != 0 puts
+ * omega = 0 at (n/2, n/2) (the paper's Psi layout), else natural
+ * FFT bin order. */
+ffst_status ffst_shearlet_spectra(ffst_plan* plan, void* psi, int centred, void* stream);
+
+/* Forward: img [batch][n][n] real -> coeff [batch][eta_local][n][n] complex. */
+ffst_status ffst_sheartrans(ffst_plan* plan, const void* img, void* coeff, void* stream);
+ffst_status ffst_sheartrans_batch(ffst_plan* plan, const void* img, void* coeff, int batch, void* stream);
+
+/* Inverse / adjoint: coeff [batch][eta_local][n][n] complex -> img_out [batch][n][n] real
+ * = Re ifft2(sum_{local i} psi_hat_i fft2(c_i)) (the full image when shard_count == 1). */
+ffst_status ffst_inversesheartrans(ffst_plan* plan, const void* coeff, void* img_out, void* stream);
+ffst_status ffst_inversesheartrans_batch(ffst_plan* plan, const void* coeff, void* img_out, int batch, void* stream);
+
+/* ---- host-buffer variants (end-to-end path) ----------------------------- */
+
+/* Same as the _batch calls, with the image in HOST memory (pinned for full speed):
+ * the host<->device copy of the image is issued on `stream` inside the call
+ * (through a plan-owned device staging buffer).  The cube stays on the device. */
+ffst_status ffst_sheartrans_host(ffst_plan* plan, const void* img_host, void* coeff, int batch, void* stream);
+ffst_status ffst_inversesheartrans_host(ffst_plan* plan, const void* coeff, void* img_host, int batch, void* stream);
+
+/* ---- instrumentation ----------------------------------------------------- */
+
+/* enable != 0: record CUDA events around each internal kernel phase (on the
+ * call's stream).  ffst_plan_phase_times returns the durations (ms) of the last
+ * call of each direction: times[0] = forward main kernel, [1] = inverse main
+ * kernel, [2] = forward total, [3] = inverse total; launches[0..1] = number of
+ * kernels the last forward / inverse call launched.  Synchronises the events. */
+ffst_status ffst_plan_set_timing(ffst_plan* plan, int enable);
+ffst_status ffst_plan_phase_times(ffst_plan* plan, float* times, int* launches);
+
+const char* ffst_status_string(ffst_status status);
+const char* ffst_last_error_detail(void);
+
+#ifdef __cplusplus
+}
+#endif
+#endif /* FFST_H */

@@ -1,0 +1,9 @@
+"""B200-native Fast Finite Shearlet Transform (arxiv 1202.1773): forward
+transform and its adjoint as sm_100a CUDA kernels behind the C ABI of
+include/ffst.h.  See DESIGN.md."""
+from ._lib import EXPORTED, FFSTError, LIB_PATH, lib  # noqa: F401
+from .plan import (KIND_NAMES, Plan, index_to_params, num_shearlets, params_to_index,  # noqa: F401
+                   plane_is_nyquist, plane_support, scales_for_size)
+
+__all__ = ["Plan", "FFSTError", "scales_for_size", "num_shearlets", "index_to_params",
+           "params_to_index", "plane_support", "plane_is_nyquist", "KIND_NAMES"]

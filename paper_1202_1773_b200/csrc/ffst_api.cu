@@ -1,0 +1,730 @@
+// ffst_api.cu — host planner and the C ABI of include/ffst.h.
+//
+// The planner turns (n, j0, batch, shard) into:
+//  * the local plane table (flat index order of Sec. 3.5.1), each plane's
+//    Hermitian-half column range (pruning of the first FFT pass) and Nyquist flag;
+//  * the work queues of the persistent kernels: units (image, plane) grouped into
+//    single-image chunks whose intermediates fit one ring slot (L2-resident), items
+//    ordered P1(0), P1(1), P2(0), P1(2), P2(1), ... so that every dependency of an
+//    item is an earlier item (deadlock-free dynamic scheduling);
+//  * all device workspace, allocated once here (no allocation per call).
+#include <cuda_runtime.h>
+
+#include <algorithm>
+#include <cmath>
+#include <cstdio>
+#include <cstdlib>
+#include <cstring>
+#include <map>
+#include <string>
+#include <vector>
+
+#include "../../include/ffst.h"
+#include "ffst_internal.h"
+
+using namespace ffst;
+
+namespace {
+
+thread_local std::string g_detail;
+
+ffst_status fail(ffst_status s, const std::string& why) {
+  g_detail = why;
+  return s;
+}
+
+ffst_status cuda_fail(cudaError_t e, const char* where) {
+  g_detail = std::string(where) + ": " + cudaGetErrorString(e);
+  return FFST_ERR_CUDA;
+}
+
+#define API_CUDA(x, where)                       \
+  do {                                           \
+    cudaError_t e_ = (x);                        \
+    if (e_ != cudaSuccess) return cuda_fail(e_, where); \
+  } while (0)
+
+bool is_pow2(int n) { return n > 0 && (n & (n - 1)) == 0; }
+
+int default_j0(int n) {
+  int bits = 0;
+  while ((1 << (bits + 1)) <= n) ++bits;   // floor(log2 n)
+  return bits / 2;
+}
+
+struct Triple { int kind, j, k; };
+
+std::vector<Triple> index_table(int j0) {
+  std::vector<Triple> t;
+  t.push_back({0, 0, 0});
+  for (int j = 0; j < j0; ++j) {
+    const int K = 1 << j;
+    t.push_back({1, j, 0});
+    for (int k = -1; k > -K; --k) t.push_back({1, j, k});
+    t.push_back({3, j, -K});
+    for (int k = -K + 1; k < K; ++k) t.push_back({2, j, k});
+    t.push_back({3, j, K});
+    for (int k = K - 1; k > 0; --k) t.push_back({1, j, k});
+  }
+  return t;
+}
+
+double grid_delta(int n, int j0) { return std::ldexp(1.0, 2 * j0) / (double)n; }   // P:L2180, N_odd - 1 = n
+
+// Superset of the columns c = |u1| (0..n/2) where the plane can be non-zero.
+void plane_columns(int n, int j0, const Triple& tr, int* lo, int* hi) {
+  const int H = n / 2;
+  const double delta = grid_delta(n, j0);
+  auto clampi = [&](long v) { return (int)std::max(0L, std::min((long)H, v)); };
+  if (tr.kind == 0) {
+    *lo = 0;
+    *hi = clampi((long)std::ceil(1.0 / delta));
+    return;
+  }
+  const double s = delta / std::ldexp(1.0, 2 * tr.j);      // 4^-j Delta
+  const long band_lo = (long)std::floor(0.5 / s);           // psi1(s a) > 0  <=>  1/2 < s a < 4
+  const long band_hi = (long)std::ceil(4.0 / s);
+  const int K = 1 << tr.j;
+  const int ak = std::abs(tr.k);
+  int hlo = H + 1, hhi = -1, vlo = H + 1, vhi = -1;
+  if (tr.kind == 1 || tr.kind == 3) {
+    hlo = clampi(band_lo);
+    hhi = clampi(band_hi);
+  }
+  if (tr.kind == 2 || tr.kind == 3) {
+    const long u2max = std::min((long)H, band_hi);
+    const double frac_hi = std::min(1.0, (double)(1 + ak) / K);
+    vhi = clampi((long)std::ceil(u2max * frac_hi) + 1);
+    vlo = ak >= 2 ? clampi((long)std::floor(band_lo * (double)(ak - 1) / K) - 1) : 0;
+  }
+  *lo = std::min(hlo, vlo);
+  *hi = std::max(hhi, vhi);
+}
+
+bool plane_nyquist(int n, int j0, const Triple& tr) {
+  PlaneDev P{};
+  P.kind = tr.kind; P.j = tr.j; P.k = tr.k;
+  const int H = n / 2;
+  const double delta = grid_delta(n, j0);
+  for (int u = -H; u < H; ++u) {
+    if (window_anti<double>(P, u, -H, H, delta) != 0.0) return true;
+    if (window_anti<double>(P, -H, u, H, delta) != 0.0) return true;
+  }
+  return false;
+}
+
+struct Queue {
+  int batch = 0;
+  int n_chunks = 0, n_fwd = 0, n_inv = 0, n_g = 0;
+  long long slot_elems = 0;
+  int nslots = 0;
+  UnitDev* d_units = nullptr;
+  ChunkDev* d_chunks = nullptr;
+  ItemDev* d_fwd = nullptr;
+  ItemDev* d_inv = nullptr;
+};
+
+}  // namespace
+
+struct ffst_plan {
+  ffst_plan_desc d{};
+  int n = 0, j0 = 0, eta = 0, eta_l = 0, H = 0;
+  size_t rsz = 0;       // bytes per real
+  double delta = 0;
+  std::vector<PlaneDev> planes;
+  std::vector<int> nyq;
+  Geometry geo{};
+  int sm_count = 0, grid_fwd = 0, grid_inv = 0;
+  long long slot_budget = 0;
+  // device memory
+  PlaneDev* d_planes = nullptr;
+  int* d_nyq = nullptr;
+  void* d_tw = nullptr;
+  void *F = nullptr, *Fscr = nullptr, *A = nullptr, *W = nullptr;
+  long long W_elems = 0;
+  void *nyq_fwd = nullptr, *nyq_S = nullptr, *nyq_T = nullptr, *corr = nullptr;
+  void* stage = nullptr;          // host-variant image staging [batch][n][n]
+  int* d_ctr = nullptr;
+  size_t ctr_cap = 0;
+  int n_rowitems = 0;
+  std::map<int, Queue> queues;
+  size_t ws_bytes = 0;
+  bool timing = false;
+  cudaEvent_t ev[8] = {};
+  int launches[2] = {0, 0};
+  std::vector<void*> allocs;
+};
+
+namespace {
+
+template <typename T>
+void fill_twiddles(std::vector<unsigned char>& buf, int n) {
+  buf.resize((size_t)n * sizeof(cpx<T>));
+  cpx<T>* tw = reinterpret_cast<cpx<T>*>(buf.data());
+  for (int m = 0; m < n; ++m) {
+    // exp(-2 pi i m / n) from the angle reduced to [0, pi/4] for accuracy
+    const long double a = 2.0L * 3.14159265358979323846264338327950288L * (long double)m / (long double)n;
+    tw[m].x = (T)cosl(a);
+    tw[m].y = (T)(-sinl(a));
+  }
+}
+
+ffst_status dalloc(ffst_plan* p, void** ptr, size_t bytes) {
+  if (bytes == 0) bytes = 16;
+  cudaError_t e = cudaMalloc(ptr, bytes);
+  if (e != cudaSuccess) {
+    cudaGetLastError();
+    return fail(FFST_ERR_OOM, std::string("cudaMalloc ") + std::to_string(bytes) + " bytes: " + cudaGetErrorString(e));
+  }
+  p->allocs.push_back(*ptr);
+  p->ws_bytes += bytes;
+  return FFST_OK;
+}
+
+#define TRY(x) do { ffst_status s_ = (x); if (s_ != FFST_OK) return s_; } while (0)
+
+ffst_status build_queue(ffst_plan* p, int batch, Queue** out) {
+  auto it = p->queues.find(batch);
+  if (it != p->queues.end()) { *out = &it->second; return FFST_OK; }
+  const int N = p->n, H = p->H;
+  const Geometry& g = p->geo;
+  std::vector<UnitDev> units;
+  std::vector<ChunkDev> chunks;
+  // chunking: single-image chunks, intermediates of the chunk <= slot budget
+  for (int b = 0; b < batch; ++b) {
+    long long used = 0;
+    int start = (int)units.size();
+    for (int lp = 0; lp < p->eta_l; ++lp) {
+      const long long need = (long long)N * p->planes[lp].ncols_pad;
+      if ((int)units.size() > start && used + need > p->slot_budget) {
+        ChunkDev c{};
+        c.b = b; c.unit0 = start; c.nunits = (int)units.size() - start;
+        chunks.push_back(c);
+        start = (int)units.size();
+        used = 0;
+      }
+      UnitDev u{};
+      u.b = b; u.p = lp; u.chunk = (int)chunks.size(); u.woff = (int)used;
+      units.push_back(u);
+      used += need;
+    }
+    ChunkDev c{};
+    c.b = b; c.unit0 = start; c.nunits = (int)units.size() - start;
+    chunks.push_back(c);
+  }
+  Queue q;
+  q.batch = batch;
+  q.n_chunks = (int)chunks.size();
+  long long slot = 0;
+  for (auto& c : chunks) {
+    long long s = 0;
+    for (int u = c.unit0; u < c.unit0 + c.nunits; ++u) {
+      units[u].chunk = (int)(&c - chunks.data());
+      s += (long long)N * p->planes[units[u].p].ncols_pad;
+    }
+    slot = std::max(slot, s);
+  }
+  q.slot_elems = (slot + 63) / 64 * 64;
+  q.nslots = std::min(3, q.n_chunks);
+  if (q.slot_elems * q.nslots > p->W_elems)
+    return fail(FFST_ERR_INVALID_ARG, "intermediate ring larger than the planned workspace");
+  // first-of-image flags
+  for (size_t c = 0; c < chunks.size(); ++c) {
+    chunks[c].slot = (int)(c % q.nslots);
+    chunks[c].prev_slot_chunk = (int)c - q.nslots >= 0 ? (int)c - q.nslots : -1;
+    chunks[c].first_of_image = (c == 0 || chunks[c - 1].b != chunks[c].b) ? 1 : 0;
+  }
+  // ---- forward items
+  std::vector<std::vector<ItemDev>> f1(chunks.size()), f2(chunks.size()), i1(chunks.size()), i2(chunks.size());
+  const int ngroups = (H + 1 + g.lpc - 1) / g.lpc;
+  std::vector<int> last_self((size_t)batch * ngroups, -1);
+  int n_self = 0;
+  for (size_t c = 0; c < chunks.size(); ++c) {
+    const ChunkDev& ch = chunks[c];
+    for (int u = ch.unit0; u < ch.unit0 + ch.nunits; ++u) {
+      const PlaneDev& P = p->planes[units[u].p];
+      const int ng1 = (P.ncols + g.gc - 1) / g.gc;
+      for (int gi = 0; gi < ng1; ++gi) f1[c].push_back({0, (int)c, u, gi, -1, -1});
+      const int ng2 = (N + g.rp2 - 1) / g.rp2;
+      for (int gi = 0; gi < ng2; ++gi) f2[c].push_back({1, (int)c, u, gi, -1, -1});
+      const int ni1 = (N + g.rpi - 1) / g.rpi;
+      for (int gi = 0; gi < ni1; ++gi) i1[c].push_back({0, (int)c, u, gi, -1, -1});
+    }
+    for (int gg = 0; gg < ngroups; ++gg) {
+      bool touched = ch.first_of_image != 0;
+      const int g0 = gg * g.lpc, g1 = std::min(g0 + g.lpc, H + 1);
+      for (int u = ch.unit0; u < ch.unit0 + ch.nunits && !touched; ++u) {
+        const PlaneDev& P = p->planes[units[u].p];
+        if (g1 > P.c_lo && g0 < P.c_lo + P.ncols) touched = true;
+      }
+      if (!touched) continue;
+      int& last = last_self[(size_t)ch.b * ngroups + gg];
+      i2[c].push_back({1, (int)c, -1, gg, last, n_self});
+      last = n_self++;
+    }
+  }
+  std::vector<ItemDev> fwd, inv;
+  auto order = [&](std::vector<std::vector<ItemDev>>& a, std::vector<std::vector<ItemDev>>& b,
+                   std::vector<ItemDev>& dst) {
+    const int C = (int)chunks.size();
+    for (int c = 0; c < C; ++c) {
+      dst.insert(dst.end(), a[c].begin(), a[c].end());
+      if (c >= 1) dst.insert(dst.end(), b[c - 1].begin(), b[c - 1].end());
+    }
+    dst.insert(dst.end(), b[C - 1].begin(), b[C - 1].end());
+  };
+  order(f1, f2, fwd);
+  order(i1, i2, inv);
+  for (size_t c = 0; c < chunks.size(); ++c) {
+    chunks[c].p1_items = (int)f1[c].size();   // forward counts; inverse counts set at launch
+    chunks[c].p2_items = (int)f2[c].size();
+  }
+  std::vector<ChunkDev> chunks_inv = chunks;
+  for (size_t c = 0; c < chunks.size(); ++c) {
+    chunks_inv[c].p1_items = (int)i1[c].size();
+    chunks_inv[c].p2_items = (int)i2[c].size();
+  }
+  q.n_fwd = (int)fwd.size();
+  q.n_inv = (int)inv.size();
+  q.n_g = n_self;
+  const size_t need_ctr = 1 + 2 * chunks.size() + (size_t)n_self;
+  if (need_ctr > p->ctr_cap) {
+    void* c = nullptr;
+    TRY(dalloc(p, &c, need_ctr * sizeof(int)));
+    p->d_ctr = static_cast<int*>(c);
+    p->ctr_cap = need_ctr;
+  }
+  void* ptr = nullptr;
+  TRY(dalloc(p, &ptr, units.size() * sizeof(UnitDev)));
+  q.d_units = static_cast<UnitDev*>(ptr);
+  TRY(dalloc(p, &ptr, 2 * chunks.size() * sizeof(ChunkDev)));
+  q.d_chunks = static_cast<ChunkDev*>(ptr);
+  TRY(dalloc(p, &ptr, fwd.size() * sizeof(ItemDev)));
+  q.d_fwd = static_cast<ItemDev*>(ptr);
+  TRY(dalloc(p, &ptr, inv.size() * sizeof(ItemDev)));
+  q.d_inv = static_cast<ItemDev*>(ptr);
+  API_CUDA(cudaMemcpy(q.d_units, units.data(), units.size() * sizeof(UnitDev), cudaMemcpyHostToDevice), "queue upload");
+  API_CUDA(cudaMemcpy(q.d_chunks, chunks.data(), chunks.size() * sizeof(ChunkDev), cudaMemcpyHostToDevice), "queue upload");
+  API_CUDA(cudaMemcpy(q.d_chunks + chunks.size(), chunks_inv.data(), chunks.size() * sizeof(ChunkDev),
+                      cudaMemcpyHostToDevice), "queue upload");
+  API_CUDA(cudaMemcpy(q.d_fwd, fwd.data(), fwd.size() * sizeof(ItemDev), cudaMemcpyHostToDevice), "queue upload");
+  API_CUDA(cudaMemcpy(q.d_inv, inv.data(), inv.size() * sizeof(ItemDev), cudaMemcpyHostToDevice), "queue upload");
+  auto res = p->queues.emplace(batch, q);
+  *out = &res.first->second;
+  return FFST_OK;
+}
+
+KParams base_params(ffst_plan* p) {
+  KParams k{};
+  k.n = p->n; k.j0 = p->j0; k.batch = p->d.batch; k.eta_l = p->eta_l; k.n_nyq = (int)p->nyq.size();
+  k.delta = p->delta;
+  k.planes = p->d_planes;
+  k.nyq_planes = p->d_nyq;
+  k.tw = p->d_tw;
+  k.F = p->F; k.Fscr = p->Fscr; k.A = p->A; k.W = p->W;
+  k.nyq_fwd = p->nyq_fwd; k.nyq_S = p->nyq_S; k.nyq_T = p->nyq_T; k.corr = p->corr;
+  k.n_rowitems = p->n_rowitems;
+  return k;
+}
+
+template <typename T>
+struct Ops {
+  static Geometry geo(int n) { return geometry<T>(n); }
+};
+
+cudaError_t L_spectrum(ffst_plan* p, const KParams& k, int b, cudaStream_t s) {
+  return p->d.dtype == FFST_F32 ? launch_spectrum<float>(k, b, s) : launch_spectrum<double>(k, b, s);
+}
+cudaError_t L_nyq_fwd(ffst_plan* p, const KParams& k, int b, cudaStream_t s) {
+  return p->d.dtype == FFST_F32 ? launch_nyq_fwd<float>(k, b, s) : launch_nyq_fwd<double>(k, b, s);
+}
+cudaError_t L_fwd_main(ffst_plan* p, const KParams& k, int g, cudaStream_t s) {
+  return p->d.dtype == FFST_F32 ? launch_fwd_main<float>(k, g, s) : launch_fwd_main<double>(k, g, s);
+}
+cudaError_t L_inv_main(ffst_plan* p, const KParams& k, int g, cudaStream_t s) {
+  return p->d.dtype == FFST_F32 ? launch_inv_main<float>(k, g, s) : launch_inv_main<double>(k, g, s);
+}
+cudaError_t L_nyq_inv(ffst_plan* p, const KParams& k, int b, cudaStream_t s) {
+  return p->d.dtype == FFST_F32 ? launch_nyq_inv<float>(k, b, s) : launch_nyq_inv<double>(k, b, s);
+}
+cudaError_t L_final(ffst_plan* p, const KParams& k, int b, cudaStream_t s) {
+  return p->d.dtype == FFST_F32 ? launch_final<float>(k, b, s) : launch_final<double>(k, b, s);
+}
+
+bool aligned16(const void* ptr) { return (reinterpret_cast<uintptr_t>(ptr) & 15u) == 0; }
+
+ffst_status set_device(ffst_plan* p) {
+  API_CUDA(cudaSetDevice(p->d.device), "cudaSetDevice");
+  return FFST_OK;
+}
+
+ffst_status forward_impl(ffst_plan* p, const void* img, void* coeff, int batch, cudaStream_t s) {
+  if (!img || !coeff) return fail(FFST_ERR_INVALID_ARG, "null buffer");
+  if (batch < 1 || batch > p->d.batch) return fail(FFST_ERR_INVALID_ARG, "batch outside 1..plan batch");
+  if (!aligned16(img) || !aligned16(coeff)) return fail(FFST_ERR_ALIGNMENT, "buffers must be 16-byte aligned");
+  TRY(set_device(p));
+  Queue* q = nullptr;
+  TRY(build_queue(p, batch, &q));
+  KParams k = base_params(p);
+  k.batch = batch;
+  k.img = img;
+  k.coeff = coeff;
+  k.units = q->d_units;
+  k.chunks = q->d_chunks;
+  k.items = q->d_fwd;
+  k.n_items = q->n_fwd;
+  k.slot_elems = q->slot_elems;
+  k.ctr = p->d_ctr;
+  k.ctr_p1 = 1;
+  k.ctr_p2 = 1 + q->n_chunks;
+  k.ctr_g = 1 + 2 * q->n_chunks;
+  int nl = 0;
+  if (p->timing) API_CUDA(cudaEventRecord(p->ev[0], s), "event");
+  API_CUDA(L_spectrum(p, k, batch, s), "spectrum kernels");
+  nl += 2;
+  if (!p->nyq.empty()) {
+    API_CUDA(L_nyq_fwd(p, k, batch, s), "nyq_fwd kernel");
+    ++nl;
+  }
+  API_CUDA(cudaMemsetAsync(p->d_ctr, 0, (1 + 2 * (size_t)q->n_chunks) * sizeof(int), s), "counter reset");
+  if (p->timing) API_CUDA(cudaEventRecord(p->ev[1], s), "event");
+  API_CUDA(L_fwd_main(p, k, p->grid_fwd, s), "fwd_main kernel");
+  ++nl;
+  if (p->timing) {
+    API_CUDA(cudaEventRecord(p->ev[2], s), "event");
+  }
+  p->launches[0] = nl;
+  return FFST_OK;
+}
+
+ffst_status inverse_impl(ffst_plan* p, const void* coeff, void* img_out, int batch, cudaStream_t s) {
+  if (!img_out || !coeff) return fail(FFST_ERR_INVALID_ARG, "null buffer");
+  if (batch < 1 || batch > p->d.batch) return fail(FFST_ERR_INVALID_ARG, "batch outside 1..plan batch");
+  if (!aligned16(img_out) || !aligned16(coeff)) return fail(FFST_ERR_ALIGNMENT, "buffers must be 16-byte aligned");
+  TRY(set_device(p));
+  Queue* q = nullptr;
+  TRY(build_queue(p, batch, &q));
+  KParams k = base_params(p);
+  k.batch = batch;
+  k.coeff = const_cast<void*>(coeff);
+  k.img_out = img_out;
+  k.units = q->d_units;
+  k.chunks = q->d_chunks + q->n_chunks;
+  k.items = q->d_inv;
+  k.n_items = q->n_inv;
+  k.slot_elems = q->slot_elems;
+  k.ctr = p->d_ctr;
+  k.ctr_p1 = 1;
+  k.ctr_p2 = 1 + q->n_chunks;
+  k.ctr_g = 1 + 2 * q->n_chunks;
+  int nl = 0;
+  if (p->timing) API_CUDA(cudaEventRecord(p->ev[3], s), "event");
+  API_CUDA(cudaMemsetAsync(p->d_ctr, 0, (1 + 2 * (size_t)q->n_chunks + q->n_g) * sizeof(int), s), "counter reset");
+  if (p->timing) API_CUDA(cudaEventRecord(p->ev[4], s), "event");
+  API_CUDA(L_inv_main(p, k, p->grid_inv, s), "inv_main kernel");
+  ++nl;
+  if (p->timing) API_CUDA(cudaEventRecord(p->ev[5], s), "event");
+  if (!p->nyq.empty()) {
+    API_CUDA(L_nyq_inv(p, k, batch, s), "nyq_inv kernel");
+    ++nl;
+  }
+  API_CUDA(L_final(p, k, batch, s), "final kernels");
+  nl += 2;
+  if (p->timing) API_CUDA(cudaEventRecord(p->ev[6], s), "event");
+  p->launches[1] = nl;
+  return FFST_OK;
+}
+
+}  // namespace
+
+// ============================================================================ C ABI
+
+extern "C" {
+
+ffst_status ffst_scales_for_size(int n, int* j0) {
+  if (!j0) return fail(FFST_ERR_INVALID_ARG, "null j0");
+  if (n < 4) return fail(FFST_ERR_INVALID_SIZE, "n < 4: no scale fits (P:L2163-2168)");
+  *j0 = default_j0(n);
+  return FFST_OK;
+}
+
+int ffst_num_shearlets(int j0) { return j0 < 1 || j0 > 12 ? -1 : (1 << (j0 + 2)) - 3; }
+
+ffst_status ffst_index_to_params(int j0, int index, int* kind, int* j, int* k) {
+  if (!kind || !j || !k) return fail(FFST_ERR_INVALID_ARG, "null output");
+  if (j0 < 1 || j0 > 12) return fail(FFST_ERR_INVALID_ARG, "j0 outside 1..12");
+  if (index < 0 || index >= ffst_num_shearlets(j0)) return fail(FFST_ERR_INDEX, "index outside 0..eta-1");
+  const Triple t = index_table(j0)[index];
+  *kind = t.kind; *j = t.j; *k = t.k;
+  return FFST_OK;
+}
+
+ffst_status ffst_params_to_index(int j0, int kind, int j, int k, int* index) {
+  if (!index) return fail(FFST_ERR_INVALID_ARG, "null output");
+  if (j0 < 1 || j0 > 12) return fail(FFST_ERR_INVALID_ARG, "j0 outside 1..12");
+  const auto t = index_table(j0);
+  for (size_t i = 0; i < t.size(); ++i)
+    if (t[i].kind == kind && t[i].j == j && t[i].k == k && (kind != 0 || (j == 0 && k == 0))) {
+      *index = (int)i;
+      return FFST_OK;
+    }
+  return fail(FFST_ERR_INDEX, "no shearlet with these parameters");
+}
+
+ffst_status ffst_plane_support(int n, int j0, int index, int* col_lo, int* col_hi) {
+  if (!col_lo || !col_hi) return fail(FFST_ERR_INVALID_ARG, "null output");
+  if (n < 4) return fail(FFST_ERR_INVALID_SIZE, "n < 4");
+  if (!is_pow2(n)) return fail(FFST_ERR_UNSUPPORTED, "n must be a power of two");
+  if (j0 == 0) j0 = default_j0(n);
+  if (j0 < 1 || j0 > 12) return fail(FFST_ERR_INVALID_ARG, "j0 outside 1..12");
+  if (index < 0 || index >= ffst_num_shearlets(j0)) return fail(FFST_ERR_INDEX, "index outside 0..eta-1");
+  plane_columns(n, j0, index_table(j0)[index], col_lo, col_hi);
+  return FFST_OK;
+}
+
+ffst_status ffst_plane_is_nyquist(int n, int j0, int index, int* is_nyquist) {
+  if (!is_nyquist) return fail(FFST_ERR_INVALID_ARG, "null output");
+  if (n < 4) return fail(FFST_ERR_INVALID_SIZE, "n < 4");
+  if (!is_pow2(n)) return fail(FFST_ERR_UNSUPPORTED, "n must be a power of two");
+  if (j0 == 0) j0 = default_j0(n);
+  if (j0 < 1 || j0 > 12) return fail(FFST_ERR_INVALID_ARG, "j0 outside 1..12");
+  if (index < 0 || index >= ffst_num_shearlets(j0)) return fail(FFST_ERR_INDEX, "index outside 0..eta-1");
+  *is_nyquist = plane_nyquist(n, j0, index_table(j0)[index]) ? 1 : 0;
+  return FFST_OK;
+}
+
+ffst_status ffst_plan_destroy(ffst_plan* p) {
+  if (!p) return FFST_OK;
+  int cur = -1;
+  cudaGetDevice(&cur);
+  cudaSetDevice(p->d.device);
+  for (void* a : p->allocs) cudaFree(a);
+  for (auto& e : p->ev)
+    if (e) cudaEventDestroy(e);
+  if (cur >= 0) cudaSetDevice(cur);
+  delete p;
+  return FFST_OK;
+}
+
+ffst_status ffst_plan_create(ffst_plan** out, const ffst_plan_desc* d) {
+  if (!out || !d) return fail(FFST_ERR_INVALID_ARG, "null argument");
+  *out = nullptr;
+  if (d->n < 4) return fail(FFST_ERR_INVALID_SIZE, "n < 4: no scale fits (P:L2163-2168)");
+  if (d->dtype != FFST_F32 && d->dtype != FFST_F64) return fail(FFST_ERR_DTYPE, "dtype must be FFST_F32 or FFST_F64");
+  const int maxn = d->dtype == FFST_F32 ? 4096 : 2048;
+  if (d->n > maxn) return fail(FFST_ERR_INVALID_SIZE, "n above the largest built size (4096 f32, 2048 f64)");
+  if (!is_pow2(d->n)) return fail(FFST_ERR_UNSUPPORTED, "n must be a power of two in this build");
+  if (d->variant != FFST_CLASSIC) return fail(FFST_ERR_UNSUPPORTED, "only the classic variant is built");
+  if (d->batch < 1) return fail(FFST_ERR_INVALID_ARG, "batch < 1");
+  if (d->shard_count < 1 || d->shard_rank < 0 || d->shard_rank >= d->shard_count)
+    return fail(FFST_ERR_INVALID_ARG, "bad shard_rank / shard_count");
+  const int j0 = d->j0 == 0 ? default_j0(d->n) : d->j0;
+  if (j0 < 1 || (1 << (2 * j0)) > 4 * d->n || j0 > 12)
+    return fail(FFST_ERR_INVALID_ARG, "j0 outside 1..(floor(log2 n)/2 + 1)");
+  const int eta = ffst_num_shearlets(j0);
+  if (d->shard_count > eta) return fail(FFST_ERR_INVALID_ARG, "more shards than shearlets");
+
+  ffst_plan* p = new ffst_plan();
+  p->d = *d;
+  p->n = d->n; p->j0 = j0; p->eta = eta; p->H = d->n / 2;
+  p->rsz = d->dtype == FFST_F32 ? 4 : 8;
+  p->delta = grid_delta(d->n, j0);
+  p->geo = d->dtype == FFST_F32 ? geometry<float>(d->n) : geometry<double>(d->n);
+  const auto table = index_table(j0);
+  for (int i = d->shard_rank; i < eta; i += d->shard_count) {
+    PlaneDev P{};
+    P.gi = i; P.kind = table[i].kind; P.j = table[i].j; P.k = table[i].k;
+    int lo, hi;
+    plane_columns(d->n, j0, table[i], &lo, &hi);
+    P.c_lo = lo; P.ncols = hi - lo + 1;
+    P.ncols_pad = (P.ncols + p->geo.gc - 1) / p->geo.gc * p->geo.gc;
+    P.nyq = -1;
+    if (plane_nyquist(d->n, j0, table[i])) {
+      P.nyq = (int)p->nyq.size();
+      p->nyq.push_back((int)p->planes.size());
+    }
+    p->planes.push_back(P);
+  }
+  p->eta_l = (int)p->planes.size();
+
+  auto cleanup = [&](ffst_status s) { ffst_plan_destroy(p); return s; };
+  cudaError_t e = cudaSetDevice(d->device);
+  if (e != cudaSuccess) return cleanup(cuda_fail(e, "cudaSetDevice"));
+  int dev = d->device;
+  e = cudaDeviceGetAttribute(&p->sm_count, cudaDevAttrMultiProcessorCount, dev);
+  if (e != cudaSuccess) return cleanup(cuda_fail(e, "device query"));
+  const int af = d->dtype == FFST_F32 ? max_active_main<float>(d->n, dev, 0) : max_active_main<double>(d->n, dev, 0);
+  const int ai = d->dtype == FFST_F32 ? max_active_main<float>(d->n, dev, 1) : max_active_main<double>(d->n, dev, 1);
+  if (af < 1 || ai < 1) return cleanup(fail(FFST_ERR_CUDA, "persistent kernels cannot be made resident"));
+  p->grid_fwd = p->sm_count * af;
+  p->grid_inv = p->sm_count * ai;
+
+  const size_t B = (size_t)d->batch, N = (size_t)d->n, H1 = N / 2 + 1;
+  const size_t csz = 2 * p->rsz;
+  const size_t ncpf = (H1 + p->geo.gc - 1) / p->geo.gc * p->geo.gc;
+  // ring of intermediates: slot budget ~ L2 share, at least the largest plane
+  long long maxplane = 0, image_total = 0;
+  for (auto& P : p->planes) {
+    maxplane = std::max(maxplane, (long long)N * P.ncols_pad);
+    image_total += (long long)N * P.ncols_pad;
+  }
+  const char* env = std::getenv("FFST_SLOT_MB");
+  const long long budget_bytes = (env ? std::atoll(env) : 12) * 1024LL * 1024LL;
+  p->slot_budget = std::max(maxplane, budget_bytes / (long long)csz);
+  const long long slot_max = std::min(image_total, std::max(maxplane, p->slot_budget)) + 64;
+  p->W_elems = 3 * slot_max;
+  p->n_rowitems = (int)((N + p->geo.rpi - 1) / p->geo.rpi);
+  const size_t nn = std::max<size_t>(1, p->nyq.size());
+
+  void* ptr = nullptr;
+  ffst_status st;
+#define ALLOC(dst, bytes) do { st = dalloc(p, &ptr, (bytes)); if (st != FFST_OK) return cleanup(st); dst = static_cast<decltype(dst)>(ptr); } while (0)
+  ALLOC(p->d_planes, p->planes.size() * sizeof(PlaneDev));
+  ALLOC(p->d_nyq, nn * sizeof(int));
+  ALLOC(p->d_tw, N * csz);
+  ALLOC(p->F, B * H1 * N * csz);
+  ALLOC(p->Fscr, B * std::max(H1 * N, N * ncpf) * csz);
+  ALLOC(p->A, B * H1 * N * csz);
+  ALLOC(p->W, (size_t)p->W_elems * csz);
+  ALLOC(p->nyq_fwd, B * nn * 2 * N * p->rsz);
+  ALLOC(p->nyq_S, B * nn * p->n_rowitems * N * p->rsz);
+  ALLOC(p->nyq_T, B * nn * N * p->rsz);
+  ALLOC(p->corr, B * 2 * N * p->rsz);
+  ALLOC(p->stage, B * N * N * p->rsz);
+#undef ALLOC
+  std::vector<unsigned char> tw;
+  if (d->dtype == FFST_F32) fill_twiddles<float>(tw, d->n); else fill_twiddles<double>(tw, d->n);
+  e = cudaMemcpy(p->d_tw, tw.data(), tw.size(), cudaMemcpyHostToDevice);
+  if (e == cudaSuccess) e = cudaMemcpy(p->d_planes, p->planes.data(), p->planes.size() * sizeof(PlaneDev), cudaMemcpyHostToDevice);
+  if (e == cudaSuccess && !p->nyq.empty()) e = cudaMemcpy(p->d_nyq, p->nyq.data(), p->nyq.size() * sizeof(int), cudaMemcpyHostToDevice);
+  if (e == cudaSuccess) e = cudaMemset(p->nyq_S, 0, B * nn * p->n_rowitems * N * p->rsz);
+  if (e == cudaSuccess) e = cudaMemset(p->corr, 0, B * 2 * N * p->rsz);
+  if (e != cudaSuccess) return cleanup(cuda_fail(e, "plan upload"));
+  for (auto& ev : p->ev) {
+    e = cudaEventCreate(&ev);
+    if (e != cudaSuccess) return cleanup(cuda_fail(e, "event create"));
+  }
+  Queue* q = nullptr;
+  st = build_queue(p, d->batch, &q);
+  if (st != FFST_OK) return cleanup(st);
+  *out = p;
+  return FFST_OK;
+}
+
+ffst_status ffst_plan_local_planes(const ffst_plan* p, int* count, int* global_indices) {
+  if (!p || !count) return fail(FFST_ERR_INVALID_ARG, "null argument");
+  *count = p->eta_l;
+  if (global_indices)
+    for (int i = 0; i < p->eta_l; ++i) global_indices[i] = p->planes[i].gi;
+  return FFST_OK;
+}
+
+ffst_status ffst_plan_workspace_bytes(const ffst_plan* p, size_t* bytes) {
+  if (!p || !bytes) return fail(FFST_ERR_INVALID_ARG, "null argument");
+  *bytes = p->ws_bytes;
+  return FFST_OK;
+}
+
+ffst_status ffst_plan_info(const ffst_plan* p, int* n, int* j0, int* eta, int* eta_local, int* batch) {
+  if (!p) return fail(FFST_ERR_INVALID_ARG, "null plan");
+  if (n) *n = p->n;
+  if (j0) *j0 = p->j0;
+  if (eta) *eta = p->eta;
+  if (eta_local) *eta_local = p->eta_l;
+  if (batch) *batch = p->d.batch;
+  return FFST_OK;
+}
+
+ffst_status ffst_shearlet_spectra(ffst_plan* p, void* psi, int centred, void* stream) {
+  if (!p || !psi) return fail(FFST_ERR_INVALID_ARG, "null argument");
+  TRY(set_device(p));
+  KParams k = base_params(p);
+  cudaError_t e = p->d.dtype == FFST_F32
+                      ? launch_spectra_export<float>(k, psi, centred, static_cast<cudaStream_t>(stream))
+                      : launch_spectra_export<double>(k, psi, centred, static_cast<cudaStream_t>(stream));
+  if (e != cudaSuccess) return cuda_fail(e, "spectra kernel");
+  return FFST_OK;
+}
+
+ffst_status ffst_sheartrans_batch(ffst_plan* p, const void* img, void* coeff, int batch, void* stream) {
+  if (!p) return fail(FFST_ERR_INVALID_ARG, "null plan");
+  return forward_impl(p, img, coeff, batch, static_cast<cudaStream_t>(stream));
+}
+
+ffst_status ffst_sheartrans(ffst_plan* p, const void* img, void* coeff, void* stream) {
+  if (!p) return fail(FFST_ERR_INVALID_ARG, "null plan");
+  return forward_impl(p, img, coeff, p->d.batch, static_cast<cudaStream_t>(stream));
+}
+
+ffst_status ffst_inversesheartrans_batch(ffst_plan* p, const void* coeff, void* img, int batch, void* stream) {
+  if (!p) return fail(FFST_ERR_INVALID_ARG, "null plan");
+  return inverse_impl(p, coeff, img, batch, static_cast<cudaStream_t>(stream));
+}
+
+ffst_status ffst_inversesheartrans(ffst_plan* p, const void* coeff, void* img, void* stream) {
+  if (!p) return fail(FFST_ERR_INVALID_ARG, "null plan");
+  return inverse_impl(p, coeff, img, p->d.batch, static_cast<cudaStream_t>(stream));
+}
+
+ffst_status ffst_sheartrans_host(ffst_plan* p, const void* img_host, void* coeff, int batch, void* stream) {
+  if (!p || !img_host) return fail(FFST_ERR_INVALID_ARG, "null argument");
+  if (batch < 1 || batch > p->d.batch) return fail(FFST_ERR_INVALID_ARG, "batch outside 1..plan batch");
+  TRY(set_device(p));
+  cudaStream_t s = static_cast<cudaStream_t>(stream);
+  const size_t bytes = (size_t)batch * p->n * p->n * p->rsz;
+  API_CUDA(cudaMemcpyAsync(p->stage, img_host, bytes, cudaMemcpyHostToDevice, s), "H2D image copy");
+  return forward_impl(p, p->stage, coeff, batch, s);
+}
+
+ffst_status ffst_inversesheartrans_host(ffst_plan* p, const void* coeff, void* img_host, int batch, void* stream) {
+  if (!p || !img_host) return fail(FFST_ERR_INVALID_ARG, "null argument");
+  TRY(set_device(p));
+  cudaStream_t s = static_cast<cudaStream_t>(stream);
+  TRY(inverse_impl(p, coeff, p->stage, batch, s));
+  const size_t bytes = (size_t)batch * p->n * p->n * p->rsz;
+  API_CUDA(cudaMemcpyAsync(img_host, p->stage, bytes, cudaMemcpyDeviceToHost, s), "D2H image copy");
+  return FFST_OK;
+}
+
+ffst_status ffst_plan_set_timing(ffst_plan* p, int enable) {
+  if (!p) return fail(FFST_ERR_INVALID_ARG, "null plan");
+  p->timing = enable != 0;
+  return FFST_OK;
+}
+
+ffst_status ffst_plan_phase_times(ffst_plan* p, float* times, int* launches) {
+  if (!p || !times) return fail(FFST_ERR_INVALID_ARG, "null argument");
+  if (!p->timing) return fail(FFST_ERR_INVALID_ARG, "timing not enabled");
+  TRY(set_device(p));
+  API_CUDA(cudaEventSynchronize(p->ev[6]), "event sync");
+  API_CUDA(cudaEventSynchronize(p->ev[2]), "event sync");
+  API_CUDA(cudaEventElapsedTime(&times[0], p->ev[1], p->ev[2]), "event time");
+  API_CUDA(cudaEventElapsedTime(&times[1], p->ev[4], p->ev[5]), "event time");
+  API_CUDA(cudaEventElapsedTime(&times[2], p->ev[0], p->ev[2]), "event time");
+  API_CUDA(cudaEventElapsedTime(&times[3], p->ev[3], p->ev[6]), "event time");
+  if (launches) {
+    launches[0] = p->launches[0];
+    launches[1] = p->launches[1];
+  }
+  return FFST_OK;
+}
+
+const char* ffst_status_string(ffst_status s) {
+  switch (s) {
+    case FFST_OK: return "ok";
+    case FFST_ERR_INVALID_SIZE: return "invalid size";
+    case FFST_ERR_INVALID_ARG: return "invalid argument";
+    case FFST_ERR_INDEX: return "index out of range";
+    case FFST_ERR_DTYPE: return "invalid dtype";
+    case FFST_ERR_ALIGNMENT: return "misaligned buffer";
+    case FFST_ERR_OOM: return "out of device memory";
+    case FFST_ERR_CUDA: return "CUDA error";
+    case FFST_ERR_NCCL: return "NCCL error";
+    case FFST_ERR_UNSUPPORTED: return "unsupported";
+  }
+  return "unknown status";
+}
+
+const char* ffst_last_error_detail(void) { return g_detail.c_str(); }
+
+}  // extern "C"

@@ -1,0 +1,85 @@
+// ffst_internal.h — structures shared by the host planner (ffst_api.cu) and the
+// kernels (ffst_kernels.cuh).  Not part of the public ABI.
+#pragma once
+#include <cuda_runtime.h>
+#include <stdint.h>
+#include "ffst_math.cuh"
+
+namespace ffst {
+
+// One (image, local plane) of a batch call.
+struct UnitDev {
+  int b, p;        // image in the batch, local plane index
+  int chunk;       // chunk this unit belongs to
+  int woff;        // element (complex) offset of its intermediate inside the ring slot
+};
+
+// A work item of the persistent kernels.
+//   type 0 = first pass (fwd: window * F -> column IFFT; inv: row R2C of a coefficient plane)
+//   type 1 = second pass (fwd: row C2R -> coefficients; inv: column FFT * window, accumulate)
+struct ItemDev {
+  int type, chunk, unit, group;
+  int dep;         // inverse pass 2: counter (in the group block) of the previous chunk of the same
+                   // image for this column group, or -1
+  int self;        // inverse pass 2: own counter in the group block
+};
+
+struct ChunkDev {
+  int slot;            // ring slot of the chunk's intermediates
+  int b;               // image (chunks never span images)
+  int unit0, nunits;   // units [unit0, unit0 + nunits)
+  int p1_items, p2_items;
+  int first_of_image;  // inverse: this chunk initialises the image's accumulator
+  int prev_slot_chunk; // chunk that used the same slot before (or -1)
+};
+
+struct KParams {
+  int n, j0, batch, eta_l, n_nyq;
+  double delta;                 // grid spacing Delta = 2^(2 j0) / n
+  const PlaneDev* planes;       // [eta_l]
+  const int* nyq_planes;        // [n_nyq] local plane index of each Nyquist plane
+  const void* tw;               // cpx<T>[n]: exp(-2 pi i m / n)
+  const void* img;              // [batch][n][n] T
+  void* coeff;                  // [batch][eta_l][n][n] cpx<T>
+  void* img_out;                // [batch][n][n] T
+  void* F;                      // [batch][n/2+1][n] cpx<T>: image spectrum, column-major half (F[b][u1][u2])
+  void* Fscr;                   // [batch][n/2+1][n] cpx<T>: scratch (row-pass output)
+  void* A;                      // [batch][n/2+1][n] cpx<T>: adjoint accumulator, same layout as F
+  void* W;                      // ring of intermediates, slot s at W + s * slot_elems
+  long long slot_elems;
+  void* nyq_fwd;                // [batch][n_nyq][2][n] T: forward Nyquist terms G(m1), H(r)
+  void* nyq_S;                  // [batch][n_nyq][n_rowitems][n] T: partial alternating column sums
+  void* nyq_T;                  // [batch][n_nyq][n] T: alternating row sums
+  void* corr;                   // [batch][2][n] T: inverse Nyquist corrections
+  int n_rowitems;               // inverse pass-1 items per plane (row groups)
+  const ItemDev* items;
+  int n_items;
+  const ChunkDev* chunks;
+  const UnitDev* units;
+  int* ctr;                     // [0] dispatch; [ctr_p1 + c]; [ctr_p2 + c]; [ctr_g + item]
+  int ctr_p1, ctr_p2, ctr_g;
+};
+
+// Launch geometry of one (T, N) instantiation (host + device visible).
+struct Geometry {
+  int nt;            // threads per CTA
+  int gc;            // fwd pass 1: columns per item
+  int rp2;           // fwd pass 2: rows per item
+  int rpi;           // inv pass 1: rows per item
+  int gr;            // inv pass 1: rows per tile
+  int lpc;           // inv pass 2: columns per item
+  size_t smem_fwd, smem_inv, smem_aux;   // dynamic shared bytes of the kernels
+};
+
+// Launchers (defined per dtype in ffst_kern_f32.cu / ffst_kern_f64.cu).
+template <typename T> Geometry geometry(int n);
+template <typename T> cudaError_t launch_spectrum(const KParams& p, int batch, cudaStream_t s);
+template <typename T> cudaError_t launch_nyq_fwd(const KParams& p, int batch, cudaStream_t s);
+template <typename T> cudaError_t launch_fwd_main(const KParams& p, int grid, cudaStream_t s);
+template <typename T> cudaError_t launch_inv_main(const KParams& p, int grid, cudaStream_t s);
+template <typename T> cudaError_t launch_nyq_inv(const KParams& p, int batch, cudaStream_t s);
+template <typename T> cudaError_t launch_final(const KParams& p, int batch, cudaStream_t s);
+template <typename T> cudaError_t launch_spectra_export(const KParams& p, void* psi, int centred, cudaStream_t s);
+template <typename T> int max_active_main(int n, int device, int which);   // CTAs/SM of fwd (0) / inv (1)
+
+}  // namespace ffst

@@ -1,0 +1,664 @@
+// ffst_kernels.cuh — the FFST hot path on sm_100a (included once per dtype).
+//
+// Path:
+//   forward  (eq:shearletTransform)
+//     spectrum   f -> F = fft2(f), Hermitian half, column-major  (row R2C, column FFT)
+//     nyq_fwd    rank-2 imaginary Nyquist terms of the even-N grid (per Nyquist plane)
+//     fwd_main   persistent: pass 1 = window sym_i(u) * F on the plane's column range,
+//                column IFFT -> L2-resident intermediate W; pass 2 = row C2R of W,
+//                + Nyquist term -> complex coefficient plane c_i (the only HBM stream)
+//   inverse  (eq:inverseShearletTransform)
+//     inv_main   persistent: pass 1 = row R2C of Re c_i (dense read of the cube) pruned to
+//                the plane's columns -> W (+ alternating sums of Im c_i for Nyquist planes);
+//                pass 2 = column FFT of W, * sym_i, accumulated over planes into A
+//                (deterministic: one owner per column group, chained across chunks)
+//     nyq_inv    Nyquist correction of the adjoint
+//     final      f = Re ifft2(A) (column IFFT + row C2R) - correction
+#pragma once
+#include "ffst_fft.cuh"
+#include "ffst_internal.h"
+
+namespace ffst {
+
+template <typename T, int N>
+struct Geo {
+  static constexpr int NT = 256;
+  static constexpr int ESZ = (int)sizeof(cpx<T>);
+  static constexpr int H = N / 2;
+  static constexpr int EC = RadixPlan<N>::E, THC = N / EC, LPC = NT / THC;
+  static constexpr int ER = RadixPlan<H>::E, THR = H / ER, LPR = NT / THR;
+  static constexpr int SMC = Pad<T>::len(N), SMR = Pad<T>::len(H);
+  static constexpr int SCR_C = LPC * SMC, SCR_R = LPR * SMR;
+  // forward pass 1: columns per item (>= 32-byte row segments of the intermediate)
+  static constexpr int GC = LPC > (32 / ESZ) ? LPC : (32 / ESZ);
+  static constexpr int GCP = GC + 1;
+  static constexpr int TILE_C = N * GCP;
+  // forward pass 2 / final rows: rows per item (~128 KB of output)
+  static constexpr int RP2_ = (131072 / (N * ESZ)) > LPR ? (131072 / (N * ESZ)) : LPR;
+  static constexpr int RP2 = RP2_ < N ? RP2_ : N;
+  // inverse pass 1: rows per tile and per item
+  static constexpr int GR_ = LPR > (32 / ESZ) ? LPR : (32 / ESZ);
+  static constexpr int GR = GR_ < N ? GR_ : N;
+  static constexpr int TSTR = H + 2;
+  static constexpr int TILE_R = GR * TSTR;
+  static constexpr int RPI_ = (N / 16) > GR ? (N / 16) : GR;
+  static constexpr int RPI = RPI_ < N ? RPI_ : N;
+  // padded row stride of the final column pass output
+  static constexpr int NCPF = ((H + 1 + GC - 1) / GC) * GC;
+  static constexpr size_t SMEM_FWD = (size_t)((SCR_C + TILE_C) > SCR_R ? (SCR_C + TILE_C) : SCR_R) * ESZ;
+  static constexpr size_t SMEM_INV = (size_t)((SCR_R + TILE_R) > SCR_C ? (SCR_R + TILE_R) : SCR_C) * ESZ + 256;
+  static constexpr size_t SMEM_AUX = SMEM_FWD > SMEM_INV ? SMEM_FWD : SMEM_INV;
+  static_assert(RPI % GR == 0, "RPI must be a multiple of GR");
+  static_assert(GC % LPC == 0 || LPC > GC, "GC vs LPC");
+};
+
+enum { MODE_MAIN = 0, MODE_AUX = 1 };
+
+template <typename T> __device__ __forceinline__ void store_pair_cs(cpx<T>* dst, cpx<T> a, cpx<T> b);
+template <> __device__ __forceinline__ void store_pair_cs<float>(float2* dst, float2 a, float2 b) {
+  __stcs(reinterpret_cast<float4*>(dst), make_float4(a.x, a.y, b.x, b.y));
+}
+template <> __device__ __forceinline__ void store_pair_cs<double>(double2* dst, double2 a, double2 b) {
+  __stcs(dst, a);
+  __stcs(dst + 1, b);
+}
+template <typename T> __device__ __forceinline__ void load_pair_cs(const cpx<T>* src, cpx<T>& a, cpx<T>& b);
+template <> __device__ __forceinline__ void load_pair_cs<float>(const float2* src, float2& a, float2& b) {
+  const float4 v = __ldcs(reinterpret_cast<const float4*>(src));
+  a = make_float2(v.x, v.y);
+  b = make_float2(v.z, v.w);
+}
+template <> __device__ __forceinline__ void load_pair_cs<double>(const double2* src, double2& a, double2& b) {
+  a = __ldcs(src);
+  b = __ldcs(src + 1);
+}
+
+__device__ __forceinline__ void spin_wait(const int* ctr, int target) {
+  const volatile int* v = ctr;
+  while (*v < target) __nanosleep(40);
+  __threadfence();
+}
+
+template <typename T, int N>
+struct K {
+  using G = Geo<T, N>;
+  using C = cpx<T>;
+  static constexpr int H = N / 2;
+  static constexpr int NT = G::NT;
+
+  // ------------------------------------------------------------------ column IFFT item
+  // MAIN: forward pass 1 — column bins [c0, c0+cnt) of plane P: X(u) = sym_P(u) F(u),
+  //       IFFT along u2, rows -> W (row-major, stride P.ncols_pad, column c - P.c_lo).
+  // AUX:  final pass 1 — column bins of A[b] (no window) -> Fscr[b] (row-major, stride NCPF).
+  template <int MODE>
+  static __device__ void col_ifft(const KParams& p, int b, const PlaneDev& P, int c0, int cnt,
+                                  const C* __restrict__ src, C* dst, int dst_stride, int dst_col0,
+                                  C* smem) {
+    C* scr = smem;
+    C* tile = smem + G::SCR_C;
+    const int tid = threadIdx.x, line = tid / G::THC, t = tid % G::THC;
+    const C* tw = static_cast<const C*>(p.tw);
+    const T delta = (T)p.delta;
+    constexpr int ROUNDS = G::GC / G::LPC > 0 ? G::GC / G::LPC : 1;
+#pragma unroll 1
+    for (int rd = 0; rd < ROUNDS; ++rd) {
+      const int ci = rd * G::LPC + line;
+      const bool act = ci < cnt;
+      const int cb = c0 + ci;
+      const int u1 = cb == H ? -H : cb;
+      const C* col = src + (size_t)cb * N;
+      C r[G::EC];
+#pragma unroll
+      for (int q = 0; q < G::EC; ++q) {
+        const int rb = t + q * G::THC;
+        if constexpr (MODE == MODE_MAIN) {
+          const T w = act ? window_sym<T>(P, u1, centred(rb, N), H, delta) : T(0);
+          r[q] = w != T(0) ? cscale<T>(__ldg(col + rb), w) : czero<T>();
+        } else {
+          r[q] = act ? __ldcg(col + rb) : czero<T>();
+        }
+      }
+      LineFFT<T, N, true, N>::run(r, scr + line * G::SMC, t, tw);
+      if (ci < G::GC) {
+#pragma unroll
+        for (int q = 0; q < G::EC; ++q) tile[(t + q * G::THC) * G::GCP + ci] = r[q];
+      }
+      __syncthreads();
+    }
+    const int ncopy = cnt < G::GC ? cnt : G::GC;
+#pragma unroll 1
+    for (int e = tid; e < N * G::GC; e += NT) {
+      const int rr = e / G::GC, ci = e - rr * G::GC;
+      if (ci < ncopy) dst[(size_t)rr * dst_stride + dst_col0 + ci] = tile[rr * G::GCP + ci];
+    }
+  }
+
+  // ------------------------------------------------------------------ row C2R item
+  // Rows [r0, r0+cnt) of an intermediate holding Hermitian-half bins [c_lo, c_lo+ncols)
+  // (row-major, stride `stride`).  MAIN: complex coefficient rows (+ Nyquist imaginary
+  // term); AUX: real image rows minus the adjoint's Nyquist correction.
+  template <int MODE>
+  static __device__ void row_c2r(const KParams& p, const C* __restrict__ src, int stride, int c_lo, int ncols,
+                                 int r0, int cnt, C* out_c, T* out_r, const T* nyqG, const T* nyqH,
+                                 C* smem) {
+    C* scr = smem;
+    const int tid = threadIdx.x, line = tid / G::THR, t = tid % G::THR;
+    const C* tw = static_cast<const C*>(p.tw);
+    const T scale = T(1) / (T(N) * T(N));
+    constexpr int ROUNDS = G::RP2 / G::LPR > 0 ? G::RP2 / G::LPR : 1;
+#pragma unroll 1
+    for (int rd = 0; rd < ROUNDS; ++rd) {
+      const int ri = rd * G::LPR + line;
+      const bool act = ri < cnt;
+      const int r = r0 + ri;
+      const C* row = src + (size_t)r * stride - c_lo;
+      C z[G::ER];
+#pragma unroll
+      for (int q = 0; q < G::ER; ++q) {
+        const int k = t + q * G::THR, km = H - k;
+        const C xk = (act && k >= c_lo && k < c_lo + ncols) ? __ldcg(row + k) : czero<T>();
+        const C xm = (act && km >= c_lo && km < c_lo + ncols) ? __ldcg(row + km) : czero<T>();
+        const C a = mk<T>(xk.x + xm.x, xk.y - xm.y);      // xk + conj(xm)
+        const C d = mk<T>(xk.x - xm.x, xk.y + xm.y);      // xk - conj(xm)
+        const C e = cmulc<T>(d, __ldg(tw + k));            // d * exp(+2 pi i k / N)
+        z[q] = mk<T>(a.x - e.y, a.y + e.x);                 // a + i e
+      }
+      LineFFT<T, H, true, N>::run(z, scr + line * G::SMR, t, tw);
+      if (act) {
+        const T sr = (r & 1) ? T(-1) : T(1);
+#pragma unroll
+        for (int q = 0; q < G::ER; ++q) {
+          const int m1 = 2 * (t + q * G::THR);
+          const T x0 = z[q].x * scale, x1 = z[q].y * scale;
+          if constexpr (MODE == MODE_MAIN) {
+            T i0 = T(0), i1 = T(0);
+            if (nyqG != nullptr) {
+              const T hr = nyqH[r];
+              i0 = sr * nyqG[m1] + hr;
+              i1 = sr * nyqG[m1 + 1] - hr;
+            }
+            store_pair_cs<T>(out_c + (size_t)r * N + m1, mk<T>(x0, i0), mk<T>(x1, i1));
+          } else {
+            T c0 = T(0), c1 = T(0);
+            if (nyqG != nullptr) {
+              const T hr = nyqH[r];
+              c0 = sr * nyqG[m1] + hr;
+              c1 = sr * nyqG[m1 + 1] - hr;
+            }
+            cpx<T> v = mk<T>(x0 - c0, x1 - c1);
+            *reinterpret_cast<cpx<T>*>(out_r + (size_t)r * N + m1) = v;
+          }
+        }
+      }
+      SyncOf<G::THR>::sync();
+    }
+  }
+
+  // ------------------------------------------------------------------ row R2C item
+  // Rows [r0, r0+cnt): MAIN reads Re of a coefficient plane (and, for Nyquist planes,
+  // the alternating sums of Im); AUX reads a real image.  R2C along m1, keeps bins
+  // [c_lo, c_lo+ncols) -> dst column-major (dst[(k - c_lo) * N + r]).
+  template <int MODE>
+  static __device__ void row_r2c(const KParams& p, const C* __restrict__ src_c, const T* __restrict__ src_r,
+                                 int c_lo, int ncols, int r0, int cnt, C* dst, int nyq_b, int nyq_idx,
+                                 int nyq_group, C* smem) {
+    C* scr = smem;
+    C* tile = smem + G::SCR_R;
+    const int tid = threadIdx.x, line = tid / G::THR, t = tid % G::THR;
+    const C* tw = static_cast<const C*>(p.tw);
+    const bool nyq = MODE == MODE_MAIN && nyq_idx >= 0;
+    T sacc[G::ER][2];
+#pragma unroll
+    for (int q = 0; q < G::ER; ++q) sacc[q][0] = sacc[q][1] = T(0);
+    constexpr int ROUNDS = G::GR / G::LPR > 0 ? G::GR / G::LPR : 1;
+    const int ntiles = (cnt + G::GR - 1) / G::GR;
+#pragma unroll 1
+    for (int ti = 0; ti < ntiles; ++ti) {
+      const int rt0 = r0 + ti * G::GR;
+#pragma unroll 1
+      for (int rd = 0; rd < ROUNDS; ++rd) {
+        const int ri = rd * G::LPR + line;              // row inside the tile
+        const bool act = ri < G::GR && ti * G::GR + ri < cnt;
+        const int r = rt0 + ri;
+        C z[G::ER];
+        T trow = T(0);
+        const T sr = (r & 1) ? T(-1) : T(1);
+#pragma unroll
+        for (int q = 0; q < G::ER; ++q) {
+          const int m1 = 2 * (t + q * G::THR);
+          if (act) {
+            if constexpr (MODE == MODE_MAIN) {
+              C v0, v1;
+              load_pair_cs<T>(src_c + (size_t)r * N + m1, v0, v1);
+              z[q] = mk<T>(v0.x, v1.x);
+              if (nyq) {
+                sacc[q][0] += sr * v0.y;
+                sacc[q][1] += sr * v1.y;
+                trow += v0.y - v1.y;
+              }
+            } else {
+              const cpx<T> v = *reinterpret_cast<const cpx<T>*>(src_r + (size_t)r * N + m1);
+              z[q] = v;
+            }
+          } else {
+            z[q] = czero<T>();
+          }
+        }
+        LineFFT<T, H, false, N>::run(z, scr + line * G::SMR, t, tw);
+        if (nyq) {
+          // alternating row sum t(r) = sum_m1 (-1)^m1 Im c(r, m1), reduced over the line
+          T v = trow;
+#pragma unroll
+          for (int o = (G::THR < 32 ? G::THR : 32) / 2; o > 0; o >>= 1) v += __shfl_xor_sync(0xffffffffu, v, o);
+          if constexpr (G::THR > 32) {
+            T* red = reinterpret_cast<T*>(tile + G::TILE_R);   // NT/32 scalars past the tile
+            __syncthreads();
+            if ((tid & 31) == 0) red[tid >> 5] = v;
+            __syncthreads();
+            if (t == 0) {
+              v = T(0);
+              for (int w = 0; w < G::THR / 32; ++w) v += red[(line * G::THR) / 32 + w];
+            }
+          }
+          if (t == 0 && act)
+            static_cast<T*>(p.nyq_T)[((size_t)nyq_b * p.n_nyq + nyq_idx) * N + r] = v;
+        }
+        C* sl = scr + line * G::SMR;
+        SyncOf<G::THR>::sync();
+#pragma unroll
+        for (int q = 0; q < G::ER; ++q) sl[Pad<T>::at(t + q * G::THR)] = z[q];
+        SyncOf<G::THR>::sync();
+        if (act) {
+#pragma unroll 1
+          for (int kk = t; kk < ncols; kk += G::THR) {
+            const int k = c_lo + kk;                         // 0..H
+            const C zk = sl[Pad<T>::at(k == H ? 0 : k)];
+            const C zm = sl[Pad<T>::at(k == 0 ? 0 : H - k)];
+            const C a = mk<T>(zk.x + zm.x, zk.y - zm.y);    // Z[k] + conj(Z[H-k])
+            const C d = mk<T>(zk.x - zm.x, zk.y + zm.y);    // Z[k] - conj(Z[H-k])
+            const C e = cmul<T>(d, __ldg(tw + k));           // W^k d
+            tile[ri * G::TSTR + kk] = mk<T>(T(0.5) * (a.x + e.y), T(0.5) * (a.y - e.x));   // (a - i e)/2
+          }
+        }
+        SyncOf<G::THR>::sync();
+      }
+      __syncthreads();
+      const int rows_here = cnt - ti * G::GR < G::GR ? cnt - ti * G::GR : G::GR;
+#pragma unroll 1
+      for (int e = tid; e < ncols * G::GR; e += NT) {
+        const int kk = e / G::GR, ri = e - kk * G::GR;
+        if (ri < rows_here) dst[(size_t)kk * N + rt0 + ri] = tile[ri * G::TSTR + kk];
+      }
+      __syncthreads();
+    }
+    if (nyq) {
+      // partial alternating column sums s(m1) = sum_r (-1)^r Im c(r, m1) over this item's rows
+      T* red = reinterpret_cast<T*>(scr);                  // [LPR][N] scalars (fits SCR_R)
+#pragma unroll
+      for (int q = 0; q < G::ER; ++q) {
+        const int m1 = 2 * (t + q * G::THR);
+        red[line * N + m1] = sacc[q][0];
+        red[line * N + m1 + 1] = sacc[q][1];
+      }
+      __syncthreads();
+      T* outp = static_cast<T*>(p.nyq_S) + (((size_t)nyq_b * p.n_nyq + nyq_idx) * p.n_rowitems + nyq_group) * N;
+#pragma unroll 1
+      for (int m = tid; m < N; m += NT) {
+        T s = T(0);
+        for (int l = 0; l < G::LPR; ++l) s += red[l * N + m];
+        outp[m] = s;
+      }
+      __syncthreads();
+    }
+  }
+
+  // ------------------------------------------------------------------ column FFT items
+  // inverse pass 2: columns [g0, g0+LPC) of image b over the planes of one chunk:
+  // FFT along r of W, * sym_i, summed over planes, written / accumulated into A[b].
+  static __device__ void col_fft_acc(const KParams& p, const ItemDev& I, const ChunkDev& Ch, C* smem) {
+    C* scr = smem;
+    const int tid = threadIdx.x, line = tid / G::THC, t = tid % G::THC;
+    const C* tw = static_cast<const C*>(p.tw);
+    const T delta = (T)p.delta;
+    const int g0 = I.group * G::LPC;
+    const int g1 = g0 + G::LPC < H + 1 ? g0 + G::LPC : H + 1;
+    const int cb = g0 + line;
+    const bool act = cb <= H;
+    const int u1 = cb == H ? -H : cb;
+    const C* slot = static_cast<const C*>(p.W) + (size_t)Ch.slot * p.slot_elems;
+    C acc[G::EC];
+#pragma unroll
+    for (int q = 0; q < G::EC; ++q) acc[q] = czero<T>();
+#pragma unroll 1
+    for (int u = Ch.unit0; u < Ch.unit0 + Ch.nunits; ++u) {
+      const UnitDev U = p.units[u];
+      const PlaneDev P = p.planes[U.p];
+      if (g1 <= P.c_lo || g0 >= P.c_lo + P.ncols) continue;          // CTA-uniform
+      const bool in = act && cb >= P.c_lo && cb < P.c_lo + P.ncols;
+      const C* col = slot + U.woff + (size_t)(cb - P.c_lo) * N;
+      C r[G::EC];
+#pragma unroll
+      for (int q = 0; q < G::EC; ++q) r[q] = in ? __ldcg(col + t + q * G::THC) : czero<T>();
+      LineFFT<T, N, false, N>::run(r, scr + line * G::SMC, t, tw);
+      if (in) {
+#pragma unroll
+        for (int q = 0; q < G::EC; ++q) {
+          const T w = window_sym<T>(P, u1, centred(t + q * G::THC, N), H, delta);
+          acc[q].x += w * r[q].x;
+          acc[q].y += w * r[q].y;
+        }
+      }
+      SyncOf<G::THC>::sync();
+    }
+    if (act) {
+      C* a = static_cast<C*>(p.A) + ((size_t)Ch.b * (H + 1) + cb) * N;
+#pragma unroll
+      for (int q = 0; q < G::EC; ++q) {
+        const int idx = t + q * G::THC;
+        if (Ch.first_of_image) {
+          a[idx] = acc[q];
+        } else {
+          const C o = __ldcg(a + idx);
+          a[idx] = mk<T>(o.x + acc[q].x, o.y + acc[q].y);
+        }
+      }
+    }
+  }
+
+  // spectrum pass 2: columns of Fscr[b] (column-major) -> F[b] (plain FFT along r)
+  static __device__ void col_fft_plain(const KParams& p, int b, int g, C* smem) {
+    C* scr = smem;
+    const int tid = threadIdx.x, line = tid / G::THC, t = tid % G::THC;
+    const C* tw = static_cast<const C*>(p.tw);
+    const int cb = g * G::LPC + line;
+    const bool act = cb <= H;
+    const C* col = static_cast<const C*>(p.Fscr) + ((size_t)b * (H + 1) + cb) * N;
+    C r[G::EC];
+#pragma unroll
+    for (int q = 0; q < G::EC; ++q) r[q] = act ? col[t + q * G::THC] : czero<T>();
+    LineFFT<T, N, false, N>::run(r, scr + line * G::SMC, t, tw);
+    if (act) {
+      C* f = static_cast<C*>(p.F) + ((size_t)b * (H + 1) + cb) * N;
+#pragma unroll
+      for (int q = 0; q < G::EC; ++q) f[t + q * G::THC] = r[q];
+    }
+  }
+
+  // ------------------------------------------------------------------ persistent kernels
+  static __device__ void fwd_item(const KParams& p, const ItemDev& I, C* smem) {
+    const UnitDev U = p.units[I.unit];
+    const PlaneDev P = p.planes[U.p];
+    const ChunkDev& Ch = p.chunks[I.chunk];
+    C* w = static_cast<C*>(p.W) + (size_t)Ch.slot * p.slot_elems + U.woff;
+    if (I.type == 0) {
+      const int c0 = P.c_lo + I.group * G::GC;
+      const int rem = P.c_lo + P.ncols - c0;
+      const C* Fb = static_cast<const C*>(p.F) + (size_t)U.b * (H + 1) * N;
+      col_ifft<MODE_MAIN>(p, U.b, P, c0, rem < G::GC ? rem : G::GC, Fb, w, P.ncols_pad, c0 - P.c_lo, smem);
+    } else {
+      const int r0 = I.group * G::RP2;
+      const int cnt = N - r0 < G::RP2 ? N - r0 : G::RP2;
+      const T* nyqG = nullptr;
+      const T* nyqH = nullptr;
+      if (P.nyq >= 0) {
+        nyqG = static_cast<const T*>(p.nyq_fwd) + ((size_t)U.b * p.n_nyq + P.nyq) * 2 * N;
+        nyqH = nyqG + N;
+      }
+      C* out = static_cast<C*>(p.coeff) + ((size_t)U.b * p.eta_l + U.p) * N * N;
+      row_c2r<MODE_MAIN>(p, w, P.ncols_pad, P.c_lo, P.ncols, r0, cnt, out, nullptr, nyqG, nyqH, smem);
+    }
+  }
+
+  static __device__ void inv_item(const KParams& p, const ItemDev& I, C* smem) {
+    const ChunkDev& Ch = p.chunks[I.chunk];
+    if (I.type == 0) {
+      const UnitDev U = p.units[I.unit];
+      const PlaneDev P = p.planes[U.p];
+      C* w = static_cast<C*>(p.W) + (size_t)Ch.slot * p.slot_elems + U.woff;
+      const int r0 = I.group * G::RPI;
+      const int cnt = N - r0 < G::RPI ? N - r0 : G::RPI;
+      const C* src = static_cast<const C*>(p.coeff) + ((size_t)U.b * p.eta_l + U.p) * N * N;
+      row_r2c<MODE_MAIN>(p, src, nullptr, P.c_lo, P.ncols, r0, cnt, w, U.b, P.nyq, I.group, smem);
+    } else {
+      col_fft_acc(p, I, Ch, smem);
+    }
+  }
+};
+
+template <typename T, int N>
+__global__ void __launch_bounds__(256) fwd_main_kernel(KParams p) {
+  extern __shared__ __align__(16) unsigned char smem_raw[];
+  cpx<T>* smem = reinterpret_cast<cpx<T>*>(smem_raw);
+  __shared__ int s_item;
+  for (;;) {
+    if (threadIdx.x == 0) s_item = atomicAdd(p.ctr, 1);
+    __syncthreads();
+    const int it = s_item;
+    if (it >= p.n_items) break;
+    const ItemDev I = p.items[it];
+    if (threadIdx.x == 0) {
+      const ChunkDev& Ch = p.chunks[I.chunk];
+      if (I.type == 0) {
+        if (Ch.prev_slot_chunk >= 0)
+          spin_wait(p.ctr + p.ctr_p2 + Ch.prev_slot_chunk, p.chunks[Ch.prev_slot_chunk].p2_items);
+      } else {
+        spin_wait(p.ctr + p.ctr_p1 + I.chunk, Ch.p1_items);
+      }
+    }
+    __syncthreads();
+    K<T, N>::fwd_item(p, I, smem);
+    __syncthreads();
+    if (threadIdx.x == 0) {
+      __threadfence();
+      atomicAdd(p.ctr + (I.type == 0 ? p.ctr_p1 : p.ctr_p2) + I.chunk, 1);
+    }
+  }
+}
+
+template <typename T, int N>
+__global__ void __launch_bounds__(256) inv_main_kernel(KParams p) {
+  extern __shared__ __align__(16) unsigned char smem_raw[];
+  cpx<T>* smem = reinterpret_cast<cpx<T>*>(smem_raw);
+  __shared__ int s_item;
+  for (;;) {
+    if (threadIdx.x == 0) s_item = atomicAdd(p.ctr, 1);
+    __syncthreads();
+    const int it = s_item;
+    if (it >= p.n_items) break;
+    const ItemDev I = p.items[it];
+    if (threadIdx.x == 0) {
+      const ChunkDev& Ch = p.chunks[I.chunk];
+      if (I.type == 0) {
+        if (Ch.prev_slot_chunk >= 0)
+          spin_wait(p.ctr + p.ctr_p2 + Ch.prev_slot_chunk, p.chunks[Ch.prev_slot_chunk].p2_items);
+      } else {
+        spin_wait(p.ctr + p.ctr_p1 + I.chunk, Ch.p1_items);
+        if (I.dep >= 0) spin_wait(p.ctr + p.ctr_g + I.dep, 1);
+      }
+    }
+    __syncthreads();
+    K<T, N>::inv_item(p, I, smem);
+    __syncthreads();
+    if (threadIdx.x == 0) {
+      __threadfence();
+      if (I.type == 0) {
+        atomicAdd(p.ctr + p.ctr_p1 + I.chunk, 1);
+      } else {
+        atomicAdd(p.ctr + p.ctr_g + I.self, 1);
+        atomicAdd(p.ctr + p.ctr_p2 + I.chunk, 1);
+      }
+    }
+  }
+}
+
+// ---------------------------------------------------------------------- auxiliary kernels
+
+// spectrum pass 1: rows of img[b] -> Fscr[b] column-major (all bins 0..H); grid (N/RPI, B)
+template <typename T, int N>
+__global__ void __launch_bounds__(256) spec_rows_kernel(KParams p) {
+  extern __shared__ __align__(16) unsigned char smem_raw[];
+  using G = Geo<T, N>;
+  const int b = blockIdx.y, g = blockIdx.x;
+  const int r0 = g * G::RPI;
+  const int cnt = N - r0 < G::RPI ? N - r0 : G::RPI;
+  const T* src = static_cast<const T*>(p.img) + (size_t)b * N * N;
+  cpx<T>* dst = static_cast<cpx<T>*>(p.Fscr) + (size_t)b * (N / 2 + 1) * N;
+  K<T, N>::template row_r2c<MODE_AUX>(p, nullptr, src, 0, N / 2 + 1, r0, cnt, dst, b, -1, 0,
+                                      reinterpret_cast<cpx<T>*>(smem_raw));
+}
+
+// spectrum pass 2: grid (ceil((H+1)/LPC), B)
+template <typename T, int N>
+__global__ void __launch_bounds__(256) spec_cols_kernel(KParams p) {
+  extern __shared__ __align__(16) unsigned char smem_raw[];
+  K<T, N>::col_fft_plain(p, blockIdx.y, blockIdx.x, reinterpret_cast<cpx<T>*>(smem_raw));
+}
+
+// final pass 1: columns of A[b] -> Fscr[b] row-major (stride NCPF); grid (ceil((H+1)/GC), B)
+template <typename T, int N>
+__global__ void __launch_bounds__(256) fin_cols_kernel(KParams p) {
+  extern __shared__ __align__(16) unsigned char smem_raw[];
+  using G = Geo<T, N>;
+  const int b = blockIdx.y;
+  const int c0 = blockIdx.x * G::GC;
+  const int rem = N / 2 + 1 - c0;
+  const cpx<T>* src = static_cast<const cpx<T>*>(p.A) + (size_t)b * (N / 2 + 1) * N;
+  cpx<T>* dst = static_cast<cpx<T>*>(p.Fscr) + (size_t)b * N * G::NCPF;
+  PlaneDev dummy{};
+  K<T, N>::template col_ifft<MODE_AUX>(p, b, dummy, c0, rem < G::GC ? rem : G::GC, src, dst, G::NCPF, c0,
+                                       reinterpret_cast<cpx<T>*>(smem_raw));
+}
+
+// final pass 2: rows of Fscr[b] -> img_out[b] minus the Nyquist correction; grid (N/RP2, B)
+template <typename T, int N>
+__global__ void __launch_bounds__(256) fin_rows_kernel(KParams p) {
+  extern __shared__ __align__(16) unsigned char smem_raw[];
+  using G = Geo<T, N>;
+  const int b = blockIdx.y;
+  const int r0 = blockIdx.x * G::RP2;
+  const int cnt = N - r0 < G::RP2 ? N - r0 : G::RP2;
+  const cpx<T>* src = static_cast<const cpx<T>*>(p.Fscr) + (size_t)b * N * G::NCPF;
+  T* out = static_cast<T*>(p.img_out) + (size_t)b * N * N;
+  const T* cg = nullptr;
+  const T* ch = nullptr;
+  if (p.n_nyq > 0) {
+    cg = static_cast<const T*>(p.corr) + (size_t)b * 2 * N;
+    ch = cg + N;
+  }
+  K<T, N>::template row_c2r<MODE_AUX>(p, src, G::NCPF, 0, N / 2 + 1, r0, cnt, nullptr, out, cg, ch,
+                                      reinterpret_cast<cpx<T>*>(smem_raw));
+}
+
+// forward Nyquist terms: grid (n_nyq, 2, B).  which = 0: G(m1) from the Nyquist row,
+// which = 1: H(r) from the Nyquist column.
+template <typename T, int N>
+__global__ void __launch_bounds__(256) nyq_fwd_kernel(KParams p) {
+  extern __shared__ __align__(16) unsigned char smem_raw[];
+  using G = Geo<T, N>;
+  using C = cpx<T>;
+  constexpr int H = N / 2;
+  const int nq = blockIdx.x, which = blockIdx.y, b = blockIdx.z;
+  const PlaneDev P = p.planes[p.nyq_planes[nq]];
+  const int tid = threadIdx.x, line = tid / G::THC, t = tid % G::THC;
+  const C* F = static_cast<const C*>(p.F) + (size_t)b * (H + 1) * N;
+  const T delta = (T)p.delta;
+  C r[G::EC];
+#pragma unroll
+  for (int q = 0; q < G::EC; ++q) {
+    const int bin = t + q * G::THC;
+    C v = czero<T>();
+    if (line == 0) {
+      const int u = centred(bin, N);
+      if (which == 0) {
+        const T a = window_anti<T>(P, u, -H, H, delta);
+        if (a != T(0)) v = cscale<T>(bin <= H ? F[(size_t)bin * N + H] : conj_<T>(F[(size_t)(N - bin) * N + H]), a);
+      } else {
+        const T a = window_anti<T>(P, -H, u, H, delta);
+        if (a != T(0)) v = cscale<T>(F[(size_t)H * N + bin], a);
+      }
+    }
+    r[q] = v;
+  }
+  LineFFT<T, N, true, N>::run(r, reinterpret_cast<C*>(smem_raw) + line * G::SMC, t, static_cast<const C*>(p.tw));
+  if (line == 0) {
+    T* out = static_cast<T*>(p.nyq_fwd) + (((size_t)b * p.n_nyq + nq) * 2 + which) * N;
+    const T s = T(1) / (T(N) * T(N));
+#pragma unroll
+    for (int q = 0; q < G::EC; ++q) out[t + q * G::THC] = r[q].y * s;
+  }
+}
+
+// inverse Nyquist correction: grid (2, B)
+template <typename T, int N>
+__global__ void __launch_bounds__(256) nyq_inv_kernel(KParams p) {
+  extern __shared__ __align__(16) unsigned char smem_raw[];
+  using G = Geo<T, N>;
+  using C = cpx<T>;
+  constexpr int H = N / 2;
+  const int which = blockIdx.x, b = blockIdx.y;
+  const int tid = threadIdx.x, line = tid / G::THC, t = tid % G::THC;
+  const C* tw = static_cast<const C*>(p.tw);
+  C* scr = reinterpret_cast<C*>(smem_raw) + line * G::SMC;
+  const T delta = (T)p.delta;
+  C acc[G::EC];
+#pragma unroll
+  for (int q = 0; q < G::EC; ++q) acc[q] = czero<T>();
+#pragma unroll 1
+  for (int nq = 0; nq < p.n_nyq; ++nq) {
+    const PlaneDev P = p.planes[p.nyq_planes[nq]];
+    C r[G::EC];
+#pragma unroll
+    for (int q = 0; q < G::EC; ++q) {
+      const int m = t + q * G::THC;
+      T s = T(0);
+      if (line == 0) {
+        if (which == 0) {
+          const T* ps = static_cast<const T*>(p.nyq_S) + ((size_t)b * p.n_nyq + nq) * p.n_rowitems * N + m;
+          for (int g = 0; g < p.n_rowitems; ++g) s += ps[(size_t)g * N];
+        } else {
+          s = static_cast<const T*>(p.nyq_T)[((size_t)b * p.n_nyq + nq) * N + m];
+        }
+      }
+      r[q] = mk<T>(s, T(0));
+    }
+    LineFFT<T, N, false, N>::run(r, scr, t, tw);
+#pragma unroll
+    for (int q = 0; q < G::EC; ++q) {
+      const int u = centred(t + q * G::THC, N);
+      const T a = which == 0 ? window_anti<T>(P, u, -H, H, delta) : window_anti<T>(P, -H, u, H, delta);
+      acc[q].x += a * r[q].x;
+      acc[q].y += a * r[q].y;
+    }
+    __syncthreads();
+  }
+  LineFFT<T, N, true, N>::run(acc, scr, t, tw);
+  if (line == 0) {
+    T* out = static_cast<T*>(p.corr) + ((size_t)b * 2 + which) * N;
+    const T s = T(1) / (T(N) * T(N));
+#pragma unroll
+    for (int q = 0; q < G::EC; ++q) out[t + q * G::THC] = acc[q].y * s;
+  }
+}
+
+// materialise spectra (tests only): psi[i][row][col], grid-stride
+template <typename T, int N>
+__global__ void spectra_kernel(KParams p, T* psi, int centred_layout) {
+  const size_t total = (size_t)p.eta_l * N * N;
+  const T delta = (T)p.delta;
+  for (size_t e = blockIdx.x * (size_t)blockDim.x + threadIdx.x; e < total; e += (size_t)gridDim.x * blockDim.x) {
+    const int i = (int)(e / ((size_t)N * N));
+    const int rem = (int)(e - (size_t)i * N * N);
+    const int row = rem / N, col = rem - row * N;
+    int u1, u2;
+    if (centred_layout) {
+      u1 = col - N / 2;
+      u2 = row - N / 2;
+    } else {
+      u1 = centred(col, N);
+      u2 = centred(row, N);
+    }
+    psi[e] = window<T>(p.planes[i], u1, u2, delta);
+  }
+}
+
+}  // namespace ffst

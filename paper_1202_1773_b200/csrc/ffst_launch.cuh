@@ -1,0 +1,120 @@
+// ffst_launch.cuh — host launchers: runtime n -> compile-time N dispatch.
+#pragma once
+#include "ffst_kernels.cuh"
+
+namespace ffst {
+
+template <typename T> struct MaxN;
+template <> struct MaxN<float> { static constexpr int v = 4096; };
+template <> struct MaxN<double> { static constexpr int v = 2048; };
+
+template <typename K>
+static cudaError_t set_smem(K kernel, size_t bytes) {
+  if (bytes <= 48 * 1024) return cudaSuccess;
+  return cudaFuncSetAttribute(kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)bytes);
+}
+
+#define FFST_CHECK(x) do { cudaError_t e_ = (x); if (e_ != cudaSuccess) return e_; } while (0)
+
+template <typename T, int N> struct Launch {
+  using G = Geo<T, N>;
+  static Geometry geometry() {
+    Geometry g;
+    g.nt = G::NT; g.gc = G::GC; g.rp2 = G::RP2; g.rpi = G::RPI; g.gr = G::GR; g.lpc = G::LPC;
+    g.smem_fwd = G::SMEM_FWD; g.smem_inv = G::SMEM_INV; g.smem_aux = G::SMEM_AUX;
+    return g;
+  }
+  static cudaError_t spectrum(const KParams& p, int batch, cudaStream_t s) {
+    FFST_CHECK(set_smem(spec_rows_kernel<T, N>, G::SMEM_INV));
+    spec_rows_kernel<T, N><<<dim3(N / G::RPI, batch), G::NT, G::SMEM_INV, s>>>(p);
+    FFST_CHECK(cudaGetLastError());
+    FFST_CHECK(set_smem(spec_cols_kernel<T, N>, G::SMEM_AUX));
+    spec_cols_kernel<T, N><<<dim3((N / 2 + 1 + G::LPC - 1) / G::LPC, batch), G::NT, G::SMEM_AUX, s>>>(p);
+    return cudaGetLastError();
+  }
+  static cudaError_t nyq_fwd(const KParams& p, int batch, cudaStream_t s) {
+    FFST_CHECK(set_smem(nyq_fwd_kernel<T, N>, G::SMEM_AUX));
+    nyq_fwd_kernel<T, N><<<dim3(p.n_nyq, 2, batch), G::NT, G::SMEM_AUX, s>>>(p);
+    return cudaGetLastError();
+  }
+  static cudaError_t fwd_main(const KParams& p, int grid, cudaStream_t s) {
+    FFST_CHECK(set_smem(fwd_main_kernel<T, N>, G::SMEM_FWD));
+    fwd_main_kernel<T, N><<<grid, G::NT, G::SMEM_FWD, s>>>(p);
+    return cudaGetLastError();
+  }
+  static cudaError_t inv_main(const KParams& p, int grid, cudaStream_t s) {
+    FFST_CHECK(set_smem(inv_main_kernel<T, N>, G::SMEM_INV));
+    inv_main_kernel<T, N><<<grid, G::NT, G::SMEM_INV, s>>>(p);
+    return cudaGetLastError();
+  }
+  static cudaError_t nyq_inv(const KParams& p, int batch, cudaStream_t s) {
+    FFST_CHECK(set_smem(nyq_inv_kernel<T, N>, G::SMEM_AUX));
+    nyq_inv_kernel<T, N><<<dim3(2, batch), G::NT, G::SMEM_AUX, s>>>(p);
+    return cudaGetLastError();
+  }
+  static cudaError_t final_(const KParams& p, int batch, cudaStream_t s) {
+    FFST_CHECK(set_smem(fin_cols_kernel<T, N>, G::SMEM_FWD));
+    fin_cols_kernel<T, N><<<dim3((N / 2 + 1 + G::GC - 1) / G::GC, batch), G::NT, G::SMEM_FWD, s>>>(p);
+    FFST_CHECK(cudaGetLastError());
+    FFST_CHECK(set_smem(fin_rows_kernel<T, N>, G::SMEM_FWD));
+    fin_rows_kernel<T, N><<<dim3((N + G::RP2 - 1) / G::RP2, batch), G::NT, G::SMEM_FWD, s>>>(p);
+    return cudaGetLastError();
+  }
+  static cudaError_t spectra(const KParams& p, void* psi, int centred, cudaStream_t s) {
+    const size_t total = (size_t)p.eta_l * N * N;
+    int grid = (int)((total + 255) / 256);
+    if (grid > 148 * 32) grid = 148 * 32;
+    if (grid < 1) grid = 1;
+    spectra_kernel<T, N><<<grid, 256, 0, s>>>(p, static_cast<T*>(psi), centred);
+    return cudaGetLastError();
+  }
+  static int max_active(int which) {
+    int nb = 0;
+    if (which == 0) {
+      if (set_smem(fwd_main_kernel<T, N>, G::SMEM_FWD) != cudaSuccess) return 0;
+      cudaOccupancyMaxActiveBlocksPerMultiprocessor(&nb, fwd_main_kernel<T, N>, G::NT, G::SMEM_FWD);
+    } else {
+      if (set_smem(inv_main_kernel<T, N>, G::SMEM_INV) != cudaSuccess) return 0;
+      cudaOccupancyMaxActiveBlocksPerMultiprocessor(&nb, inv_main_kernel<T, N>, G::NT, G::SMEM_INV);
+    }
+    return nb;
+  }
+};
+
+#define FFST_DISPATCH(T, n, CALL, FAIL)                                  \
+  switch (n) {                                                           \
+    case 4: return Launch<T, 4>::CALL;                                   \
+    case 8: return Launch<T, 8>::CALL;                                   \
+    case 16: return Launch<T, 16>::CALL;                                 \
+    case 32: return Launch<T, 32>::CALL;                                 \
+    case 64: return Launch<T, 64>::CALL;                                 \
+    case 128: return Launch<T, 128>::CALL;                               \
+    case 256: return Launch<T, 256>::CALL;                               \
+    case 512: return Launch<T, 512>::CALL;                               \
+    case 1024: return Launch<T, 1024>::CALL;                             \
+    case 2048: return Launch<T, 2048>::CALL;                             \
+    case 4096: if constexpr (MaxN<T>::v >= 4096) return Launch<T, (MaxN<T>::v >= 4096 ? 4096 : 2048)>::CALL; \
+      else return FAIL;                                                  \
+    default: return FAIL;                                                \
+  }
+
+#define FFST_INSTANTIATE(T)                                                                                    \
+  template <> Geometry geometry<T>(int n) { FFST_DISPATCH(T, n, geometry(), Geometry{}) }                      \
+  template <> cudaError_t launch_spectrum<T>(const KParams& p, int b, cudaStream_t s) {                        \
+    FFST_DISPATCH(T, p.n, spectrum(p, b, s), cudaErrorInvalidValue) }                                          \
+  template <> cudaError_t launch_nyq_fwd<T>(const KParams& p, int b, cudaStream_t s) {                         \
+    FFST_DISPATCH(T, p.n, nyq_fwd(p, b, s), cudaErrorInvalidValue) }                                           \
+  template <> cudaError_t launch_fwd_main<T>(const KParams& p, int g, cudaStream_t s) {                        \
+    FFST_DISPATCH(T, p.n, fwd_main(p, g, s), cudaErrorInvalidValue) }                                          \
+  template <> cudaError_t launch_inv_main<T>(const KParams& p, int g, cudaStream_t s) {                        \
+    FFST_DISPATCH(T, p.n, inv_main(p, g, s), cudaErrorInvalidValue) }                                          \
+  template <> cudaError_t launch_nyq_inv<T>(const KParams& p, int b, cudaStream_t s) {                         \
+    FFST_DISPATCH(T, p.n, nyq_inv(p, b, s), cudaErrorInvalidValue) }                                           \
+  template <> cudaError_t launch_final<T>(const KParams& p, int b, cudaStream_t s) {                           \
+    FFST_DISPATCH(T, p.n, final_(p, b, s), cudaErrorInvalidValue) }                                            \
+  template <> cudaError_t launch_spectra_export<T>(const KParams& p, void* psi, int c, cudaStream_t s) {       \
+    FFST_DISPATCH(T, p.n, spectra(p, psi, c, s), cudaErrorInvalidValue) }                                      \
+  template <> int max_active_main<T>(int n, int device, int which) {                                           \
+    (void)device; FFST_DISPATCH(T, n, max_active(which), 0) }
+
+}  // namespace ffst

@@ -1,0 +1,149 @@
+// ffst_math.cuh — complex helpers and the shearlet window psi_hat_i evaluated on
+// the fly from integer frequencies (product code; shares nothing with oracle/).
+//
+// The window is the paper's cone-adapted Meyer shearlet system (Sec. 2-3.5):
+//   v        eq:v
+//   psi1     eq:Psi1     closed form of Sec. 3.4
+//   psi2     eq:Psi2
+//   varphi   P:L696-703 and the cone low-pass eq:phi P:L705-711
+//   cones    P:L547-594; horizontal / vertical / glued seam P:L603-688
+//   sampling psi_hat(Delta * u) on the centred integer grid u.
+//
+// Integer formulation: with u = (u1, u2) integers
+// and Delta a power of two, the shear argument of a horizontal shearlet is
+//   2^j * w2/w1 + k = (k*u1 + 2^j*u2) / u1
+// so |arg| < 1  <=>  |k*u1 + 2^j*u2| < |u1|  is decided exactly in integers and
+// 1 - |arg| = (|u1| - |num|)/|u1| is a single rounded division.  The radial
+// argument 4^-j * Delta * |u1| is exact (powers of two).
+#pragma once
+#include <cuda_runtime.h>
+#include <math.h>
+
+#define FFST_HD __host__ __device__ __forceinline__
+
+namespace ffst {
+
+template <typename T> struct Cpx;
+template <> struct Cpx<float> { using type = float2; };
+template <> struct Cpx<double> { using type = double2; };
+template <typename T> using cpx = typename Cpx<T>::type;
+
+template <typename T> FFST_HD cpx<T> mk(T x, T y) { cpx<T> r; r.x = x; r.y = y; return r; }
+template <typename T> FFST_HD cpx<T> cadd(cpx<T> a, cpx<T> b) { return mk<T>(a.x + b.x, a.y + b.y); }
+template <typename T> FFST_HD cpx<T> csub(cpx<T> a, cpx<T> b) { return mk<T>(a.x - b.x, a.y - b.y); }
+template <typename T> FFST_HD cpx<T> cmul(cpx<T> a, cpx<T> b) {
+  return mk<T>(a.x * b.x - a.y * b.y, a.x * b.y + a.y * b.x);
+}
+// a * conj(b)
+template <typename T> FFST_HD cpx<T> cmulc(cpx<T> a, cpx<T> b) {
+  return mk<T>(a.x * b.x + a.y * b.y, a.y * b.x - a.x * b.y);
+}
+template <typename T> FFST_HD cpx<T> conj_(cpx<T> a) { return mk<T>(a.x, -a.y); }
+template <typename T> FFST_HD cpx<T> cscale(cpx<T> a, T s) { return mk<T>(a.x * s, a.y * s); }
+template <typename T> FFST_HD cpx<T> czero() { return mk<T>(T(0), T(0)); }
+
+// ---------------------------------------------------------------- window math
+
+template <typename T> FFST_HD T sinpi_(T x);
+template <typename T> FFST_HD T cospi_(T x);
+#ifdef __CUDA_ARCH__
+template <> FFST_HD float sinpi_<float>(float x) { return sinpif(x); }
+template <> FFST_HD float cospi_<float>(float x) { return cospif(x); }
+template <> FFST_HD double sinpi_<double>(double x) { return sinpi(x); }
+template <> FFST_HD double cospi_<double>(double x) { return cospi(x); }
+#else   // host planner (support / Nyquist classification only)
+template <> FFST_HD float sinpi_<float>(float x) { return (float)sin(3.14159265358979323846 * x); }
+template <> FFST_HD float cospi_<float>(float x) { return (float)cos(3.14159265358979323846 * x); }
+template <> FFST_HD double sinpi_<double>(double x) { return sin(3.14159265358979323846 * x); }
+template <> FFST_HD double cospi_<double>(double x) { return cos(3.14159265358979323846 * x); }
+#endif
+
+// Meyer's v on [0,1] (eq:v), reflected through v(x) = 1 - v(1-x) (Lemma P:L321-348)
+// for x > 1/2 so the polynomial is always evaluated where it is small.
+template <typename T> FFST_HD T meyer_v(T x) {
+  if (x <= T(0)) return T(0);
+  if (x >= T(1)) return T(1);
+  const bool refl = x > T(0.5);
+  const T y = refl ? T(1) - x : x;
+  const T y2 = y * y;
+  const T p = y2 * y2 * (T(35) + y * (T(-84) + y * (T(70) + y * T(-20))));
+  return refl ? T(1) - p : p;
+}
+
+// psi1_hat(a), a >= 0, closed form P:L1824-1835; sin(pi/2 v) = sinpi(v/2).
+template <typename T> FFST_HD T psi1_w(T a) {
+  if (a <= T(0.5) || a >= T(4)) return T(0);
+  if (a < T(1)) return sinpi_<T>(T(0.5) * meyer_v<T>(T(2) * a - T(1)));
+  if (a <= T(2)) return T(1);
+  return cospi_<T>(T(0.5) * meyer_v<T>(T(0.5) * a - T(1)));
+}
+
+// varphi(a), a >= 0
+template <typename T> FFST_HD T varphi_w(T a) {
+  if (a <= T(0.5)) return T(1);
+  if (a >= T(1)) return T(0);
+  return cospi_<T>(T(0.5) * meyer_v<T>(T(2) * a - T(1)));
+}
+
+// Plane descriptor shared by host planner and kernels.
+struct PlaneDev {
+  int gi;            // global 0-based flat index
+  int kind;          // 0 low-pass, 1 h, 2 v, 3 x (ffst_kind)
+  int j, k;          // scale, shear
+  int c_lo, ncols;   // Hermitian-half column range [c_lo, c_lo + ncols), columns 0..n/2
+  int ncols_pad;     // row stride of the forward intermediate
+  int nyq;           // index among the plan's Nyquist planes, or -1
+};
+
+// psi1_hat(4^-j Delta |ua|) psi2_hat((k ua + 2^j ub)/ua) for |ub| <= |ua| (cone shearlet,
+// P:L845-848); `rscale` = 4^-j * Delta.
+template <typename T> FFST_HD T cone_shearlet(int j, int k, int ua, int ub, T rscale) {
+  const int aa = ua < 0 ? -ua : ua;
+  if (aa == 0) return T(0);                              // reading A5: 0 on w_a = 0
+  const int num = k * ua + ub * (1 << j);                // exact (|num| < 2^24)
+  const int anum = num < 0 ? -num : num;
+  if (anum >= aa) return T(0);                           // |shear argument| >= 1 -> psi2 = 0
+  const T r = psi1_w<T>(rscale * T(aa));
+  if (r == T(0)) return T(0);
+  const T t = T(aa - anum) / T(aa);                      // 1 - |argument|, one rounding
+  return r * sqrt(meyer_v<T>(t));                        // psi2 = sqrt(v(1 - |x|))
+}
+
+// psi_hat_i(Delta u1, Delta u2) for integer u (u may be +n/2: the mirrored point).
+template <typename T> FFST_HD T window(const PlaneDev& P, int u1, int u2, T delta) {
+  const int a1 = u1 < 0 ? -u1 : u1, a2 = u2 < 0 ? -u2 : u2;
+  if (P.kind == 0) {                                     // eq:phi
+    return varphi_w<T>(delta * T(a2 <= a1 ? a1 : a2));
+  }
+  const T rs = delta * (T(1) / T(1 << (2 * P.j)));       // 4^-j Delta, exact
+  if (P.kind == 1) {                                     // horizontal cone |u2| < |u1|
+    return a2 < a1 ? cone_shearlet<T>(P.j, P.k, u1, u2, rs) : T(0);
+  }
+  if (P.kind == 2) {                                     // vertical cone |u1| < |u2|
+    return a1 < a2 ? cone_shearlet<T>(P.j, P.k, u2, u1, rs) : T(0);
+  }
+  // glued seam shearlet: h on C^h, v on C^v, horizontal formula on the seam |u1| = |u2|
+  if (a1 < a2) return cone_shearlet<T>(P.j, P.k, u2, u1, rs);
+  return cone_shearlet<T>(P.j, P.k, u1, u2, rs);
+}
+
+// Point-symmetric part of the sampled window on the even grid:
+// sym(u) = (w(u) + w(mirror u)) / 2 with w(mirror u) = psi(Delta u^), u^ = u with any
+// -n/2 component replaced by +n/2 (psi is even).  anti = (w(u) - w(u^)) / 2 lives on the
+// Nyquist row / column only.
+template <typename T> FFST_HD T window_sym(const PlaneDev& P, int u1, int u2, int half, T delta) {
+  const T w = window<T>(P, u1, u2, delta);
+  if (u1 != -half && u2 != -half) return w;
+  const int e1 = u1 == -half ? half : u1, e2 = u2 == -half ? half : u2;
+  return T(0.5) * (w + window<T>(P, e1, e2, delta));
+}
+template <typename T> FFST_HD T window_anti(const PlaneDev& P, int u1, int u2, int half, T delta) {
+  if (u1 != -half && u2 != -half) return T(0);
+  const int e1 = u1 == -half ? half : u1, e2 = u2 == -half ? half : u2;
+  return T(0.5) * (window<T>(P, u1, u2, delta) - window<T>(P, e1, e2, delta));
+}
+
+// natural FFT bin -> centred frequency in [-n/2, n/2)
+FFST_HD int centred(int bin, int n) { return bin < (n >> 1) ? bin : bin - n; }
+
+}  // namespace ffst

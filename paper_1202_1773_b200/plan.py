@@ -1,0 +1,194 @@
+"""Python face of the C ABI: ``Plan`` and the host-only queries.
+
+PyTorch provides device memory and streams; every step of the transform runs
+in libffst.so's kernels (include/ffst.h).  Names follow the paper's API
+(shearletTransformSpect / inverseShearletTransformSpect) and
+the boundary of SURVEY.md 8(b).
+"""
+from __future__ import annotations
+
+import ctypes as C
+
+import torch
+
+from ._lib import PlanDesc, check, lib
+
+KIND_NAMES = {0: "lowpass", 1: "h", 2: "v", 3: "x"}
+_DTYPES = {torch.float32: 0, torch.float64: 1}
+_CDTYPES = {torch.float32: torch.complex64, torch.float64: torch.complex128}
+
+
+def scales_for_size(n: int) -> int:
+    """j0 = floor(1/2 log2 n)."""
+    j0 = C.c_int()
+    check(lib.ffst_scales_for_size(int(n), C.byref(j0)), "ffst_scales_for_size")
+    return j0.value
+
+
+def num_shearlets(j0: int) -> int:
+    """eta = 2^(j0+2) - 3."""
+    return lib.ffst_num_shearlets(int(j0))
+
+
+def index_to_params(j0: int, index: int):
+    """0-based flat index -> (kind, j, k) (Sec. 3.5.1)."""
+    kind, j, k = C.c_int(), C.c_int(), C.c_int()
+    check(lib.ffst_index_to_params(int(j0), int(index), C.byref(kind), C.byref(j), C.byref(k)),
+          "ffst_index_to_params")
+    return kind.value, j.value, k.value
+
+
+def params_to_index(j0: int, kind: int, j: int, k: int) -> int:
+    i = C.c_int()
+    check(lib.ffst_params_to_index(int(j0), int(kind), int(j), int(k), C.byref(i)), "ffst_params_to_index")
+    return i.value
+
+
+def plane_support(n: int, index: int, j0: int = 0):
+    lo, hi = C.c_int(), C.c_int()
+    check(lib.ffst_plane_support(int(n), int(j0), int(index), C.byref(lo), C.byref(hi)), "ffst_plane_support")
+    return lo.value, hi.value
+
+
+def plane_is_nyquist(n: int, index: int, j0: int = 0) -> bool:
+    v = C.c_int()
+    check(lib.ffst_plane_is_nyquist(int(n), int(j0), int(index), C.byref(v)), "ffst_plane_is_nyquist")
+    return bool(v.value)
+
+
+def _stream_handle(stream, device):
+    if stream is None:
+        stream = torch.cuda.current_stream(device)
+    return C.c_void_p(stream.cuda_stream)
+
+
+class Plan:
+    """A forward/inverse FFST plan for n x n images on one CUDA device.
+
+    ``shard_rank``/``shard_count`` select the planes i (0-based) with
+    i % shard_count == shard_rank (eta-sharding)."""
+
+    def __init__(self, n: int, batch: int = 1, dtype=torch.float32, device=None, j0: int = 0,
+                 shard_rank: int = 0, shard_count: int = 1):
+        if not torch.cuda.is_available():
+            raise RuntimeError("FFST Plan needs a CUDA device (no CPU fallback)")
+        if dtype not in _DTYPES:
+            raise TypeError("dtype must be torch.float32 or torch.float64")
+        self.device = torch.device("cuda", torch.cuda.current_device() if device is None else
+                                   torch.device(device).index or 0)
+        self.dtype = dtype
+        self.cdtype = _CDTYPES[dtype]
+        desc = PlanDesc(int(n), int(j0), int(batch), _DTYPES[dtype], 0, self.device.index,
+                        int(shard_rank), int(shard_count))
+        handle = C.c_void_p()
+        with torch.cuda.device(self.device):
+            torch.cuda.init()
+            check(lib.ffst_plan_create(C.byref(handle), C.byref(desc)), "ffst_plan_create")
+        self._h = handle
+        vals = [C.c_int() for _ in range(5)]
+        check(lib.ffst_plan_info(self._h, *[C.byref(v) for v in vals]), "ffst_plan_info")
+        self.n, self.j0, self.eta, self.eta_local, self.batch = (v.value for v in vals)
+        idx = (C.c_int * self.eta_local)()
+        cnt = C.c_int()
+        check(lib.ffst_plan_local_planes(self._h, C.byref(cnt), idx), "ffst_plan_local_planes")
+        self.local_planes = list(idx)
+        self.shard_rank, self.shard_count = int(shard_rank), int(shard_count)
+
+    # -------------------------------------------------------------- buffers
+    def empty_coeffs(self, batch: int | None = None):
+        b = self.batch if batch is None else batch
+        return torch.empty((b, self.eta_local, self.n, self.n), dtype=self.cdtype, device=self.device)
+
+    def empty_images(self, batch: int | None = None):
+        b = self.batch if batch is None else batch
+        return torch.empty((b, self.n, self.n), dtype=self.dtype, device=self.device)
+
+    def _check_images(self, x):
+        if x.dim() == 2:
+            x = x.unsqueeze(0)
+        if x.dtype != self.dtype or x.device != self.device or x.shape[-2:] != (self.n, self.n):
+            raise ValueError(f"images must be {self.dtype} on {self.device} with shape (B, {self.n}, {self.n})")
+        if x.shape[0] > self.batch or x.shape[0] < 1:
+            raise ValueError(f"batch {x.shape[0]} outside 1..{self.batch}")
+        return x.contiguous()
+
+    # -------------------------------------------------------------- transforms
+    def forward(self, x, out=None, stream=None):
+        """Coefficient cube (B, eta_local, n, n) complex of images x (B, n, n)
+        (shearletTransformSpect, eq:shearletTransform)."""
+        x = self._check_images(x)
+        b = x.shape[0]
+        out = self.empty_coeffs(b) if out is None else out
+        if out.dtype != self.cdtype or not out.is_contiguous() or out.shape != (b, self.eta_local, self.n, self.n):
+            raise ValueError("bad output cube")
+        check(lib.ffst_sheartrans_batch(self._h, C.c_void_p(x.data_ptr()), C.c_void_p(out.data_ptr()), b,
+                                        _stream_handle(stream, self.device)), "ffst_sheartrans_batch")
+        return out
+
+    def inverse(self, c, out=None, stream=None):
+        """Re ifft2(sum_i psi_i fft2(c_i)) over the local planes (inverseShearletTransformSpect,
+        eq:inverseShearletTransform).  c: (B, eta_local, n, n) complex."""
+        if c.dim() == 3:
+            c = c.unsqueeze(0)
+        if c.dtype != self.cdtype or c.device != self.device or c.shape[1:] != (self.eta_local, self.n, self.n):
+            raise ValueError("bad coefficient cube")
+        c = c.contiguous()
+        b = c.shape[0]
+        if b < 1 or b > self.batch:
+            raise ValueError(f"batch {b} outside 1..{self.batch}")
+        out = self.empty_images(b) if out is None else out
+        check(lib.ffst_inversesheartrans_batch(self._h, C.c_void_p(c.data_ptr()), C.c_void_p(out.data_ptr()), b,
+                                               _stream_handle(stream, self.device)), "ffst_inversesheartrans_batch")
+        return out
+
+    def forward_host(self, x_host, out=None, stream=None):
+        """Forward from a host (ideally pinned) tensor; the H2D copy runs inside the C call."""
+        if x_host.device.type != "cpu" or x_host.dtype != self.dtype:
+            raise ValueError("host images of the plan dtype expected")
+        x_host = x_host.contiguous()
+        b = x_host.shape[0] if x_host.dim() == 3 else 1
+        out = self.empty_coeffs(b) if out is None else out
+        check(lib.ffst_sheartrans_host(self._h, C.c_void_p(x_host.data_ptr()), C.c_void_p(out.data_ptr()), b,
+                                       _stream_handle(stream, self.device)), "ffst_sheartrans_host")
+        return out
+
+    def inverse_host(self, c, out_host, stream=None):
+        """Inverse into a host (ideally pinned) tensor; the D2H copy runs inside the C call."""
+        b = c.shape[0]
+        check(lib.ffst_inversesheartrans_host(self._h, C.c_void_p(c.data_ptr()), C.c_void_p(out_host.data_ptr()), b,
+                                              _stream_handle(stream, self.device)), "ffst_inversesheartrans_host")
+        return out_host
+
+    def spectra(self, centred: bool = True, stream=None):
+        """The local spectra psi_hat_i as (eta_local, n, n) real (tests / diagnostics)."""
+        psi = torch.empty((self.eta_local, self.n, self.n), dtype=self.dtype, device=self.device)
+        check(lib.ffst_shearlet_spectra(self._h, C.c_void_p(psi.data_ptr()), int(bool(centred)),
+                                        _stream_handle(stream, self.device)), "ffst_shearlet_spectra")
+        return psi
+
+    # -------------------------------------------------------------- instrumentation
+    def set_timing(self, enable: bool = True):
+        check(lib.ffst_plan_set_timing(self._h, int(bool(enable))), "ffst_plan_set_timing")
+
+    def phase_times(self):
+        """(fwd_main_ms, inv_main_ms, fwd_total_ms, inv_total_ms), (fwd_launches, inv_launches)."""
+        t = (C.c_float * 4)()
+        n = (C.c_int * 2)()
+        check(lib.ffst_plan_phase_times(self._h, t, n), "ffst_plan_phase_times")
+        return tuple(t), tuple(n)
+
+    def workspace_bytes(self) -> int:
+        v = C.c_size_t()
+        check(lib.ffst_plan_workspace_bytes(self._h, C.byref(v)), "ffst_plan_workspace_bytes")
+        return v.value
+
+    def close(self):
+        if getattr(self, "_h", None):
+            lib.ffst_plan_destroy(self._h)
+            self._h = None
+
+    def __del__(self):
+        try:
+            self.close()
+        except Exception:
+            pass

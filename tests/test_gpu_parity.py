@@ -1,0 +1,259 @@
+"""GPU parity: the CUDA path (through the C ABI) against the float64 oracle on
+the same seeded inputs.
+
+Metric (reading A15, BASELINE.json tolerance): per-plane normwise
+relative error max|gpu - oracle| / max|oracle|, worst plane, must be <= 1e-4
+in float32 and <= 1e-10 in float64; the same on reconstructed images.
+"""
+import numpy as np
+import pytest
+import torch
+
+import oracle as O
+import synth
+
+pytestmark = pytest.mark.gpu
+
+TOL = {torch.float32: 1e-4, torch.float64: 1e-10}
+
+
+@pytest.fixture(scope="module")
+def F():
+    if not torch.cuda.is_available():
+        pytest.skip("no CUDA device")
+    import paper_1202_1773_b200 as mod
+    return mod
+
+
+def plane_err(g, o, floor_scale=1.0):
+    g = np.asarray(g)
+    o = np.asarray(o)
+    num = np.max(np.abs(g - o), axis=(-2, -1))
+    den = np.max(np.abs(o), axis=(-2, -1))
+    return np.where(den > 0, num / np.where(den > 0, den, 1.0), num / floor_scale)
+
+
+def images(cid, batch, n, dtype):
+    x = synth.make_batch(cid, batch=batch, n=n)
+    xt = torch.from_numpy(x).to(dtype)
+    return xt, xt.double().numpy()          # the oracle consumes the cast values
+
+
+# ------------------------------------------------------------------ spectra
+
+@pytest.mark.parametrize("n,dtype", [(64, torch.float64), (256, torch.float32), (16, torch.float64),
+                                     (4, torch.float64), (512, torch.float32)])
+def test_spectra_match_oracle(F, n, dtype):
+    plan = F.Plan(n, 1, dtype)
+    psi = plan.spectra(centred=True).cpu().double().numpy()
+    ref = O.shearlet_spectra(n)
+    tol = 1e-13 if dtype == torch.float64 else 2e-6
+    assert np.max(np.abs(psi - ref)) < tol
+    # frame tightness of the on-the-fly window (Fig. frameTightness)
+    assert np.max(np.abs(np.sum(psi**2, axis=0) - 1.0)) < (1e-13 if dtype == torch.float64 else 1e-5)
+
+
+# ------------------------------------------------------------------ forward / inverse, small sizes
+
+@pytest.mark.parametrize("n", [4, 8, 16, 32, 64, 128])
+@pytest.mark.parametrize("dtype", [torch.float64, torch.float32])
+def test_forward_inverse_small(F, n, dtype):
+    batch = 3
+    x, xo = images(2, batch, n, dtype)
+    plan = F.Plan(n, batch, dtype)
+    c = plan.forward(x.cuda())
+    rec = plan.inverse(c)
+    torch.cuda.synchronize()
+    c = c.cpu().numpy()
+    rec = rec.cpu().numpy()
+    psi = O.shearlet_spectra(n)
+    for b in range(batch):
+        ref = O.forward(xo[b], psi=psi)
+        assert plane_err(c[b], ref, np.max(np.abs(xo[b]))).max() <= TOL[dtype], (n, b)
+        # inverse of the GPU cube vs the oracle's inverse of the same cube (adjoint on its input)
+        ref_inv = O.inverse(c[b].astype(np.complex128), psi=psi).real
+        assert plane_err(rec[b], ref_inv).max() <= TOL[dtype]
+        # exactness
+        assert plane_err(rec[b], xo[b]).max() <= TOL[dtype]
+
+
+def test_config1_float64(F):
+    # BASELINE.json configs[0]: 64x64 float64 single image, forward then inverse, 1e-10
+    x, xo = images(1, 1, 64, torch.float64)
+    plan = F.Plan(64, 1, torch.float64)
+    c = plan.forward(x.cuda())
+    rec = plan.inverse(c)
+    ref = O.forward(xo[0])
+    assert plane_err(c.cpu().numpy()[0], ref).max() <= 1e-10
+    assert plane_err(rec.cpu().numpy()[0], xo[0]).max() <= 1e-10
+    assert np.max(np.abs(rec.cpu().numpy()[0] - xo[0])) < 1e-12
+
+
+@pytest.mark.parametrize("dtype", [torch.float64, torch.float32])
+def test_inverse_random_cube_adjoint(F, dtype):
+    # the inverse on cubes outside the range of the forward (adjoint identity)
+    n, batch = 64, 2
+    plan = F.Plan(n, batch, dtype)
+    z = synth.random_cube((batch, plan.eta, n, n), 7)
+    zt = torch.from_numpy(z).to(plan.cdtype)
+    zo = zt.to(torch.complex128).numpy()
+    rec = plan.inverse(zt.cuda()).cpu().numpy()
+    psi = O.shearlet_spectra(n)
+    for b in range(batch):
+        ref = O.inverse(zo[b], psi=psi).real
+        assert plane_err(rec[b], ref).max() <= TOL[dtype]
+    # Re <T f, Z> = <f, T* Z>
+    x, xo = images(2, batch, n, dtype)
+    c = plan.forward(x.cuda()).cpu().numpy().astype(np.complex128)
+    lhs = np.real(np.sum(c * np.conj(zo)))
+    rhs = np.sum(xo * rec)
+    assert abs(lhs - rhs) <= (1e-9 if dtype == torch.float64 else 1e-4) * abs(lhs)
+
+
+def test_constant_image(F):
+    n = 64
+    plan = F.Plan(n, 1, torch.float64)
+    c = plan.forward(torch.full((1, n, n), 0.7, dtype=torch.float64, device="cuda")).cpu().numpy()[0]
+    assert np.max(np.abs(c[0] - 0.7)) < 1e-13
+    assert np.max(np.abs(c[1:])) < 1e-13
+
+
+def test_batch_subset_and_determinism(F):
+    n, batch = 128, 4
+    x, _ = images(2, batch, n, torch.float32)
+    plan = F.Plan(n, batch, torch.float32)
+    c_all = plan.forward(x.cuda()).clone()
+    c_one = plan.forward(x[2:3].cuda())
+    assert torch.equal(c_all[2:3], c_one)          # same arithmetic whatever the batch
+    c_again = plan.forward(x.cuda())
+    assert torch.equal(c_all, c_again)             # bitwise deterministic (no atomics)
+    r1 = plan.inverse(c_all).clone()
+    r2 = plan.inverse(c_all)
+    assert torch.equal(r1, r2)
+
+
+def test_shards_sum_to_full(F):
+    # eta-sharding: each shard's cube holds its planes; partial images sum to the full inverse
+    n, batch, shards = 64, 2, 3
+    x, xo = images(2, batch, n, torch.float64)
+    full = F.Plan(n, batch, torch.float64)
+    c_full = full.forward(x.cuda()).cpu()
+    rec_sum = torch.zeros(batch, n, n, dtype=torch.float64)
+    for r in range(shards):
+        p = F.Plan(n, batch, torch.float64, shard_rank=r, shard_count=shards)
+        assert p.local_planes == list(range(r, full.eta, shards))
+        c = p.forward(x.cuda())
+        assert torch.allclose(c.cpu(), c_full[:, r::shards], atol=1e-13, rtol=0)
+        rec_sum += p.inverse(c).cpu()
+    assert np.max(np.abs(rec_sum.numpy() - xo)) < 1e-12
+
+
+def test_host_variants(F):
+    n, batch = 64, 2
+    x, xo = images(2, batch, n, torch.float32)
+    plan = F.Plan(n, batch, torch.float32)
+    c = plan.forward_host(x.pin_memory())
+    out = torch.empty(batch, n, n, dtype=torch.float32).pin_memory()
+    plan.inverse_host(c, out)
+    torch.cuda.synchronize()
+    assert plane_err(out.numpy(), xo).max() <= 1e-4
+    assert torch.equal(c, plan.forward(x.cuda()))
+
+
+def test_errors(F):
+    with pytest.raises(F.FFSTError):
+        F.Plan(3, 1)
+    with pytest.raises(F.FFSTError):
+        F.Plan(96, 1)
+    with pytest.raises(F.FFSTError):
+        F.Plan(4096, 1, torch.float64)
+    plan = F.Plan(32, 2)
+    with pytest.raises(ValueError):
+        plan.forward(torch.zeros(3, 32, 32, device="cuda"))
+
+
+# ------------------------------------------------------------------ the benchmark configs
+
+def _check_forward_planes(c_gpu, x64, planes, tol, n):
+    f_hat = O.dft2_centred(x64)
+    errs = []
+    for i in planes:
+        ref = O.forward_plane(x64, i + 1, f_hat=f_hat)
+        errs.append(plane_err(c_gpu[i], ref, np.max(np.abs(x64))))
+    return max(errs)
+
+
+def test_config2_full(F):
+    # configs[1]: 256x256 float32 batch 16 — every plane of every image, and the inverse
+    cfg = synth.config(2)
+    x, xo = images(2, cfg.batch, cfg.n, torch.float32)
+    plan = F.Plan(cfg.n, cfg.batch, torch.float32)
+    c = plan.forward(x.cuda())
+    rec = plan.inverse(c).cpu().numpy()
+    c = c.cpu().numpy()
+    psi = O.shearlet_spectra(cfg.n)
+    worst = 0.0
+    for b in range(cfg.batch):
+        ref = O.forward(xo[b], psi=psi)
+        worst = max(worst, plane_err(c[b], ref, np.max(np.abs(xo[b]))).max())
+        ref_inv = O.inverse(c[b].astype(np.complex128), psi=psi).real
+        assert plane_err(rec[b], ref_inv).max() <= 1e-4
+        assert plane_err(rec[b], xo[b]).max() <= 1e-4
+    assert worst <= 1e-4, worst
+
+
+@pytest.mark.parametrize("cid,images_checked,plane_stride", [(3, (0, 63), 1), (4, (0, 31), 5)])
+def test_config_sampled(F, cid, images_checked, plane_stride):
+    # configs[2], configs[3] at their full batch (the bench launch configuration):
+    # sampled images x planes against the oracle, round trip and Parseval on every image.
+    cfg = synth.config(cid)
+    x, _ = images(cid, cfg.batch, cfg.n, torch.float32)
+    plan = F.Plan(cfg.n, cfg.batch, torch.float32)
+    xd = x.cuda()
+    c = plan.forward(xd)
+    rec = plan.inverse(c)
+    # properties at full size on every image
+    err_rt = (rec - xd).abs().amax(dim=(1, 2)) / xd.abs().amax(dim=(1, 2))
+    assert float(err_rt.max()) <= 1e-4
+    energy_c = (c.abs() ** 2).double().sum(dim=(1, 2, 3))
+    energy_f = (xd.double() ** 2).sum(dim=(1, 2))
+    assert float(((energy_c - energy_f).abs() / energy_f).max()) <= 1e-4
+    j0 = O.scales_for_size(cfg.n)
+    eta = O.num_shearlets(j0)
+    planes = sorted(set(range(0, eta, plane_stride)) | {eta - 1, eta - 2})
+    for b in images_checked:
+        cb = c[b].cpu().numpy()
+        x64 = x[b].double().numpy()
+        assert _check_forward_planes(cb, x64, planes, 1e-4, cfg.n) <= 1e-4
+        # inverse parity on a cube restricted to a few planes (others zeroed)
+        keep = planes[:3] + planes[-2:]
+        z = torch.zeros_like(c[b:b + 1])
+        z[0, keep] = c[b, keep]
+        sub = F.Plan(cfg.n, 1, torch.float32)
+        r = sub.inverse(z).cpu().numpy()[0]
+        ref = O.inverse(cb[keep].astype(np.complex128), planes=[i + 1 for i in keep]).real
+        assert plane_err(r, ref).max() <= 1e-4
+    del c, rec
+
+
+def test_config5_sampled(F):
+    # configs[4]: 4096x4096 float32 single image, sampled planes, round trip, Parseval
+    cfg = synth.config(5)
+    x, _ = images(5, 1, cfg.n, torch.float32)
+    plan = F.Plan(cfg.n, 1, torch.float32)
+    xd = x.cuda()
+    c = plan.forward(xd)
+    rec = plan.inverse(c)
+    assert float((rec - xd).abs().max() / xd.abs().max()) <= 1e-4
+    ec = float((c.abs() ** 2).double().sum())
+    ef = float((xd.double() ** 2).sum())
+    assert abs(ec - ef) / ef <= 1e-4
+    eta = plan.eta
+    nyq = [i for i in range(eta) if F.plane_is_nyquist(cfg.n, i)]
+    planes = sorted({0, 1, eta // 2, eta - 1, nyq[0], nyq[len(nyq) // 2]})
+    x64 = x[0].double().numpy()
+    f_hat = O.dft2_centred(x64)
+    for i in planes:
+        g = c[0, i].cpu().numpy()
+        ref = O.forward_plane(x64, i + 1, f_hat=f_hat)
+        assert plane_err(g, ref, np.max(np.abs(x64))) <= 1e-4, i
