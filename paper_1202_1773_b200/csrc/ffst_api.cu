@@ -136,6 +136,7 @@ struct ffst_plan {
   Geometry geo{};
   int sm_count = 0, grid_fwd = 0, grid_inv = 0;
   long long slot_budget = 0;
+  int chunk_planes = 8;           // max planes per chunk (pipelining granularity of the passes)
   // device memory
   PlaneDev* d_planes = nullptr;
   int* d_nyq = nullptr;
@@ -183,72 +184,109 @@ ffst_status dalloc(ffst_plan* p, void** ptr, size_t bytes) {
 
 #define TRY(x) do { ffst_status s_ = (x); if (s_ != FFST_OK) return s_; } while (0)
 
+// Work queues of the persistent kernels for `batch` images.
+//
+// 1. Chunks: consecutive planes of ONE image, at most chunk_planes planes and
+//    slot_budget elements of intermediates.
+// 2. Chunk order S: images in groups of Wg, round-robin over the chunk index inside
+//    a group, so two chunks of the same image are Wg apart (the inverse chains the
+//    accumulation of one image's chunks per column group).
+// 3. Lookahead D: P2(S_c) is queued after P1(S_{c+D}); D is the smallest number of
+//    chunks whose items cover ~3 waves of the grid, so the pass-1 items a pass-2 item
+//    depends on have normally finished by the time it is dispatched.  The ring has
+//    R = D + 2 slots; P1(S_c) reuses the slot of S_{c-R}, whose P2 items are queued
+//    earlier.  Every dependency of an item is an earlier item: deadlock-free.
 ffst_status build_queue(ffst_plan* p, int batch, Queue** out) {
   auto it = p->queues.find(batch);
   if (it != p->queues.end()) { *out = &it->second; return FFST_OK; }
   const int N = p->n, H = p->H;
   const Geometry& g = p->geo;
-  std::vector<UnitDev> units;
-  std::vector<ChunkDev> chunks;
-  // chunking: single-image chunks, intermediates of the chunk <= slot budget
+  // ---- 1. chunks per image (in image order)
+  struct Proto { int b, lp0, np; long long elems; };
+  std::vector<Proto> protos;
   for (int b = 0; b < batch; ++b) {
+    int lp0 = 0;
     long long used = 0;
-    int start = (int)units.size();
     for (int lp = 0; lp < p->eta_l; ++lp) {
       const long long need = (long long)N * p->planes[lp].ncols_pad;
-      if ((int)units.size() > start && used + need > p->slot_budget) {
-        ChunkDev c{};
-        c.b = b; c.unit0 = start; c.nunits = (int)units.size() - start;
-        chunks.push_back(c);
-        start = (int)units.size();
+      const int in_chunk = lp - lp0;
+      if (in_chunk > 0 && (used + need > p->slot_budget || in_chunk >= p->chunk_planes)) {
+        protos.push_back({b, lp0, in_chunk, used});
+        lp0 = lp;
         used = 0;
       }
-      UnitDev u{};
-      u.b = b; u.p = lp; u.chunk = (int)chunks.size(); u.woff = (int)used;
-      units.push_back(u);
       used += need;
     }
-    ChunkDev c{};
-    c.b = b; c.unit0 = start; c.nunits = (int)units.size() - start;
-    chunks.push_back(c);
+    protos.push_back({b, lp0, p->eta_l - lp0, used});
   }
-  Queue q;
-  q.batch = batch;
-  q.n_chunks = (int)chunks.size();
+  const int chunks_per_image = (int)protos.size() / batch;   // identical for every image
+  auto items_fwd = [&](const Proto& c) {
+    int n1 = 0;
+    for (int lp = c.lp0; lp < c.lp0 + c.np; ++lp) n1 += (p->planes[lp].ncols + g.gc - 1) / g.gc;
+    return n1 + c.np * ((N + g.rp2 - 1) / g.rp2);
+  };
+  double avg_items = 0;
   long long slot = 0;
-  for (auto& c : chunks) {
-    long long s = 0;
-    for (int u = c.unit0; u < c.unit0 + c.nunits; ++u) {
-      units[u].chunk = (int)(&c - chunks.data());
-      s += (long long)N * p->planes[units[u].p].ncols_pad;
+  for (auto& c : protos) {
+    avg_items += items_fwd(c);
+    slot = std::max(slot, c.elems);
+  }
+  avg_items /= (double)protos.size();
+  const int grid = std::max(p->grid_fwd, p->grid_inv);
+  int D = (int)std::ceil(3.0 * grid / std::max(1.0, avg_items));
+  D = std::max(1, std::min(D, (int)protos.size()));
+  const long long slot_elems = (slot + 63) / 64 * 64;
+  // slot reuse distance R - D = D + 2: a pass-1 item reuses the slot of a chunk whose
+  // pass-2 items were queued ~D chunks earlier
+  const int max_slots = (int)std::max(2LL, p->W_elems / slot_elems);
+  D = std::min(D, std::max(1, (max_slots - 2) / 2));
+  int R = std::min((int)protos.size(), std::min(max_slots, 2 * D + 2));
+  if ((long long)R * slot_elems > p->W_elems) return fail(FFST_ERR_INVALID_ARG, "intermediate ring exceeds workspace");
+  // ---- 2. interleaved chunk order
+  const int Wg = std::max(1, std::min(batch, D));
+  std::vector<int> order;   // indices into protos
+  for (int b0 = 0; b0 < batch; b0 += Wg) {
+    const int b1 = std::min(batch, b0 + Wg);
+    for (int ci = 0; ci < chunks_per_image; ++ci)
+      for (int b = b0; b < b1; ++b) order.push_back(b * chunks_per_image + ci);
+  }
+  const int C = (int)order.size();
+  std::vector<UnitDev> units;
+  std::vector<ChunkDev> chunks(C);
+  std::vector<int> last_chunk_of_image(batch, -1);
+  for (int c = 0; c < C; ++c) {
+    const Proto& pr = protos[order[c]];
+    ChunkDev& ch = chunks[c];
+    ch.b = pr.b;
+    ch.unit0 = (int)units.size();
+    ch.nunits = pr.np;
+    ch.slot = c % R;
+    ch.prev_slot_chunk = c - R >= 0 ? c - R : -1;
+    ch.first_of_image = last_chunk_of_image[pr.b] < 0 ? 1 : 0;
+    last_chunk_of_image[pr.b] = c;
+    long long used = 0;
+    for (int lp = pr.lp0; lp < pr.lp0 + pr.np; ++lp) {
+      UnitDev u{};
+      u.b = pr.b; u.p = lp; u.chunk = c; u.woff = (int)used;
+      units.push_back(u);
+      used += (long long)N * p->planes[lp].ncols_pad;
     }
-    slot = std::max(slot, s);
   }
-  q.slot_elems = (slot + 63) / 64 * 64;
-  q.nslots = std::min(3, q.n_chunks);
-  if (q.slot_elems * q.nslots > p->W_elems)
-    return fail(FFST_ERR_INVALID_ARG, "intermediate ring larger than the planned workspace");
-  // first-of-image flags
-  for (size_t c = 0; c < chunks.size(); ++c) {
-    chunks[c].slot = (int)(c % q.nslots);
-    chunks[c].prev_slot_chunk = (int)c - q.nslots >= 0 ? (int)c - q.nslots : -1;
-    chunks[c].first_of_image = (c == 0 || chunks[c - 1].b != chunks[c].b) ? 1 : 0;
-  }
-  // ---- forward items
-  std::vector<std::vector<ItemDev>> f1(chunks.size()), f2(chunks.size()), i1(chunks.size()), i2(chunks.size());
+  // ---- 3. items
+  std::vector<std::vector<ItemDev>> f1(C), f2(C), i1(C), i2(C);
   const int ngroups = (H + 1 + g.lpc - 1) / g.lpc;
   std::vector<int> last_self((size_t)batch * ngroups, -1);
   int n_self = 0;
-  for (size_t c = 0; c < chunks.size(); ++c) {
+  for (int c = 0; c < C; ++c) {
     const ChunkDev& ch = chunks[c];
     for (int u = ch.unit0; u < ch.unit0 + ch.nunits; ++u) {
       const PlaneDev& P = p->planes[units[u].p];
       const int ng1 = (P.ncols + g.gc - 1) / g.gc;
-      for (int gi = 0; gi < ng1; ++gi) f1[c].push_back({0, (int)c, u, gi, -1, -1});
+      for (int gi = 0; gi < ng1; ++gi) f1[c].push_back({0, c, u, gi, -1, -1});
       const int ng2 = (N + g.rp2 - 1) / g.rp2;
-      for (int gi = 0; gi < ng2; ++gi) f2[c].push_back({1, (int)c, u, gi, -1, -1});
+      for (int gi = 0; gi < ng2; ++gi) f2[c].push_back({1, c, u, gi, -1, -1});
       const int ni1 = (N + g.rpi - 1) / g.rpi;
-      for (int gi = 0; gi < ni1; ++gi) i1[c].push_back({0, (int)c, u, gi, -1, -1});
+      for (int gi = 0; gi < ni1; ++gi) i1[c].push_back({0, c, u, gi, -1, -1});
     }
     for (int gg = 0; gg < ngroups; ++gg) {
       bool touched = ch.first_of_image != 0;
@@ -259,35 +297,37 @@ ffst_status build_queue(ffst_plan* p, int batch, Queue** out) {
       }
       if (!touched) continue;
       int& last = last_self[(size_t)ch.b * ngroups + gg];
-      i2[c].push_back({1, (int)c, -1, gg, last, n_self});
+      i2[c].push_back({1, c, -1, gg, last, n_self});
       last = n_self++;
     }
   }
-  std::vector<ItemDev> fwd, inv;
-  auto order = [&](std::vector<std::vector<ItemDev>>& a, std::vector<std::vector<ItemDev>>& b,
-                   std::vector<ItemDev>& dst) {
-    const int C = (int)chunks.size();
+  auto emit = [&](std::vector<std::vector<ItemDev>>& a, std::vector<std::vector<ItemDev>>& b,
+                  std::vector<ItemDev>& dst) {
+    for (int c = 0; c < std::min(D, C); ++c) dst.insert(dst.end(), a[c].begin(), a[c].end());
     for (int c = 0; c < C; ++c) {
-      dst.insert(dst.end(), a[c].begin(), a[c].end());
-      if (c >= 1) dst.insert(dst.end(), b[c - 1].begin(), b[c - 1].end());
+      if (c + D < C) dst.insert(dst.end(), a[c + D].begin(), a[c + D].end());
+      dst.insert(dst.end(), b[c].begin(), b[c].end());
     }
-    dst.insert(dst.end(), b[C - 1].begin(), b[C - 1].end());
   };
-  order(f1, f2, fwd);
-  order(i1, i2, inv);
-  for (size_t c = 0; c < chunks.size(); ++c) {
-    chunks[c].p1_items = (int)f1[c].size();   // forward counts; inverse counts set at launch
-    chunks[c].p2_items = (int)f2[c].size();
-  }
+  std::vector<ItemDev> fwd, inv;
+  emit(f1, f2, fwd);
+  emit(i1, i2, inv);
   std::vector<ChunkDev> chunks_inv = chunks;
-  for (size_t c = 0; c < chunks.size(); ++c) {
+  for (int c = 0; c < C; ++c) {
+    chunks[c].p1_items = (int)f1[c].size();
+    chunks[c].p2_items = (int)f2[c].size();
     chunks_inv[c].p1_items = (int)i1[c].size();
     chunks_inv[c].p2_items = (int)i2[c].size();
   }
+  Queue q;
+  q.batch = batch;
+  q.n_chunks = C;
+  q.slot_elems = slot_elems;
+  q.nslots = R;
   q.n_fwd = (int)fwd.size();
   q.n_inv = (int)inv.size();
   q.n_g = n_self;
-  const size_t need_ctr = 1 + 2 * chunks.size() + (size_t)n_self;
+  const size_t need_ctr = 1 + 2 * (size_t)C + (size_t)n_self;
   if (need_ctr > p->ctr_cap) {
     void* c = nullptr;
     TRY(dalloc(p, &c, need_ctr * sizeof(int)));
@@ -309,6 +349,9 @@ ffst_status build_queue(ffst_plan* p, int batch, Queue** out) {
                       cudaMemcpyHostToDevice), "queue upload");
   API_CUDA(cudaMemcpy(q.d_fwd, fwd.data(), fwd.size() * sizeof(ItemDev), cudaMemcpyHostToDevice), "queue upload");
   API_CUDA(cudaMemcpy(q.d_inv, inv.data(), inv.size() * sizeof(ItemDev), cudaMemcpyHostToDevice), "queue upload");
+  if (std::getenv("FFST_VERBOSE"))
+    std::fprintf(stderr, "[ffst] batch=%d chunks=%d (per image %d) D=%d R=%d Wg=%d slot=%.1f MB items fwd=%d inv=%d\n",
+                 batch, C, chunks_per_image, D, R, Wg, slot_elems * 2.0 * p->rsz / 1048576.0, q.n_fwd, q.n_inv);
   auto res = p->queues.emplace(batch, q);
   *out = &res.first->second;
   return FFST_OK;
@@ -569,10 +612,14 @@ ffst_status ffst_plan_create(ffst_plan** out, const ffst_plan_desc* d) {
     image_total += (long long)N * P.ncols_pad;
   }
   const char* env = std::getenv("FFST_SLOT_MB");
-  const long long budget_bytes = (env ? std::atoll(env) : 12) * 1024LL * 1024LL;
+  const long long budget_bytes = (env ? std::atoll(env) : 4) * 1024LL * 1024LL;
   p->slot_budget = std::max(maxplane, budget_bytes / (long long)csz);
+  const char* envc = std::getenv("FFST_CHUNK_PLANES");
+  p->chunk_planes = std::max(1, envc ? std::atoi(envc) : 8);
   const long long slot_max = std::min(image_total, std::max(maxplane, p->slot_budget)) + 64;
-  p->W_elems = 3 * slot_max;
+  const char* envr = std::getenv("FFST_RING_MB");
+  const long long ring_bytes = (envr ? std::atoll(envr) : 48) * 1024LL * 1024LL;
+  p->W_elems = std::max(3 * ((slot_max + 63) / 64 * 64), ring_bytes / (long long)csz);
   p->n_rowitems = (int)((N + p->geo.rpi - 1) / p->geo.rpi);
   const size_t nn = std::max<size_t>(1, p->nyq.size());
 

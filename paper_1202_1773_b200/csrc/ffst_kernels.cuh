@@ -39,14 +39,18 @@ struct Geo {
   // inverse pass 1: rows per tile and per item
   static constexpr int GR_ = LPR > (32 / ESZ) ? LPR : (32 / ESZ);
   static constexpr int GR = GR_ < N ? GR_ : N;
-  static constexpr int TSTR = H + 2;
+  static constexpr int TSTR = H + 1;           // odd: conflict-free column reads of the tile
   static constexpr int TILE_R = GR * TSTR;
   static constexpr int RPI_ = (N / 16) > GR ? (N / 16) : GR;
   static constexpr int RPI = RPI_ < N ? RPI_ : N;
   // padded row stride of the final column pass output
   static constexpr int NCPF = ((H + 1 + GC - 1) / GC) * GC;
-  static constexpr size_t SMEM_FWD = (size_t)((SCR_C + TILE_C) > SCR_R ? (SCR_C + TILE_C) : SCR_R) * ESZ;
-  static constexpr size_t SMEM_INV = (size_t)((SCR_R + TILE_R) > SCR_C ? (SCR_R + TILE_R) : SCR_C) * ESZ + 256;
+  // per-thread window values (EC reals per thread), staged in shared memory so the window
+  // arithmetic is not unrolled into the FFT's register footprint
+  static constexpr int WBUF = NT * EC * (int)sizeof(T) / ESZ;      // in complex elements
+  static constexpr int NYQB = (N + RP2) * (int)sizeof(T) / ESZ + 1;   // staged Nyquist terms (complex units)
+  static constexpr size_t SMEM_FWD = (size_t)((SCR_C + TILE_C + WBUF) > (SCR_R + NYQB) ? (SCR_C + TILE_C + WBUF) : (SCR_R + NYQB)) * ESZ;
+  static constexpr size_t SMEM_INV = (size_t)((SCR_R + TILE_R) > (SCR_C + WBUF) ? (SCR_R + TILE_R) : (SCR_C + WBUF)) * ESZ + 256;
   static constexpr size_t SMEM_AUX = SMEM_FWD > SMEM_INV ? SMEM_FWD : SMEM_INV;
   static_assert(RPI % GR == 0, "RPI must be a multiple of GR");
   static_assert(GC % LPC == 0 || LPC > GC, "GC vs LPC");
@@ -108,15 +112,19 @@ struct K {
       const int u1 = cb == H ? -H : cb;
       const C* col = src + (size_t)cb * N;
       C r[G::EC];
+      if constexpr (MODE == MODE_MAIN) {
+        T* wbuf = reinterpret_cast<T*>(tile + G::TILE_C);
+#pragma unroll 1
+        for (int q = 0; q < G::EC; ++q)
+          wbuf[q * NT + tid] = act ? window_sym<T>(P, u1, centred(t + q * G::THC, N), H, delta) : T(0);
 #pragma unroll
-      for (int q = 0; q < G::EC; ++q) {
-        const int rb = t + q * G::THC;
-        if constexpr (MODE == MODE_MAIN) {
-          const T w = act ? window_sym<T>(P, u1, centred(rb, N), H, delta) : T(0);
-          r[q] = w != T(0) ? cscale<T>(__ldg(col + rb), w) : czero<T>();
-        } else {
-          r[q] = act ? __ldcg(col + rb) : czero<T>();
+        for (int q = 0; q < G::EC; ++q) {
+          const T w = wbuf[q * NT + tid];
+          r[q] = w != T(0) ? cscale<T>(__ldg(col + t + q * G::THC), w) : czero<T>();
         }
+      } else {
+#pragma unroll
+        for (int q = 0; q < G::EC; ++q) r[q] = act ? __ldcg(col + t + q * G::THC) : czero<T>();
       }
       LineFFT<T, N, true, N>::run(r, scr + line * G::SMC, t, tw);
       if (ci < G::GC) {
@@ -146,6 +154,14 @@ struct K {
     const C* tw = static_cast<const C*>(p.tw);
     const T scale = T(1) / (T(N) * T(N));
     constexpr int ROUNDS = G::RP2 / G::LPR > 0 ? G::RP2 / G::LPR : 1;
+    // Nyquist terms of this item staged in shared memory: G(m1) for all m1, H(r) for its rows
+    T* sG = reinterpret_cast<T*>(smem + G::SCR_R);
+    T* sH = sG + N;
+    if (nyqG != nullptr) {
+      for (int m = tid; m < N; m += NT) sG[m] = nyqG[m];
+      for (int i = tid; i < cnt; i += NT) sH[i] = nyqH[r0 + i];
+      __syncthreads();
+    }
 #pragma unroll 1
     for (int rd = 0; rd < ROUNDS; ++rd) {
       const int ri = rd * G::LPR + line;
@@ -173,17 +189,17 @@ struct K {
           if constexpr (MODE == MODE_MAIN) {
             T i0 = T(0), i1 = T(0);
             if (nyqG != nullptr) {
-              const T hr = nyqH[r];
-              i0 = sr * nyqG[m1] + hr;
-              i1 = sr * nyqG[m1 + 1] - hr;
+              const T hr = sH[ri];
+              i0 = sr * sG[m1] + hr;
+              i1 = sr * sG[m1 + 1] - hr;
             }
             store_pair_cs<T>(out_c + (size_t)r * N + m1, mk<T>(x0, i0), mk<T>(x1, i1));
           } else {
             T c0 = T(0), c1 = T(0);
             if (nyqG != nullptr) {
-              const T hr = nyqH[r];
-              c0 = sr * nyqG[m1] + hr;
-              c1 = sr * nyqG[m1 + 1] - hr;
+              const T hr = sH[ri];
+              c0 = sr * sG[m1] + hr;
+              c1 = sr * sG[m1 + 1] - hr;
             }
             cpx<T> v = mk<T>(x0 - c0, x1 - c1);
             *reinterpret_cast<cpx<T>*>(out_r + (size_t)r * N + m1) = v;
@@ -336,6 +352,11 @@ struct K {
       if (g1 <= P.c_lo || g0 >= P.c_lo + P.ncols) continue;          // CTA-uniform
       const bool in = act && cb >= P.c_lo && cb < P.c_lo + P.ncols;
       const C* col = slot + U.woff + (size_t)(cb - P.c_lo) * N;
+      T* wbuf = reinterpret_cast<T*>(smem + G::SCR_C);
+      if (in) {
+#pragma unroll 1
+        for (int q = 0; q < G::EC; ++q) wbuf[q * NT + tid] = window_sym<T>(P, u1, centred(t + q * G::THC, N), H, delta);
+      }
       C r[G::EC];
 #pragma unroll
       for (int q = 0; q < G::EC; ++q) r[q] = in ? __ldcg(col + t + q * G::THC) : czero<T>();
@@ -343,7 +364,7 @@ struct K {
       if (in) {
 #pragma unroll
         for (int q = 0; q < G::EC; ++q) {
-          const T w = window_sym<T>(P, u1, centred(t + q * G::THC, N), H, delta);
+          const T w = wbuf[q * NT + tid];
           acc[q].x += w * r[q].x;
           acc[q].y += w * r[q].y;
         }
@@ -426,7 +447,7 @@ struct K {
 };
 
 template <typename T, int N>
-__global__ void __launch_bounds__(256) fwd_main_kernel(KParams p) {
+__global__ void __launch_bounds__(256, 2) fwd_main_kernel(KParams p) {
   extern __shared__ __align__(16) unsigned char smem_raw[];
   cpx<T>* smem = reinterpret_cast<cpx<T>*>(smem_raw);
   __shared__ int s_item;
@@ -456,7 +477,7 @@ __global__ void __launch_bounds__(256) fwd_main_kernel(KParams p) {
 }
 
 template <typename T, int N>
-__global__ void __launch_bounds__(256) inv_main_kernel(KParams p) {
+__global__ void __launch_bounds__(256, 2) inv_main_kernel(KParams p) {
   extern __shared__ __align__(16) unsigned char smem_raw[];
   cpx<T>* smem = reinterpret_cast<cpx<T>*>(smem_raw);
   __shared__ int s_item;
