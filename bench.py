@@ -195,13 +195,18 @@ def run_gpu(args, cfg):
     flush = torch.empty(L2_FLUSH_BYTES // 4, dtype=torch.float32, device=dev)
     stream = torch.cuda.current_stream(dev)
 
-    def step():
-        if world > 1:
-            dist.broadcast(x, src=0)
-        plan.forward(x, out=cube)
-        plan.inverse(cube, out=rec)
-        if world > 1:
-            dist.reduce(rec, dst=0, op=dist.ReduceOp.SUM)
+    if world > 1:
+        from paper_1202_1773_b200.dist import ShardedTransform
+        sharded = ShardedTransform(plan)
+
+        def step():
+            dist.broadcast(x, src=0)                       # images in (NCCL)
+            plan.forward(x, out=cube)                      # local planes
+            sharded.inverse(cube, out=rec)                 # partial image, NCCL reduce to rank 0
+    else:
+        def step():
+            plan.forward(x, out=cube)
+            plan.inverse(cube, out=rec)
 
     for _ in range(args.warmup):
         step()

@@ -52,6 +52,7 @@ struct Geo {
   static constexpr size_t SMEM_FWD = (size_t)((SCR_C + TILE_C + WBUF) > (SCR_R + NYQB) ? (SCR_C + TILE_C + WBUF) : (SCR_R + NYQB)) * ESZ;
   static constexpr size_t SMEM_INV = (size_t)((SCR_R + TILE_R) > (SCR_C + WBUF) ? (SCR_R + TILE_R) : (SCR_C + WBUF)) * ESZ + 256;
   static constexpr size_t SMEM_AUX = SMEM_FWD > SMEM_INV ? SMEM_FWD : SMEM_INV;
+  static constexpr size_t SMEM_NYQ = (size_t)(SCR_C + NT * EC) * ESZ;
   static_assert(RPI % GR == 0, "RPI must be a multiple of GR");
   static_assert(GC % LPC == 0 || LPC > GC, "GC vs LPC");
 };
@@ -570,25 +571,29 @@ __global__ void __launch_bounds__(256) fin_rows_kernel(KParams p) {
                                       reinterpret_cast<cpx<T>*>(smem_raw));
 }
 
-// forward Nyquist terms: grid (n_nyq, 2, B).  which = 0: G(m1) from the Nyquist row,
-// which = 1: H(r) from the Nyquist column.
+// forward Nyquist terms: grid (ceil(n_nyq / LPC), 2, B); line l of the CTA handles Nyquist
+// plane blockIdx.x * LPC + l.  which = 0: G(m1) from the Nyquist row, which = 1: H(r) from the
+// Nyquist column.
 template <typename T, int N>
 __global__ void __launch_bounds__(256) nyq_fwd_kernel(KParams p) {
   extern __shared__ __align__(16) unsigned char smem_raw[];
   using G = Geo<T, N>;
   using C = cpx<T>;
   constexpr int H = N / 2;
-  const int nq = blockIdx.x, which = blockIdx.y, b = blockIdx.z;
-  const PlaneDev P = p.planes[p.nyq_planes[nq]];
+  const int which = blockIdx.y, b = blockIdx.z;
   const int tid = threadIdx.x, line = tid / G::THC, t = tid % G::THC;
+  const int nq = blockIdx.x * G::LPC + line;
+  const bool act = nq < p.n_nyq;
+  PlaneDev P{};
+  if (act) P = p.planes[p.nyq_planes[nq]];
   const C* F = static_cast<const C*>(p.F) + (size_t)b * (H + 1) * N;
   const T delta = (T)p.delta;
   C r[G::EC];
-#pragma unroll
+#pragma unroll 1
   for (int q = 0; q < G::EC; ++q) {
     const int bin = t + q * G::THC;
     C v = czero<T>();
-    if (line == 0) {
+    if (act) {
       const int u = centred(bin, N);
       if (which == 0) {
         const T a = window_anti<T>(P, u, -H, H, delta);
@@ -598,10 +603,12 @@ __global__ void __launch_bounds__(256) nyq_fwd_kernel(KParams p) {
         if (a != T(0)) v = cscale<T>(F[(size_t)H * N + bin], a);
       }
     }
-    r[q] = v;
+    reinterpret_cast<C*>(smem_raw)[G::SCR_C + q * G::NT + tid] = v;
   }
+#pragma unroll
+  for (int q = 0; q < G::EC; ++q) r[q] = reinterpret_cast<C*>(smem_raw)[G::SCR_C + q * G::NT + tid];
   LineFFT<T, N, true, N>::run(r, reinterpret_cast<C*>(smem_raw) + line * G::SMC, t, static_cast<const C*>(p.tw));
-  if (line == 0) {
+  if (act) {
     T* out = static_cast<T*>(p.nyq_fwd) + (((size_t)b * p.n_nyq + nq) * 2 + which) * N;
     const T s = T(1) / (T(N) * T(N));
 #pragma unroll
@@ -609,7 +616,8 @@ __global__ void __launch_bounds__(256) nyq_fwd_kernel(KParams p) {
   }
 }
 
-// inverse Nyquist correction: grid (2, B)
+// inverse Nyquist correction: grid (2, B).  Line l accumulates the Nyquist planes
+// l, l + LPC, ...; the per-line sums are added in fixed line order (deterministic).
 template <typename T, int N>
 __global__ void __launch_bounds__(256) nyq_inv_kernel(KParams p) {
   extern __shared__ __align__(16) unsigned char smem_raw[];
@@ -620,19 +628,22 @@ __global__ void __launch_bounds__(256) nyq_inv_kernel(KParams p) {
   const int tid = threadIdx.x, line = tid / G::THC, t = tid % G::THC;
   const C* tw = static_cast<const C*>(p.tw);
   C* scr = reinterpret_cast<C*>(smem_raw) + line * G::SMC;
+  C* stage = reinterpret_cast<C*>(smem_raw) + G::SCR_C;          // [EC][NT] (also the reduction buffer)
   const T delta = (T)p.delta;
   C acc[G::EC];
 #pragma unroll
   for (int q = 0; q < G::EC; ++q) acc[q] = czero<T>();
+  const int rounds = (p.n_nyq + G::LPC - 1) / G::LPC;
 #pragma unroll 1
-  for (int nq = 0; nq < p.n_nyq; ++nq) {
-    const PlaneDev P = p.planes[p.nyq_planes[nq]];
+  for (int rd = 0; rd < rounds; ++rd) {
+    const int nq = rd * G::LPC + line;
+    const bool act = nq < p.n_nyq;
     C r[G::EC];
 #pragma unroll
     for (int q = 0; q < G::EC; ++q) {
       const int m = t + q * G::THC;
       T s = T(0);
-      if (line == 0) {
+      if (act) {
         if (which == 0) {
           const T* ps = static_cast<const T*>(p.nyq_S) + ((size_t)b * p.n_nyq + nq) * p.n_rowitems * N + m;
           for (int g = 0; g < p.n_rowitems; ++g) s += ps[(size_t)g * N];
@@ -643,15 +654,35 @@ __global__ void __launch_bounds__(256) nyq_inv_kernel(KParams p) {
       r[q] = mk<T>(s, T(0));
     }
     LineFFT<T, N, false, N>::run(r, scr, t, tw);
+    if (act) {
+      const PlaneDev P = p.planes[p.nyq_planes[nq]];
+#pragma unroll 1
+      for (int q = 0; q < G::EC; ++q) {
+        const int u = centred(t + q * G::THC, N);
+        stage[q * G::NT + tid].x = which == 0 ? window_anti<T>(P, u, -H, H, delta) : window_anti<T>(P, -H, u, H, delta);
+      }
 #pragma unroll
-    for (int q = 0; q < G::EC; ++q) {
-      const int u = centred(t + q * G::THC, N);
-      const T a = which == 0 ? window_anti<T>(P, u, -H, H, delta) : window_anti<T>(P, -H, u, H, delta);
-      acc[q].x += a * r[q].x;
-      acc[q].y += a * r[q].y;
+      for (int q = 0; q < G::EC; ++q) {
+        const T a = stage[q * G::NT + tid].x;
+        acc[q].x += a * r[q].x;
+        acc[q].y += a * r[q].y;
+      }
     }
     __syncthreads();
   }
+  // sum the per-line accumulators (fixed order) into line 0
+#pragma unroll
+  for (int q = 0; q < G::EC; ++q) stage[q * G::NT + tid] = acc[q];
+  __syncthreads();
+  if (line == 0) {
+#pragma unroll
+    for (int q = 0; q < G::EC; ++q) {
+      C s = czero<T>();
+      for (int l = 0; l < G::LPC; ++l) s = cadd<T>(s, stage[q * G::NT + l * G::THC + t]);
+      acc[q] = s;
+    }
+  }
+  __syncthreads();
   LineFFT<T, N, true, N>::run(acc, scr, t, tw);
   if (line == 0) {
     T* out = static_cast<T*>(p.corr) + ((size_t)b * 2 + which) * N;

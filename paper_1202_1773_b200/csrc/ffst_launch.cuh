@@ -33,8 +33,8 @@ template <typename T, int N> struct Launch {
     return cudaGetLastError();
   }
   static cudaError_t nyq_fwd(const KParams& p, int batch, cudaStream_t s) {
-    FFST_CHECK(set_smem(nyq_fwd_kernel<T, N>, G::SMEM_AUX));
-    nyq_fwd_kernel<T, N><<<dim3(p.n_nyq, 2, batch), G::NT, G::SMEM_AUX, s>>>(p);
+    FFST_CHECK(set_smem(nyq_fwd_kernel<T, N>, G::SMEM_NYQ));
+    nyq_fwd_kernel<T, N><<<dim3((p.n_nyq + G::LPC - 1) / G::LPC, 2, batch), G::NT, G::SMEM_NYQ, s>>>(p);
     return cudaGetLastError();
   }
   static cudaError_t fwd_main(const KParams& p, int grid, cudaStream_t s) {
@@ -48,8 +48,8 @@ template <typename T, int N> struct Launch {
     return cudaGetLastError();
   }
   static cudaError_t nyq_inv(const KParams& p, int batch, cudaStream_t s) {
-    FFST_CHECK(set_smem(nyq_inv_kernel<T, N>, G::SMEM_AUX));
-    nyq_inv_kernel<T, N><<<dim3(2, batch), G::NT, G::SMEM_AUX, s>>>(p);
+    FFST_CHECK(set_smem(nyq_inv_kernel<T, N>, G::SMEM_NYQ));
+    nyq_inv_kernel<T, N><<<dim3(2, batch), G::NT, G::SMEM_NYQ, s>>>(p);
     return cudaGetLastError();
   }
   static cudaError_t final_(const KParams& p, int batch, cudaStream_t s) {
