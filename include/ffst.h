@@ -150,6 +150,15 @@ ffst_status ffst_inversesheartrans_host(ffst_plan* plan, const void* coeff, void
 ffst_status ffst_plan_set_timing(ffst_plan* plan, int enable);
 ffst_status ffst_plan_phase_times(ffst_plan* plan, float* times, int* launches);
 
+/* Per-item trace of the persistent kernels (diagnostics): enable, run a call, then read
+ * which = 0 (forward) / 1 (inverse) records of the queue for `batch` images:
+ * 8 x u64 per item in queue order = {smid | type << 32 | chunk << 40, t_start, t_ready, t_end,
+ * probe0..probe3} (%globaltimer ns; t_ready = after the item's dependency wait; probes = intra-item
+ * phase marks, 0 if unused).  Synchronises the device. */
+ffst_status ffst_plan_set_trace(ffst_plan* plan, int enable);
+ffst_status ffst_plan_trace(ffst_plan* plan, int which, int batch, unsigned long long* host_out, int max_records,
+                            int* n_records);
+
 const char* ffst_status_string(ffst_status status);
 const char* ffst_last_error_detail(void);
 

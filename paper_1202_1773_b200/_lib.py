@@ -63,6 +63,8 @@ _SIGS = {
     "ffst_inversesheartrans_host": (_i, [_vp, _vp, _vp, _i, _vp]),
     "ffst_plan_set_timing": (_i, [_vp, _i]),
     "ffst_plan_phase_times": (_i, [_vp, C.POINTER(C.c_float), _p]),
+    "ffst_plan_set_trace": (_i, [_vp, _i]),
+    "ffst_plan_trace": (_i, [_vp, _i, _i, C.POINTER(C.c_ulonglong), _i, _p]),
     "ffst_status_string": (C.c_char_p, [_i]),
     "ffst_last_error_detail": (C.c_char_p, []),
 }

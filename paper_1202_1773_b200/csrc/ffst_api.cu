@@ -136,7 +136,7 @@ struct ffst_plan {
   Geometry geo{};
   int sm_count = 0, grid_fwd = 0, grid_inv = 0;
   long long slot_budget = 0;
-  int chunk_planes = 8;           // max planes per chunk (pipelining granularity of the passes)
+  int chunk_planes = 4;           // max planes per chunk (pipelining granularity of the passes)
   // device memory
   PlaneDev* d_planes = nullptr;
   int* d_nyq = nullptr;
@@ -151,6 +151,9 @@ struct ffst_plan {
   std::map<int, Queue> queues;
   size_t ws_bytes = 0;
   bool timing = false;
+  unsigned long long* d_trace[2] = {nullptr, nullptr};   // per-item traces (fwd, inv), optional
+  int trace_items[2] = {0, 0};
+  bool tracing = false;
   cudaEvent_t ev[8] = {};
   int launches[2] = {0, 0};
   std::vector<void*> allocs;
@@ -272,21 +275,28 @@ ffst_status build_queue(ffst_plan* p, int batch, Queue** out) {
       used += (long long)N * p->planes[lp].ncols_pad;
     }
   }
-  // ---- 3. items
+  // ---- 3. items (self-contained; counters: [0] dispatch, [1 + c] pass-1 done, [1 + C + c] pass-2 done,
+  //      [1 + 2C + g] inverse column-group flags)
   std::vector<std::vector<ItemDev>> f1(C), f2(C), i1(C), i2(C);
   const int ngroups = (H + 1 + g.lpc - 1) / g.lpc;
   std::vector<int> last_self((size_t)batch * ngroups, -1);
   int n_self = 0;
+  auto mk_item = [](int type, int c, int group, int b, int pl, int np, int woff, int slot) {
+    ItemDev it{};
+    it.type = type; it.chunk = c; it.group = group; it.b = b; it.p = pl; it.np = np; it.woff = woff; it.slot = slot;
+    it.wait_ctr = -1; it.wait_tgt = 0; it.wait2_ctr = -1; it.first = 0; it.sig_ctr = -1; it.sig2_ctr = -1;
+    return it;
+  };
   for (int c = 0; c < C; ++c) {
     const ChunkDev& ch = chunks[c];
     for (int u = ch.unit0; u < ch.unit0 + ch.nunits; ++u) {
       const PlaneDev& P = p->planes[units[u].p];
       const int ng1 = (P.ncols + g.gc - 1) / g.gc;
-      for (int gi = 0; gi < ng1; ++gi) f1[c].push_back({0, c, u, gi, -1, -1});
+      for (int gi = 0; gi < ng1; ++gi) f1[c].push_back(mk_item(0, c, gi, ch.b, units[u].p, 1, units[u].woff, ch.slot));
       const int ng2 = (N + g.rp2 - 1) / g.rp2;
-      for (int gi = 0; gi < ng2; ++gi) f2[c].push_back({1, c, u, gi, -1, -1});
+      for (int gi = 0; gi < ng2; ++gi) f2[c].push_back(mk_item(1, c, gi, ch.b, units[u].p, 1, units[u].woff, ch.slot));
       const int ni1 = (N + g.rpi - 1) / g.rpi;
-      for (int gi = 0; gi < ni1; ++gi) i1[c].push_back({0, c, u, gi, -1, -1});
+      for (int gi = 0; gi < ni1; ++gi) i1[c].push_back(mk_item(0, c, gi, ch.b, units[u].p, 1, units[u].woff, ch.slot));
     }
     for (int gg = 0; gg < ngroups; ++gg) {
       bool touched = ch.first_of_image != 0;
@@ -297,8 +307,34 @@ ffst_status build_queue(ffst_plan* p, int batch, Queue** out) {
       }
       if (!touched) continue;
       int& last = last_self[(size_t)ch.b * ngroups + gg];
-      i2[c].push_back({1, c, -1, gg, last, n_self});
+      ItemDev it = mk_item(1, c, gg, ch.b, units[ch.unit0].p, ch.nunits, units[ch.unit0].woff, ch.slot);
+      it.first = ch.first_of_image;
+      it.wait2_ctr = last >= 0 ? 1 + 2 * C + last : -1;
+      it.sig2_ctr = 1 + 2 * C + n_self;
+      i2[c].push_back(it);
       last = n_self++;
+    }
+  }
+  // dependency / signal counters
+  for (int c = 0; c < C; ++c) {
+    const int prev = chunks[c].prev_slot_chunk;
+    for (auto* vec : {&f1[c], &i1[c]}) {
+      const bool fw = vec == &f1[c];
+      for (auto& it : *vec) {
+        it.sig_ctr = 1 + c;
+        if (prev >= 0) {
+          it.wait_ctr = 1 + C + prev;
+          it.wait_tgt = (int)(fw ? f2[prev].size() : i2[prev].size());
+        }
+      }
+    }
+    for (auto* vec : {&f2[c], &i2[c]}) {
+      const bool fw = vec == &f2[c];
+      for (auto& it : *vec) {
+        it.sig_ctr = 1 + C + c;
+        it.wait_ctr = 1 + c;
+        it.wait_tgt = (int)(fw ? f1[c].size() : i1[c].size());
+      }
     }
   }
   auto emit = [&](std::vector<std::vector<ItemDev>>& a, std::vector<std::vector<ItemDev>>& b,
@@ -401,6 +437,19 @@ ffst_status set_device(ffst_plan* p) {
   return FFST_OK;
 }
 
+ffst_status trace_buffer(ffst_plan* p, int which, int n_items, KParams* k) {
+  k->trace = nullptr;
+  if (!p->tracing) return FFST_OK;
+  if (p->trace_items[which] < n_items) {
+    void* ptr = nullptr;
+    TRY(dalloc(p, &ptr, (size_t)n_items * 8 * sizeof(unsigned long long)));
+    p->d_trace[which] = static_cast<unsigned long long*>(ptr);
+    p->trace_items[which] = n_items;
+  }
+  k->trace = p->d_trace[which];
+  return FFST_OK;
+}
+
 ffst_status forward_impl(ffst_plan* p, const void* img, void* coeff, int batch, cudaStream_t s) {
   if (!img || !coeff) return fail(FFST_ERR_INVALID_ARG, "null buffer");
   if (batch < 1 || batch > p->d.batch) return fail(FFST_ERR_INVALID_ARG, "batch outside 1..plan batch");
@@ -421,6 +470,7 @@ ffst_status forward_impl(ffst_plan* p, const void* img, void* coeff, int batch, 
   k.ctr_p1 = 1;
   k.ctr_p2 = 1 + q->n_chunks;
   k.ctr_g = 1 + 2 * q->n_chunks;
+  TRY(trace_buffer(p, 0, q->n_fwd, &k));
   int nl = 0;
   if (p->timing) API_CUDA(cudaEventRecord(p->ev[0], s), "event");
   API_CUDA(L_spectrum(p, k, batch, s), "spectrum kernels");
@@ -460,6 +510,7 @@ ffst_status inverse_impl(ffst_plan* p, const void* coeff, void* img_out, int bat
   k.ctr_p1 = 1;
   k.ctr_p2 = 1 + q->n_chunks;
   k.ctr_g = 1 + 2 * q->n_chunks;
+  TRY(trace_buffer(p, 1, q->n_inv, &k));
   int nl = 0;
   if (p->timing) API_CUDA(cudaEventRecord(p->ev[3], s), "event");
   API_CUDA(cudaMemsetAsync(p->d_ctr, 0, (1 + 2 * (size_t)q->n_chunks + q->n_g) * sizeof(int), s), "counter reset");
@@ -589,6 +640,10 @@ ffst_status ffst_plan_create(ffst_plan** out, const ffst_plan_desc* d) {
     p->planes.push_back(P);
   }
   p->eta_l = (int)p->planes.size();
+  if (p->eta_l > 256) {
+    delete p;
+    return fail(FFST_ERR_UNSUPPORTED, "more than 256 local planes: shard the plan (shard_count > 1)");
+  }
 
   auto cleanup = [&](ffst_status s) { ffst_plan_destroy(p); return s; };
   cudaError_t e = cudaSetDevice(d->device);
@@ -615,7 +670,7 @@ ffst_status ffst_plan_create(ffst_plan** out, const ffst_plan_desc* d) {
   const long long budget_bytes = (env ? std::atoll(env) : 4) * 1024LL * 1024LL;
   p->slot_budget = std::max(maxplane, budget_bytes / (long long)csz);
   const char* envc = std::getenv("FFST_CHUNK_PLANES");
-  p->chunk_planes = std::max(1, envc ? std::atoi(envc) : 8);
+  p->chunk_planes = std::max(1, envc ? std::atoi(envc) : 4);
   const long long slot_max = std::min(image_total, std::max(maxplane, p->slot_budget)) + 64;
   const char* envr = std::getenv("FFST_RING_MB");
   const long long ring_bytes = (envr ? std::atoll(envr) : 48) * 1024LL * 1024LL;
@@ -753,6 +808,32 @@ ffst_status ffst_plan_phase_times(ffst_plan* p, float* times, int* launches) {
     launches[0] = p->launches[0];
     launches[1] = p->launches[1];
   }
+  return FFST_OK;
+}
+
+ffst_status ffst_plan_set_trace(ffst_plan* p, int enable) {
+  if (!p) return fail(FFST_ERR_INVALID_ARG, "null plan");
+  p->tracing = enable != 0;
+  return FFST_OK;
+}
+
+ffst_status ffst_plan_trace(ffst_plan* p, int which, int batch, unsigned long long* host_out, int max_records,
+                            int* n_records) {
+  if (!p || !host_out || !n_records || (which != 0 && which != 1)) return fail(FFST_ERR_INVALID_ARG, "bad argument");
+  if (!p->tracing || !p->d_trace[which]) return fail(FFST_ERR_INVALID_ARG, "tracing not enabled / no call yet");
+  Queue* q = nullptr;
+  TRY(set_device(p));
+  TRY(build_queue(p, batch, &q));
+  const int n = std::min(max_records, which == 0 ? q->n_fwd : q->n_inv);
+  API_CUDA(cudaDeviceSynchronize(), "trace sync");
+  API_CUDA(cudaMemcpy(host_out, p->d_trace[which], (size_t)n * 8 * sizeof(unsigned long long), cudaMemcpyDeviceToHost),
+           "trace copy");
+  std::vector<ItemDev> items(n);
+  API_CUDA(cudaMemcpy(items.data(), which == 0 ? q->d_fwd : q->d_inv, (size_t)n * sizeof(ItemDev),
+                      cudaMemcpyDeviceToHost), "trace copy");
+  // record = {smid, t_start, t_ready, t_end} -> append type/chunk in the high bits of smid
+  for (int i = 0; i < n; ++i) host_out[8 * i] |= ((unsigned long long)items[i].type << 32) | ((unsigned long long)items[i].chunk << 40);
+  *n_records = n;
   return FFST_OK;
 }
 

@@ -14,14 +14,23 @@ struct UnitDev {
   int woff;        // element (complex) offset of its intermediate inside the ring slot
 };
 
-// A work item of the persistent kernels.
+// A self-contained work item of the persistent kernels (64 bytes, read with 4 vector loads;
+// no dependent table lookups at item start).
 //   type 0 = first pass (fwd: window * F -> column IFFT; inv: row R2C of a coefficient plane)
 //   type 1 = second pass (fwd: row C2R -> coefficients; inv: column FFT * window, accumulate)
-struct ItemDev {
-  int type, chunk, unit, group;
-  int dep;         // inverse pass 2: counter (in the group block) of the previous chunk of the same
-                   // image for this column group, or -1
-  int self;        // inverse pass 2: own counter in the group block
+struct __align__(16) ItemDev {
+  int type, chunk, group, b;
+  int p;           // local plane (inverse pass 2: first plane of the chunk)
+  int np;          // inverse pass 2: planes of the chunk (else 1)
+  int woff;        // element offset of the (first) plane's intermediate in the ring slot
+  int slot;        // ring slot
+  int wait_ctr;    // counter to wait for (-1: none); pass 1 waits only before writing its slot
+  int wait_tgt;    // value it must reach
+  int wait2_ctr;   // inverse pass 2: previous owner of the column group (-1: none), target 1
+  int first;       // inverse pass 2: first chunk of the image (initialise A)
+  int sig_ctr;     // counter incremented when done
+  int sig2_ctr;    // second counter (inverse pass 2: own column-group flag), or -1
+  int pad0, pad1;
 };
 
 struct ChunkDev {
@@ -58,6 +67,7 @@ struct KParams {
   const UnitDev* units;
   int* ctr;                     // [0] dispatch; [ctr_p1 + c]; [ctr_p2 + c]; [ctr_g + item]
   int ctr_p1, ctr_p2, ctr_g;
+  unsigned long long* trace;    // optional: per item {smid, t_start, t_ready, t_end} (globaltimer ns)
 };
 
 // Launch geometry of one (T, N) instantiation (host + device visible).

@@ -78,6 +78,20 @@ template <> __device__ __forceinline__ void load_pair_cs<double>(const double2* 
   b = __ldcs(src + 1);
 }
 
+__device__ __forceinline__ unsigned long long gtimer() {
+  unsigned long long t;
+  asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t));
+  return t;
+}
+__device__ __forceinline__ unsigned smid() {
+  unsigned r;
+  asm volatile("mov.u32 %0, %%smid;" : "=r"(r));
+  return r;
+}
+
+__shared__ unsigned long long s_probe[4];   // intra-item probes (trace mode)
+#define FFST_PROBE(p, i) do { if ((p).trace != nullptr && threadIdx.x == 0) s_probe[i] = gtimer(); } while (0)
+
 __device__ __forceinline__ void spin_wait(const int* ctr, int target) {
   const volatile int* v = ctr;
   while (*v < target) __nanosleep(40);
@@ -98,7 +112,7 @@ struct K {
   template <int MODE>
   static __device__ void col_ifft(const KParams& p, int b, const PlaneDev& P, int c0, int cnt,
                                   const C* __restrict__ src, C* dst, int dst_stride, int dst_col0,
-                                  C* smem) {
+                                  C* smem, const int* dep = nullptr, int dep_target = 0) {
     C* scr = smem;
     C* tile = smem + G::SCR_C;
     const int tid = threadIdx.x, line = tid / G::THC, t = tid % G::THC;
@@ -132,6 +146,10 @@ struct K {
 #pragma unroll
         for (int q = 0; q < G::EC; ++q) tile[(t + q * G::THC) * G::GCP + ci] = r[q];
       }
+      __syncthreads();
+    }
+    if (dep != nullptr) {                      // ring-slot reuse: wait only before writing dst
+      if (tid == 0) spin_wait(dep, dep_target);
       __syncthreads();
     }
     const int ncopy = cnt < G::GC ? cnt : G::GC;
@@ -169,18 +187,27 @@ struct K {
       const bool act = ri < cnt;
       const int r = r0 + ri;
       const C* row = src + (size_t)r * stride - c_lo;
-      C z[G::ER];
+      C z[G::ER], zm[G::ER];
+      // phase 1: issue every load of the round (no use in between: all in flight together)
 #pragma unroll
       for (int q = 0; q < G::ER; ++q) {
         const int k = t + q * G::THR, km = H - k;
-        const C xk = (act && k >= c_lo && k < c_lo + ncols) ? __ldcg(row + k) : czero<T>();
-        const C xm = (act && km >= c_lo && km < c_lo + ncols) ? __ldcg(row + km) : czero<T>();
+        z[q] = (act && k >= c_lo && k < c_lo + ncols) ? __ldcg(row + k) : czero<T>();
+        zm[q] = (act && km >= c_lo && km < c_lo + ncols) ? __ldcg(row + km) : czero<T>();
+      }
+      // phase 2: Hermitian pre-processing of the half-length C2R
+#pragma unroll
+      for (int q = 0; q < G::ER; ++q) {
+        const int k = t + q * G::THR;
+        const C xk = z[q], xm = zm[q];
         const C a = mk<T>(xk.x + xm.x, xk.y - xm.y);      // xk + conj(xm)
         const C d = mk<T>(xk.x - xm.x, xk.y + xm.y);      // xk - conj(xm)
         const C e = cmulc<T>(d, __ldg(tw + k));            // d * exp(+2 pi i k / N)
         z[q] = mk<T>(a.x - e.y, a.y + e.x);                 // a + i e
       }
+      if (rd == 0) FFST_PROBE(p, 0);
       LineFFT<T, H, true, N>::run(z, scr + line * G::SMR, t, tw);
+      if (rd == 0) FFST_PROBE(p, 1);
       if (act) {
         const T sr = (r & 1) ? T(-1) : T(1);
 #pragma unroll
@@ -218,7 +245,7 @@ struct K {
   template <int MODE>
   static __device__ void row_r2c(const KParams& p, const C* __restrict__ src_c, const T* __restrict__ src_r,
                                  int c_lo, int ncols, int r0, int cnt, C* dst, int nyq_b, int nyq_idx,
-                                 int nyq_group, C* smem) {
+                                 int nyq_group, C* smem, const int* dep = nullptr, int dep_target = 0) {
     C* scr = smem;
     C* tile = smem + G::SCR_R;
     const int tid = threadIdx.x, line = tid / G::THR, t = tid % G::THR;
@@ -240,28 +267,36 @@ struct K {
         C z[G::ER];
         T trow = T(0);
         const T sr = (r & 1) ? T(-1) : T(1);
+        if constexpr (MODE == MODE_MAIN) {
+          // phase 1: issue all loads of the round; phase 2: split real / imaginary parts
+          C va[G::ER], vb[G::ER];
 #pragma unroll
-        for (int q = 0; q < G::ER; ++q) {
-          const int m1 = 2 * (t + q * G::THR);
-          if (act) {
-            if constexpr (MODE == MODE_MAIN) {
-              C v0, v1;
-              load_pair_cs<T>(src_c + (size_t)r * N + m1, v0, v1);
-              z[q] = mk<T>(v0.x, v1.x);
-              if (nyq) {
-                sacc[q][0] += sr * v0.y;
-                sacc[q][1] += sr * v1.y;
-                trow += v0.y - v1.y;
-              }
+          for (int q = 0; q < G::ER; ++q) {
+            if (act) {
+              load_pair_cs<T>(src_c + (size_t)r * N + 2 * (t + q * G::THR), va[q], vb[q]);
             } else {
-              const cpx<T> v = *reinterpret_cast<const cpx<T>*>(src_r + (size_t)r * N + m1);
-              z[q] = v;
+              va[q] = czero<T>();
+              vb[q] = czero<T>();
             }
-          } else {
-            z[q] = czero<T>();
           }
+#pragma unroll
+          for (int q = 0; q < G::ER; ++q) z[q] = mk<T>(va[q].x, vb[q].x);
+          if (nyq) {
+#pragma unroll
+            for (int q = 0; q < G::ER; ++q) {
+              sacc[q][0] += sr * va[q].y;
+              sacc[q][1] += sr * vb[q].y;
+              trow += va[q].y - vb[q].y;
+            }
+          }
+        } else {
+#pragma unroll
+          for (int q = 0; q < G::ER; ++q)
+            z[q] = act ? *reinterpret_cast<const cpx<T>*>(src_r + (size_t)r * N + 2 * (t + q * G::THR)) : czero<T>();
         }
+        if (ti == 0 && rd == 0) FFST_PROBE(p, 0);
         LineFFT<T, H, false, N>::run(z, scr + line * G::SMR, t, tw);
+        if (ti == 0 && rd == 0) FFST_PROBE(p, 1);
         if (nyq) {
           // alternating row sum t(r) = sum_m1 (-1)^m1 Im c(r, m1), reduced over the line
           T v = trow;
@@ -298,7 +333,9 @@ struct K {
           }
         }
         SyncOf<G::THR>::sync();
+        if (ti == 0 && rd == 0) FFST_PROBE(p, 2);
       }
+      if (dep != nullptr && ti == 0 && tid == 0) spin_wait(dep, dep_target);   // slot reuse: before the first write
       __syncthreads();
       const int rows_here = cnt - ti * G::GR < G::GR ? cnt - ti * G::GR : G::GR;
 #pragma unroll 1
@@ -307,6 +344,7 @@ struct K {
         if (ri < rows_here) dst[(size_t)kk * N + rt0 + ri] = tile[ri * G::TSTR + kk];
       }
       __syncthreads();
+      if (ti == 0) FFST_PROBE(p, 3);
     }
     if (nyq) {
       // partial alternating column sums s(m1) = sum_r (-1)^r Im c(r, m1) over this item's rows
@@ -332,7 +370,7 @@ struct K {
   // ------------------------------------------------------------------ column FFT items
   // inverse pass 2: columns [g0, g0+LPC) of image b over the planes of one chunk:
   // FFT along r of W, * sym_i, summed over planes, written / accumulated into A[b].
-  static __device__ void col_fft_acc(const KParams& p, const ItemDev& I, const ChunkDev& Ch, C* smem) {
+  static __device__ void col_fft_acc(const KParams& p, const ItemDev& I, const PlaneDev* splanes, C* smem) {
     C* scr = smem;
     const int tid = threadIdx.x, line = tid / G::THC, t = tid % G::THC;
     const C* tw = static_cast<const C*>(p.tw);
@@ -342,25 +380,27 @@ struct K {
     const int cb = g0 + line;
     const bool act = cb <= H;
     const int u1 = cb == H ? -H : cb;
-    const C* slot = static_cast<const C*>(p.W) + (size_t)Ch.slot * p.slot_elems;
+    const C* slot = static_cast<const C*>(p.W) + (size_t)I.slot * p.slot_elems;
+    T* wbuf = reinterpret_cast<T*>(smem + G::SCR_C);
     C acc[G::EC];
 #pragma unroll
     for (int q = 0; q < G::EC; ++q) acc[q] = czero<T>();
+    int woff = I.woff;
 #pragma unroll 1
-    for (int u = Ch.unit0; u < Ch.unit0 + Ch.nunits; ++u) {
-      const UnitDev U = p.units[u];
-      const PlaneDev P = p.planes[U.p];
+    for (int u = 0; u < I.np; ++u) {
+      const PlaneDev& P = splanes[I.p + u];
+      const int cur = woff;
+      woff += N * P.ncols_pad;
       if (g1 <= P.c_lo || g0 >= P.c_lo + P.ncols) continue;          // CTA-uniform
       const bool in = act && cb >= P.c_lo && cb < P.c_lo + P.ncols;
-      const C* col = slot + U.woff + (size_t)(cb - P.c_lo) * N;
-      T* wbuf = reinterpret_cast<T*>(smem + G::SCR_C);
+      const C* col = slot + cur + (size_t)(cb - P.c_lo) * N;
+      C r[G::EC];
+#pragma unroll
+      for (int q = 0; q < G::EC; ++q) r[q] = in ? __ldcg(col + t + q * G::THC) : czero<T>();
       if (in) {
 #pragma unroll 1
         for (int q = 0; q < G::EC; ++q) wbuf[q * NT + tid] = window_sym<T>(P, u1, centred(t + q * G::THC, N), H, delta);
       }
-      C r[G::EC];
-#pragma unroll
-      for (int q = 0; q < G::EC; ++q) r[q] = in ? __ldcg(col + t + q * G::THC) : czero<T>();
       LineFFT<T, N, false, N>::run(r, scr + line * G::SMC, t, tw);
       if (in) {
 #pragma unroll
@@ -373,11 +413,11 @@ struct K {
       SyncOf<G::THC>::sync();
     }
     if (act) {
-      C* a = static_cast<C*>(p.A) + ((size_t)Ch.b * (H + 1) + cb) * N;
+      C* a = static_cast<C*>(p.A) + ((size_t)I.b * (H + 1) + cb) * N;
 #pragma unroll
       for (int q = 0; q < G::EC; ++q) {
         const int idx = t + q * G::THC;
-        if (Ch.first_of_image) {
+        if (I.first) {
           a[idx] = acc[q];
         } else {
           const C o = __ldcg(a + idx);
@@ -407,110 +447,123 @@ struct K {
   }
 
   // ------------------------------------------------------------------ persistent kernels
-  static __device__ void fwd_item(const KParams& p, const ItemDev& I, C* smem) {
-    const UnitDev U = p.units[I.unit];
-    const PlaneDev P = p.planes[U.p];
-    const ChunkDev& Ch = p.chunks[I.chunk];
-    C* w = static_cast<C*>(p.W) + (size_t)Ch.slot * p.slot_elems + U.woff;
+  static __device__ void fwd_item(const KParams& p, const ItemDev& I, const PlaneDev* splanes, C* smem) {
+    const PlaneDev& P = splanes[I.p];
+    C* w = static_cast<C*>(p.W) + (size_t)I.slot * p.slot_elems + I.woff;
     if (I.type == 0) {
       const int c0 = P.c_lo + I.group * G::GC;
       const int rem = P.c_lo + P.ncols - c0;
-      const C* Fb = static_cast<const C*>(p.F) + (size_t)U.b * (H + 1) * N;
-      col_ifft<MODE_MAIN>(p, U.b, P, c0, rem < G::GC ? rem : G::GC, Fb, w, P.ncols_pad, c0 - P.c_lo, smem);
+      const C* Fb = static_cast<const C*>(p.F) + (size_t)I.b * (H + 1) * N;
+      col_ifft<MODE_MAIN>(p, I.b, P, c0, rem < G::GC ? rem : G::GC, Fb, w, P.ncols_pad, c0 - P.c_lo, smem,
+                          I.wait_ctr >= 0 ? p.ctr + I.wait_ctr : nullptr, I.wait_tgt);
     } else {
       const int r0 = I.group * G::RP2;
       const int cnt = N - r0 < G::RP2 ? N - r0 : G::RP2;
       const T* nyqG = nullptr;
       const T* nyqH = nullptr;
       if (P.nyq >= 0) {
-        nyqG = static_cast<const T*>(p.nyq_fwd) + ((size_t)U.b * p.n_nyq + P.nyq) * 2 * N;
+        nyqG = static_cast<const T*>(p.nyq_fwd) + ((size_t)I.b * p.n_nyq + P.nyq) * 2 * N;
         nyqH = nyqG + N;
       }
-      C* out = static_cast<C*>(p.coeff) + ((size_t)U.b * p.eta_l + U.p) * N * N;
+      C* out = static_cast<C*>(p.coeff) + ((size_t)I.b * p.eta_l + I.p) * N * N;
       row_c2r<MODE_MAIN>(p, w, P.ncols_pad, P.c_lo, P.ncols, r0, cnt, out, nullptr, nyqG, nyqH, smem);
     }
   }
 
-  static __device__ void inv_item(const KParams& p, const ItemDev& I, C* smem) {
-    const ChunkDev& Ch = p.chunks[I.chunk];
+  static __device__ void inv_item(const KParams& p, const ItemDev& I, const PlaneDev* splanes, C* smem) {
     if (I.type == 0) {
-      const UnitDev U = p.units[I.unit];
-      const PlaneDev P = p.planes[U.p];
-      C* w = static_cast<C*>(p.W) + (size_t)Ch.slot * p.slot_elems + U.woff;
+      const PlaneDev& P = splanes[I.p];
+      C* w = static_cast<C*>(p.W) + (size_t)I.slot * p.slot_elems + I.woff;
       const int r0 = I.group * G::RPI;
       const int cnt = N - r0 < G::RPI ? N - r0 : G::RPI;
-      const C* src = static_cast<const C*>(p.coeff) + ((size_t)U.b * p.eta_l + U.p) * N * N;
-      row_r2c<MODE_MAIN>(p, src, nullptr, P.c_lo, P.ncols, r0, cnt, w, U.b, P.nyq, I.group, smem);
+      const C* src = static_cast<const C*>(p.coeff) + ((size_t)I.b * p.eta_l + I.p) * N * N;
+      row_r2c<MODE_MAIN>(p, src, nullptr, P.c_lo, P.ncols, r0, cnt, w, I.b, P.nyq, I.group, smem,
+                         I.wait_ctr >= 0 ? p.ctr + I.wait_ctr : nullptr, I.wait_tgt);
     } else {
-      col_fft_acc(p, I, Ch, smem);
+      col_fft_acc(p, I, splanes, smem);
     }
   }
 };
 
-template <typename T, int N>
-__global__ void __launch_bounds__(256, 2) fwd_main_kernel(KParams p) {
+// Persistent schedulers.  Thread 0 fetches the next item index one item ahead; pass-1 items
+// wait for their ring slot only before writing it (inside the item); pass-2 items wait for the
+// pass-1 items of their chunk (and, inverse, for the previous owner of their column group).
+// Release fences are issued only by items whose writes another item reads (pass 1, and the
+// inverse's accumulator chain); forward pass 2 writes only the cube, read by nobody in the kernel.
+constexpr int MAX_PLANES_SMEM = 256;
+
+__device__ __forceinline__ ItemDev load_item(const ItemDev* items, int it) {
+  const int4* src = reinterpret_cast<const int4*>(items + it);
+  ItemDev I;
+  int4* dst = reinterpret_cast<int4*>(&I);
+  dst[0] = __ldg(src);
+  dst[1] = __ldg(src + 1);
+  dst[2] = __ldg(src + 2);
+  dst[3] = __ldg(src + 3);
+  return I;
+}
+
+// Persistent scheduler shared by both directions.  Thread 0 fetches the next item index one item
+// ahead.  Pass-1 items wait for their ring slot inside the item (just before writing it); pass-2
+// items wait for the pass-1 items of their chunk (and, inverse, the previous owner of their column
+// group).  Release fences only where another item reads what this item wrote (every item but the
+// forward pass 2, whose output -- the cube -- nobody reads inside the kernel).
+template <typename T, int N, bool FWD>
+__device__ __forceinline__ void persistent_loop(const KParams& p) {
   extern __shared__ __align__(16) unsigned char smem_raw[];
   cpx<T>* smem = reinterpret_cast<cpx<T>*>(smem_raw);
-  __shared__ int s_item;
+  __shared__ int s_item[2];
+  __shared__ PlaneDev s_planes[MAX_PLANES_SMEM];
+  for (int i = threadIdx.x; i < p.eta_l; i += blockDim.x) s_planes[i] = p.planes[i];
+  if (threadIdx.x == 0) {
+    s_item[0] = atomicAdd(p.ctr, 1);
+    s_probe[0] = s_probe[1] = s_probe[2] = s_probe[3] = 0;
+  }
+  int cur = 0;
   for (;;) {
-    if (threadIdx.x == 0) s_item = atomicAdd(p.ctr, 1);
     __syncthreads();
-    const int it = s_item;
+    const int it = s_item[cur];
     if (it >= p.n_items) break;
-    const ItemDev I = p.items[it];
-    if (threadIdx.x == 0) {
-      const ChunkDev& Ch = p.chunks[I.chunk];
-      if (I.type == 0) {
-        if (Ch.prev_slot_chunk >= 0)
-          spin_wait(p.ctr + p.ctr_p2 + Ch.prev_slot_chunk, p.chunks[Ch.prev_slot_chunk].p2_items);
-      } else {
-        spin_wait(p.ctr + p.ctr_p1 + I.chunk, Ch.p1_items);
+    if (threadIdx.x == 0) s_item[cur ^ 1] = atomicAdd(p.ctr, 1);
+    const ItemDev I = load_item(p.items, it);
+    unsigned long long t_start = 0, t_ready = 0;
+    if (p.trace != nullptr && threadIdx.x == 0) t_start = gtimer();
+    if (I.type == 1) {
+      if (threadIdx.x == 0) {
+        spin_wait(p.ctr + I.wait_ctr, I.wait_tgt);
+        if (I.wait2_ctr >= 0) spin_wait(p.ctr + I.wait2_ctr, 1);
       }
+      __syncthreads();
     }
-    __syncthreads();
-    K<T, N>::fwd_item(p, I, smem);
+    if (p.trace != nullptr && threadIdx.x == 0) t_ready = gtimer();
+    if constexpr (FWD) K<T, N>::fwd_item(p, I, s_planes, smem);
+    else K<T, N>::inv_item(p, I, s_planes, smem);
     __syncthreads();
     if (threadIdx.x == 0) {
-      __threadfence();
-      atomicAdd(p.ctr + (I.type == 0 ? p.ctr_p1 : p.ctr_p2) + I.chunk, 1);
+      if (!FWD || I.type == 0) __threadfence();
+      atomicAdd(p.ctr + I.sig_ctr, 1);
+      if (I.sig2_ctr >= 0) atomicAdd(p.ctr + I.sig2_ctr, 1);
     }
+    if (p.trace != nullptr && threadIdx.x == 0) {
+      unsigned long long* tr = p.trace + 8 * (size_t)it;
+      tr[0] = smid();
+      tr[1] = t_start;
+      tr[2] = t_ready;
+      tr[3] = gtimer();
+      tr[4] = s_probe[0]; tr[5] = s_probe[1]; tr[6] = s_probe[2]; tr[7] = s_probe[3];
+    }
+    cur ^= 1;
   }
 }
 
 template <typename T, int N>
+__global__ void __launch_bounds__(256, 2) fwd_main_kernel(KParams p) {
+  persistent_loop<T, N, true>(p);
+}
+
+template <typename T, int N>
 __global__ void __launch_bounds__(256, 2) inv_main_kernel(KParams p) {
-  extern __shared__ __align__(16) unsigned char smem_raw[];
-  cpx<T>* smem = reinterpret_cast<cpx<T>*>(smem_raw);
-  __shared__ int s_item;
-  for (;;) {
-    if (threadIdx.x == 0) s_item = atomicAdd(p.ctr, 1);
-    __syncthreads();
-    const int it = s_item;
-    if (it >= p.n_items) break;
-    const ItemDev I = p.items[it];
-    if (threadIdx.x == 0) {
-      const ChunkDev& Ch = p.chunks[I.chunk];
-      if (I.type == 0) {
-        if (Ch.prev_slot_chunk >= 0)
-          spin_wait(p.ctr + p.ctr_p2 + Ch.prev_slot_chunk, p.chunks[Ch.prev_slot_chunk].p2_items);
-      } else {
-        spin_wait(p.ctr + p.ctr_p1 + I.chunk, Ch.p1_items);
-        if (I.dep >= 0) spin_wait(p.ctr + p.ctr_g + I.dep, 1);
-      }
-    }
-    __syncthreads();
-    K<T, N>::inv_item(p, I, smem);
-    __syncthreads();
-    if (threadIdx.x == 0) {
-      __threadfence();
-      if (I.type == 0) {
-        atomicAdd(p.ctr + p.ctr_p1 + I.chunk, 1);
-      } else {
-        atomicAdd(p.ctr + p.ctr_g + I.self, 1);
-        atomicAdd(p.ctr + p.ctr_p2 + I.chunk, 1);
-      }
-    }
-  }
+  persistent_loop<T, N, false>(p);
 }
 
 // ---------------------------------------------------------------------- auxiliary kernels

@@ -177,6 +177,26 @@ class Plan:
         check(lib.ffst_plan_phase_times(self._h, t, n), "ffst_plan_phase_times")
         return tuple(t), tuple(n)
 
+    def set_trace(self, enable: bool = True):
+        check(lib.ffst_plan_set_trace(self._h, int(bool(enable))), "ffst_plan_set_trace")
+
+    def trace(self, which: int, batch: int | None = None):
+        """Per-item records of the last call: numpy array (items, 10) =
+        [type, chunk, smid, t_start, t_ready, t_end, probe0..probe3] (ns)."""
+        import numpy as np
+        b = self.batch if batch is None else batch
+        cap = 1 << 22
+        buf = (C.c_ulonglong * (8 * cap))()
+        n = C.c_int()
+        check(lib.ffst_plan_trace(self._h, int(which), int(b), buf, cap, C.byref(n)), "ffst_plan_trace")
+        a = np.ctypeslib.as_array(buf)[: 8 * n.value].reshape(-1, 8).copy()
+        out = np.zeros((n.value, 10), dtype=np.int64)
+        out[:, 0] = (a[:, 0] >> 32) & 0xFF
+        out[:, 1] = a[:, 0] >> 40
+        out[:, 2] = a[:, 0] & 0xFFFFFFFF
+        out[:, 3:] = a[:, 1:].astype(np.int64)
+        return out
+
     def workspace_bytes(self) -> int:
         v = C.c_size_t()
         check(lib.ffst_plan_workspace_bytes(self._h, C.byref(v)), "ffst_plan_workspace_bytes")
