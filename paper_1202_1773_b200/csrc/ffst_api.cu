@@ -101,14 +101,50 @@ void plane_columns(int n, int j0, const Triple& tr, int* lo, int* hi) {
   *hi = std::max(hhi, vhi);
 }
 
+// Radial factor table (float64): rows j < j0: psi1_hat(4^-j Delta a) by the closed form of
+// P:L1824-1835; row j0: varphi(Delta a); a = 0 .. n/2.
+std::vector<double> radial_table(int n, int j0) {
+  const int H = n / 2;
+  const double delta = grid_delta(n, j0);
+  const double pi = 3.14159265358979323846;
+  auto v = [](double x) {
+    if (x <= 0) return 0.0;
+    if (x >= 1) return 1.0;
+    const bool refl = x > 0.5;
+    const double y = refl ? 1 - x : x, y2 = y * y;
+    const double p = y2 * y2 * (35 + y * (-84 + y * (70 - 20 * y)));
+    return refl ? 1 - p : p;
+  };
+  std::vector<double> t((size_t)(j0 + 1) * (H + 1));
+  for (int j = 0; j <= j0; ++j)
+    for (int a = 0; a <= H; ++a) {
+      double val;
+      if (j < j0) {
+        const double x = std::ldexp(delta * a, -2 * j);
+        if (x <= 0.5 || x >= 4) val = 0;
+        else if (x < 1) val = std::sin(pi / 2 * v(2 * x - 1));
+        else if (x <= 2) val = 1;
+        else val = std::cos(pi / 2 * v(x / 2 - 1));
+      } else {
+        const double x = delta * a;
+        if (x <= 0.5) val = 1;
+        else if (x >= 1) val = 0;
+        else val = std::cos(pi / 2 * v(2 * x - 1));
+      }
+      t[(size_t)j * (H + 1) + a] = val;
+    }
+  return t;
+}
+
 bool plane_nyquist(int n, int j0, const Triple& tr) {
   PlaneDev P{};
   P.kind = tr.kind; P.j = tr.j; P.k = tr.k;
   const int H = n / 2;
-  const double delta = grid_delta(n, j0);
+  const std::vector<double> tab = radial_table(n, j0);
+  const Radial<double> R{tab.data(), H + 1, j0};
   for (int u = -H; u < H; ++u) {
-    if (window_anti<double>(P, u, -H, H, delta) != 0.0) return true;
-    if (window_anti<double>(P, -H, u, H, delta) != 0.0) return true;
+    if (window_anti<double>(P, u, -H, H, R) != 0.0) return true;
+    if (window_anti<double>(P, -H, u, H, R) != 0.0) return true;
   }
   return false;
 }
@@ -141,6 +177,7 @@ struct ffst_plan {
   PlaneDev* d_planes = nullptr;
   int* d_nyq = nullptr;
   void* d_tw = nullptr;
+  void* d_rtab = nullptr;
   void *F = nullptr, *Fscr = nullptr, *A = nullptr, *W = nullptr;
   long long W_elems = 0;
   void *nyq_fwd = nullptr, *nyq_S = nullptr, *nyq_T = nullptr, *corr = nullptr;
@@ -400,6 +437,7 @@ KParams base_params(ffst_plan* p) {
   k.planes = p->d_planes;
   k.nyq_planes = p->d_nyq;
   k.tw = p->d_tw;
+  k.rtab = p->d_rtab;
   k.F = p->F; k.Fscr = p->Fscr; k.A = p->A; k.W = p->W;
   k.nyq_fwd = p->nyq_fwd; k.nyq_S = p->nyq_S; k.nyq_T = p->nyq_T; k.corr = p->corr;
   k.n_rowitems = p->n_rowitems;
@@ -684,6 +722,7 @@ ffst_status ffst_plan_create(ffst_plan** out, const ffst_plan_desc* d) {
   ALLOC(p->d_planes, p->planes.size() * sizeof(PlaneDev));
   ALLOC(p->d_nyq, nn * sizeof(int));
   ALLOC(p->d_tw, N * csz);
+  ALLOC(p->d_rtab, (size_t)(j0 + 1) * H1 * p->rsz);
   ALLOC(p->F, B * H1 * N * csz);
   ALLOC(p->Fscr, B * std::max(H1 * N, N * ncpf) * csz);
   ALLOC(p->A, B * H1 * N * csz);
@@ -697,6 +736,15 @@ ffst_status ffst_plan_create(ffst_plan** out, const ffst_plan_desc* d) {
   std::vector<unsigned char> tw;
   if (d->dtype == FFST_F32) fill_twiddles<float>(tw, d->n); else fill_twiddles<double>(tw, d->n);
   e = cudaMemcpy(p->d_tw, tw.data(), tw.size(), cudaMemcpyHostToDevice);
+  {
+    const std::vector<double> rt = radial_table(d->n, j0);
+    if (d->dtype == FFST_F32) {
+      std::vector<float> rf(rt.begin(), rt.end());
+      if (e == cudaSuccess) e = cudaMemcpy(p->d_rtab, rf.data(), rf.size() * sizeof(float), cudaMemcpyHostToDevice);
+    } else if (e == cudaSuccess) {
+      e = cudaMemcpy(p->d_rtab, rt.data(), rt.size() * sizeof(double), cudaMemcpyHostToDevice);
+    }
+  }
   if (e == cudaSuccess) e = cudaMemcpy(p->d_planes, p->planes.data(), p->planes.size() * sizeof(PlaneDev), cudaMemcpyHostToDevice);
   if (e == cudaSuccess && !p->nyq.empty()) e = cudaMemcpy(p->d_nyq, p->nyq.data(), p->nyq.size() * sizeof(int), cudaMemcpyHostToDevice);
   if (e == cudaSuccess) e = cudaMemset(p->nyq_S, 0, B * nn * p->n_rowitems * N * p->rsz);

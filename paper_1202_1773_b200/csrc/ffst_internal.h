@@ -48,6 +48,7 @@ struct KParams {
   const PlaneDev* planes;       // [eta_l]
   const int* nyq_planes;        // [n_nyq] local plane index of each Nyquist plane
   const void* tw;               // cpx<T>[n]: exp(-2 pi i m / n)
+  const void* rtab;             // T[(j0+1)][n/2+1]: radial factors psi1(4^-j Delta a), varphi(Delta a)
   const void* img;              // [batch][n][n] T
   void* coeff;                  // [batch][eta_l][n][n] cpx<T>
   void* img_out;                // [batch][n][n] T

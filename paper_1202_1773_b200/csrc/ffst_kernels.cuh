@@ -118,6 +118,7 @@ struct K {
     const int tid = threadIdx.x, line = tid / G::THC, t = tid % G::THC;
     const C* tw = static_cast<const C*>(p.tw);
     const T delta = (T)p.delta;
+    const Radial<T> R{static_cast<const T*>(p.rtab), N / 2 + 1, p.j0};
     constexpr int ROUNDS = G::GC / G::LPC > 0 ? G::GC / G::LPC : 1;
 #pragma unroll 1
     for (int rd = 0; rd < ROUNDS; ++rd) {
@@ -129,9 +130,14 @@ struct K {
       C r[G::EC];
       if constexpr (MODE == MODE_MAIN) {
         T* wbuf = reinterpret_cast<T*>(tile + G::TILE_C);
-#pragma unroll 1
-        for (int q = 0; q < G::EC; ++q)
-          wbuf[q * NT + tid] = act ? window_sym<T>(P, u1, centred(t + q * G::THC, N), H, delta) : T(0);
+        const ColBounds bnd = col_bounds<T>(P, u1, H, delta);
+#pragma unroll 2
+        for (int q = 0; q < G::EC; ++q) {
+          const int rb = t + q * G::THC, u2 = centred(rb, N);
+          const bool cand = act && (cb == H || rb == H || col_candidate(bnd, u2));
+          wbuf[q * NT + tid] = cand ? window_sym<T>(P, u1, u2, H, R) : T(0);
+        }
+        if (rd == 0) FFST_PROBE(p, 0);
 #pragma unroll
         for (int q = 0; q < G::EC; ++q) {
           const T w = wbuf[q * NT + tid];
@@ -141,7 +147,9 @@ struct K {
 #pragma unroll
         for (int q = 0; q < G::EC; ++q) r[q] = act ? __ldcg(col + t + q * G::THC) : czero<T>();
       }
+      if (rd == 0) FFST_PROBE(p, 1);
       LineFFT<T, N, true, N>::run(r, scr + line * G::SMC, t, tw);
+      if (rd == 0) FFST_PROBE(p, 2);
       if (ci < G::GC) {
 #pragma unroll
         for (int q = 0; q < G::EC; ++q) tile[(t + q * G::THC) * G::GCP + ci] = r[q];
@@ -153,6 +161,7 @@ struct K {
       __syncthreads();
     }
     const int ncopy = cnt < G::GC ? cnt : G::GC;
+    FFST_PROBE(p, 3);
 #pragma unroll 1
     for (int e = tid; e < N * G::GC; e += NT) {
       const int rr = e / G::GC, ci = e - rr * G::GC;
@@ -375,6 +384,7 @@ struct K {
     const int tid = threadIdx.x, line = tid / G::THC, t = tid % G::THC;
     const C* tw = static_cast<const C*>(p.tw);
     const T delta = (T)p.delta;
+    const Radial<T> R{static_cast<const T*>(p.rtab), N / 2 + 1, p.j0};
     const int g0 = I.group * G::LPC;
     const int g1 = g0 + G::LPC < H + 1 ? g0 + G::LPC : H + 1;
     const int cb = g0 + line;
@@ -398,8 +408,13 @@ struct K {
 #pragma unroll
       for (int q = 0; q < G::EC; ++q) r[q] = in ? __ldcg(col + t + q * G::THC) : czero<T>();
       if (in) {
-#pragma unroll 1
-        for (int q = 0; q < G::EC; ++q) wbuf[q * NT + tid] = window_sym<T>(P, u1, centred(t + q * G::THC, N), H, delta);
+        const ColBounds bnd = col_bounds<T>(P, u1, H, delta);
+#pragma unroll 2
+        for (int q = 0; q < G::EC; ++q) {
+          const int rb = t + q * G::THC, u2 = centred(rb, N);
+          const bool cand = cb == H || rb == H || col_candidate(bnd, u2);
+          wbuf[q * NT + tid] = cand ? window_sym<T>(P, u1, u2, H, R) : T(0);
+        }
       }
       LineFFT<T, N, false, N>::run(r, scr + line * G::SMC, t, tw);
       if (in) {
@@ -641,6 +656,7 @@ __global__ void __launch_bounds__(256) nyq_fwd_kernel(KParams p) {
   if (act) P = p.planes[p.nyq_planes[nq]];
   const C* F = static_cast<const C*>(p.F) + (size_t)b * (H + 1) * N;
   const T delta = (T)p.delta;
+  const Radial<T> R{static_cast<const T*>(p.rtab), N / 2 + 1, p.j0};
   C r[G::EC];
 #pragma unroll 1
   for (int q = 0; q < G::EC; ++q) {
@@ -649,10 +665,10 @@ __global__ void __launch_bounds__(256) nyq_fwd_kernel(KParams p) {
     if (act) {
       const int u = centred(bin, N);
       if (which == 0) {
-        const T a = window_anti<T>(P, u, -H, H, delta);
+        const T a = window_anti<T>(P, u, -H, H, R);
         if (a != T(0)) v = cscale<T>(bin <= H ? F[(size_t)bin * N + H] : conj_<T>(F[(size_t)(N - bin) * N + H]), a);
       } else {
-        const T a = window_anti<T>(P, -H, u, H, delta);
+        const T a = window_anti<T>(P, -H, u, H, R);
         if (a != T(0)) v = cscale<T>(F[(size_t)H * N + bin], a);
       }
     }
@@ -683,6 +699,7 @@ __global__ void __launch_bounds__(256) nyq_inv_kernel(KParams p) {
   C* scr = reinterpret_cast<C*>(smem_raw) + line * G::SMC;
   C* stage = reinterpret_cast<C*>(smem_raw) + G::SCR_C;          // [EC][NT] (also the reduction buffer)
   const T delta = (T)p.delta;
+  const Radial<T> R{static_cast<const T*>(p.rtab), N / 2 + 1, p.j0};
   C acc[G::EC];
 #pragma unroll
   for (int q = 0; q < G::EC; ++q) acc[q] = czero<T>();
@@ -712,7 +729,7 @@ __global__ void __launch_bounds__(256) nyq_inv_kernel(KParams p) {
 #pragma unroll 1
       for (int q = 0; q < G::EC; ++q) {
         const int u = centred(t + q * G::THC, N);
-        stage[q * G::NT + tid].x = which == 0 ? window_anti<T>(P, u, -H, H, delta) : window_anti<T>(P, -H, u, H, delta);
+        stage[q * G::NT + tid].x = which == 0 ? window_anti<T>(P, u, -H, H, R) : window_anti<T>(P, -H, u, H, R);
       }
 #pragma unroll
       for (int q = 0; q < G::EC; ++q) {
@@ -750,6 +767,7 @@ template <typename T, int N>
 __global__ void spectra_kernel(KParams p, T* psi, int centred_layout) {
   const size_t total = (size_t)p.eta_l * N * N;
   const T delta = (T)p.delta;
+  const Radial<T> R{static_cast<const T*>(p.rtab), N / 2 + 1, p.j0};
   for (size_t e = blockIdx.x * (size_t)blockDim.x + threadIdx.x; e < total; e += (size_t)gridDim.x * blockDim.x) {
     const int i = (int)(e / ((size_t)N * N));
     const int rem = (int)(e - (size_t)i * N * N);
@@ -762,7 +780,7 @@ __global__ void spectra_kernel(KParams p, T* psi, int centred_layout) {
       u1 = centred(col, N);
       u2 = centred(row, N);
     }
-    psi[e] = window<T>(p.planes[i], u1, u2, delta);
+    psi[e] = window<T>(p.planes[i], u1, u2, R);
   }
 }
 

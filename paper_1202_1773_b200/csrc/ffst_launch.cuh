@@ -8,9 +8,10 @@ template <typename T> struct MaxN;
 template <> struct MaxN<float> { static constexpr int v = 4096; };
 template <> struct MaxN<double> { static constexpr int v = 2048; };
 
+// Opt in to the dynamic shared memory a kernel needs (always: static + dynamic may exceed
+// the 48 KB default even when the dynamic part alone does not).
 template <typename K>
 static cudaError_t set_smem(K kernel, size_t bytes) {
-  if (bytes <= 48 * 1024) return cudaSuccess;
   return cudaFuncSetAttribute(kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)bytes);
 }
 

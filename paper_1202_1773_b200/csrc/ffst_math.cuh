@@ -95,52 +95,110 @@ struct PlaneDev {
   int nyq;           // index among the plan's Nyquist planes, or -1
 };
 
+// Radial factors.  psi1_hat(4^-j Delta a) and varphi(Delta a) depend only on the integer
+// radius a = |u| (0 <= a <= n/2) and the scale: a per-plan (j0+1) x (n/2+1) table holds them
+// (computed once in float64 from the closed forms above).  The 2-D window --
+// cones, seam glue and the shear factor psi2 -- is still evaluated on the fly per element.
+template <typename T> struct Radial {
+  const T* tab;   // rows j < j0: psi1(4^-j Delta a); row j0: varphi(Delta a)
+  int stride;     // n/2 + 1
+  int j0;
+  FFST_HD T ld(const T* a) const {
+#ifdef __CUDA_ARCH__
+    return __ldg(a);
+#else
+    return *a;
+#endif
+  }
+  FFST_HD T psi1(int j, int a) const { return ld(tab + j * stride + a); }
+  FFST_HD T phi(int a) const { return ld(tab + j0 * stride + a); }
+};
+
 // psi1_hat(4^-j Delta |ua|) psi2_hat((k ua + 2^j ub)/ua) for |ub| <= |ua| (cone shearlet,
-// P:L845-848); `rscale` = 4^-j * Delta.
-template <typename T> FFST_HD T cone_shearlet(int j, int k, int ua, int ub, T rscale) {
+// P:L845-848).
+template <typename T> FFST_HD T cone_shearlet(int j, int k, int ua, int ub, const Radial<T>& R) {
   const int aa = ua < 0 ? -ua : ua;
   if (aa == 0) return T(0);                              // reading A5: 0 on w_a = 0
   const int num = k * ua + ub * (1 << j);                // exact (|num| < 2^24)
   const int anum = num < 0 ? -num : num;
   if (anum >= aa) return T(0);                           // |shear argument| >= 1 -> psi2 = 0
-  const T r = psi1_w<T>(rscale * T(aa));
+  const T r = R.psi1(j, aa);
   if (r == T(0)) return T(0);
   const T t = T(aa - anum) / T(aa);                      // 1 - |argument|, one rounding
   return r * sqrt(meyer_v<T>(t));                        // psi2 = sqrt(v(1 - |x|))
 }
 
 // psi_hat_i(Delta u1, Delta u2) for integer u (u may be +n/2: the mirrored point).
-template <typename T> FFST_HD T window(const PlaneDev& P, int u1, int u2, T delta) {
+template <typename T> FFST_HD T window(const PlaneDev& P, int u1, int u2, const Radial<T>& R) {
   const int a1 = u1 < 0 ? -u1 : u1, a2 = u2 < 0 ? -u2 : u2;
-  if (P.kind == 0) {                                     // eq:phi
-    return varphi_w<T>(delta * T(a2 <= a1 ? a1 : a2));
-  }
-  const T rs = delta * (T(1) / T(1 << (2 * P.j)));       // 4^-j Delta, exact
+  if (P.kind == 0) return R.phi(a2 <= a1 ? a1 : a2);     // eq:phi
   if (P.kind == 1) {                                     // horizontal cone |u2| < |u1|
-    return a2 < a1 ? cone_shearlet<T>(P.j, P.k, u1, u2, rs) : T(0);
+    return a2 < a1 ? cone_shearlet<T>(P.j, P.k, u1, u2, R) : T(0);
   }
   if (P.kind == 2) {                                     // vertical cone |u1| < |u2|
-    return a1 < a2 ? cone_shearlet<T>(P.j, P.k, u2, u1, rs) : T(0);
+    return a1 < a2 ? cone_shearlet<T>(P.j, P.k, u2, u1, R) : T(0);
   }
   // glued seam shearlet: h on C^h, v on C^v, horizontal formula on the seam |u1| = |u2|
-  if (a1 < a2) return cone_shearlet<T>(P.j, P.k, u2, u1, rs);
-  return cone_shearlet<T>(P.j, P.k, u1, u2, rs);
+  if (a1 < a2) return cone_shearlet<T>(P.j, P.k, u2, u1, R);
+  return cone_shearlet<T>(P.j, P.k, u1, u2, R);
 }
 
 // Point-symmetric part of the sampled window on the even grid:
 // sym(u) = (w(u) + w(mirror u)) / 2 with w(mirror u) = psi(Delta u^), u^ = u with any
 // -n/2 component replaced by +n/2 (psi is even).  anti = (w(u) - w(u^)) / 2 lives on the
 // Nyquist row / column only.
-template <typename T> FFST_HD T window_sym(const PlaneDev& P, int u1, int u2, int half, T delta) {
-  const T w = window<T>(P, u1, u2, delta);
+template <typename T> FFST_HD T window_sym(const PlaneDev& P, int u1, int u2, int half, const Radial<T>& R) {
+  const T w = window<T>(P, u1, u2, R);
   if (u1 != -half && u2 != -half) return w;
   const int e1 = u1 == -half ? half : u1, e2 = u2 == -half ? half : u2;
-  return T(0.5) * (w + window<T>(P, e1, e2, delta));
+  return T(0.5) * (w + window<T>(P, e1, e2, R));
 }
-template <typename T> FFST_HD T window_anti(const PlaneDev& P, int u1, int u2, int half, T delta) {
+template <typename T> FFST_HD T window_anti(const PlaneDev& P, int u1, int u2, int half, const Radial<T>& R) {
   if (u1 != -half && u2 != -half) return T(0);
   const int e1 = u1 == -half ? half : u1, e2 = u2 == -half ? half : u2;
-  return T(0.5) * (window<T>(P, u1, u2, delta) - window<T>(P, e1, e2, delta));
+  return T(0.5) * (window<T>(P, u1, u2, R) - window<T>(P, e1, e2, R));
+}
+
+// Candidate rows of plane P in column u1 (a prefilter for the window evaluation; a superset of
+// the rows where window_sym can be non-zero, from the same integer tests):
+//   h part: the wedge |k u1 + 2^j u2| < |u1| is the open interval of u2 strictly between
+//           (-|u1| - k u1)/2^j and (|u1| - k u1)/2^j;
+//   v part: |u1| < |u2| and the radial band 1/2 < 4^-j Delta |u2| < 4;
+//   low-pass: max(|u1|, |u2|) < 1/Delta.
+struct ColBounds {
+  int hlo, hhi;   // u2 interval (inclusive), empty if hlo > hhi
+  int alo, ahi;   // |u2| interval (inclusive), empty if alo > ahi
+};
+
+FFST_HD int floordiv_(int a, int b) { return a >= 0 ? a / b : -((-a + b - 1) / b); }
+
+template <typename T> FFST_HD ColBounds col_bounds(const PlaneDev& P, int u1, int half, T delta) {
+  ColBounds b{1, 0, 1, 0};
+  const int a1 = u1 < 0 ? -u1 : u1;
+  if (P.kind == 0) {
+    const int A = (int)(T(1) / delta) + 1;
+    if (a1 <= A) { b.hlo = -A; b.hhi = A; }
+    return b;
+  }
+  const T s = delta * (T(1) / T(1 << (2 * P.j)));
+  const int band_lo = (int)(T(0.5) / s), band_hi = (int)(T(4) / s) + 1;
+  if ((P.kind == 1 || P.kind == 3) && a1 > 0 && a1 >= band_lo && a1 <= band_hi) {
+    const int K = 1 << P.j, c = P.k * u1;
+    b.hlo = floordiv_(-a1 - c, K);
+    b.hhi = floordiv_(a1 - c, K) + 1;
+    if (b.hlo < -a1) b.hlo = -a1;
+    if (b.hhi > a1) b.hhi = a1;
+  }
+  if (P.kind == 2 || P.kind == 3) {
+    b.alo = a1 > band_lo ? a1 : band_lo;
+    b.ahi = band_hi < half ? band_hi : half;
+  }
+  return b;
+}
+
+FFST_HD bool col_candidate(const ColBounds& b, int u2) {
+  const int a2 = u2 < 0 ? -u2 : u2;
+  return (u2 >= b.hlo && u2 <= b.hhi) || (a2 >= b.alo && a2 <= b.ahi);
 }
 
 // natural FFT bin -> centred frequency in [-n/2, n/2)
