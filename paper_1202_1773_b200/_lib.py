@@ -9,7 +9,10 @@ from __future__ import annotations
 import ctypes as C
 from pathlib import Path
 
-LIB_PATH = Path(__file__).resolve().parent / "libffst.so"
+import os
+
+# FFST_LIB: an alternative in-tree build of the same library (experiments); default libffst.so
+LIB_PATH = Path(os.environ.get("FFST_LIB", str(Path(__file__).resolve().parent / "libffst.so")))
 
 if not LIB_PATH.exists():
     raise ImportError(f"{LIB_PATH} is missing: run `python -c 'import __graft_entry__ as g; g.build()'` "

@@ -136,6 +136,36 @@ std::vector<double> radial_table(int n, int j0) {
   return t;
 }
 
+// Column records of the warp path (ColRec, ffst_math.cuh): hulls of the rows where sym_i is
+// non-zero in each Hermitian-half column of the plane, found by evaluating the window (float64)
+// on the whole column, widened by one row; plus the horizontal radial factor and 1/|u1|.
+template <typename T>
+void column_records(int n, int j0, PlaneDev& P, std::vector<ColRec<T>>& out) {
+  const int H = n / 2;
+  const std::vector<double> tab = radial_table(n, j0);
+  const Radial<double> R{tab.data(), H + 1, j0};
+  P.rec = (int)out.size();
+  for (int c = P.c_lo; c < P.c_lo + P.ncols; ++c) {
+    const int u1 = c == H ? -H : c, a1 = std::abs(u1);
+    int lo[3] = {H + 1, H + 1, H + 1}, hi[3] = {-H - 2, -H - 2, -H - 2};
+    for (int u2 = -H; u2 < H; ++u2) {
+      if (window_sym<double>(P, u1, u2, H, R) == 0.0) continue;
+      const int r = std::abs(u2) <= a1 ? 0 : (u2 > 0 ? 1 : 2);
+      lo[r] = std::min(lo[r], u2);
+      hi[r] = std::max(hi[r], u2);
+    }
+    ColRec<T> rc{};
+    for (int r = 0; r < 3; ++r) {
+      if (lo[r] > hi[r]) { rc.lo[r] = 1; rc.hi[r] = 0; continue; }
+      rc.lo[r] = std::max(-H, lo[r] - 1);
+      rc.hi[r] = std::min(H - 1, hi[r] + 1);
+    }
+    rc.rh = (P.kind == 1 || P.kind == 3) ? (T)tab[(size_t)P.j * (H + 1) + a1] : T(0);
+    rc.inv_a1 = a1 > 0 ? (T)(1.0 / a1) : T(0);
+    out.push_back(rc);
+  }
+}
+
 bool plane_nyquist(int n, int j0, const Triple& tr) {
   PlaneDev P{};
   P.kind = tr.kind; P.j = tr.j; P.k = tr.k;
@@ -152,6 +182,7 @@ bool plane_nyquist(int n, int j0, const Triple& tr) {
 struct Queue {
   int batch = 0;
   int n_chunks = 0, n_fwd = 0, n_inv = 0, n_g = 0;
+  int batch_fwd = 1, batch_inv = 1;   // largest safe per-CTA fetch batch (dependency distance)
   long long slot_elems = 0;
   int nslots = 0;
   UnitDev* d_units = nullptr;
@@ -171,6 +202,8 @@ struct ffst_plan {
   std::vector<int> nyq;
   Geometry geo{};
   int sm_count = 0, grid_fwd = 0, grid_inv = 0;
+  bool warp = false;              // warp-worker kernels (ffst_warp.cuh), n <= 512
+  int workers = 0;                // concurrent item consumers (warps or CTAs) of the persistent kernels
   long long slot_budget = 0;
   int chunk_planes = 4;           // max planes per chunk (pipelining granularity of the passes)
   // device memory
@@ -178,6 +211,7 @@ struct ffst_plan {
   int* d_nyq = nullptr;
   void* d_tw = nullptr;
   void* d_rtab = nullptr;
+  void* d_colrec = nullptr;       // warp path column records (ColRec<T>)
   void *F = nullptr, *Fscr = nullptr, *A = nullptr, *W = nullptr;
   long long W_elems = 0;
   void *nyq_fwd = nullptr, *nyq_S = nullptr, *nyq_T = nullptr, *corr = nullptr;
@@ -272,7 +306,7 @@ ffst_status build_queue(ffst_plan* p, int batch, Queue** out) {
     slot = std::max(slot, c.elems);
   }
   avg_items /= (double)protos.size();
-  const int grid = std::max(p->grid_fwd, p->grid_inv);
+  const int grid = p->workers;
   int D = (int)std::ceil(3.0 * grid / std::max(1.0, avg_items));
   D = std::max(1, std::min(D, (int)protos.size()));
   const long long slot_elems = (slot + 63) / 64 * 64;
@@ -346,6 +380,10 @@ ffst_status build_queue(ffst_plan* p, int batch, Queue** out) {
       int& last = last_self[(size_t)ch.b * ngroups + gg];
       ItemDev it = mk_item(1, c, gg, ch.b, units[ch.unit0].p, ch.nunits, units[ch.unit0].woff, ch.slot);
       it.first = ch.first_of_image;
+      for (int u = ch.unit0; u < ch.unit0 + ch.nunits; ++u) {
+        const PlaneDev& P = p->planes[units[u].p];
+        if (g1 > P.c_lo && g0 < P.c_lo + P.ncols) it.pad0 |= 1 << (u - ch.unit0);
+      }
       it.wait2_ctr = last >= 0 ? 1 + 2 * C + last : -1;
       it.sig2_ctr = 1 + 2 * C + n_self;
       i2[c].push_back(it);
@@ -385,6 +423,42 @@ ffst_status build_queue(ffst_plan* p, int batch, Queue** out) {
   std::vector<ItemDev> fwd, inv;
   emit(f1, f2, fwd);
   emit(i1, i2, inv);
+  // FFST_QUEUE_ONLY=1 / 2 (measurement only; results are wrong): keep only the pass-1 / pass-2
+  // items, dependencies removed, to time each pass type alone
+  if (const char* only = std::getenv("FFST_QUEUE_ONLY")) {
+    const int keep = std::atoi(only) - 1;
+    for (auto* q : {&fwd, &inv}) {
+      std::vector<ItemDev> k;
+      for (auto it : *q)
+        if (it.type == keep) {
+          it.wait_ctr = 0; it.wait_tgt = 0; it.wait2_ctr = -1;
+          k.push_back(it);
+        }
+      *q = k;
+    }
+  }
+  // Smallest distance (in queue positions) between an item and the last item it depends on:
+  // a CTA may take that many consecutive items per fetch without deadlock (an item's
+  // dependencies are then always held by other fetches).
+  auto min_slack = [&](const std::vector<ItemDev>& q) {
+    std::map<int, int> last_sig;                  // counter -> last queue position signalling it
+    for (int i = 0; i < (int)q.size(); ++i) {
+      last_sig[q[i].sig_ctr] = i;
+      if (q[i].sig2_ctr >= 0) last_sig[q[i].sig2_ctr] = i;
+    }
+    int slack = 1 << 30;
+    for (int i = 0; i < (int)q.size(); ++i) {
+      for (int c : {q[i].wait_ctr, q[i].wait2_ctr}) {
+        if (c < 0) continue;
+        auto f = last_sig.find(c);
+        if (f != last_sig.end()) slack = std::min(slack, i - f->second);
+      }
+    }
+    return slack;
+  };
+  const int want = p->warp ? p->geo.warps : 1;
+  const int batch_fwd = std::max(1, std::min(want, min_slack(fwd)));
+  const int batch_inv = std::max(1, std::min(want, min_slack(inv)));
   std::vector<ChunkDev> chunks_inv = chunks;
   for (int c = 0; c < C; ++c) {
     chunks[c].p1_items = (int)f1[c].size();
@@ -400,6 +474,8 @@ ffst_status build_queue(ffst_plan* p, int batch, Queue** out) {
   q.n_fwd = (int)fwd.size();
   q.n_inv = (int)inv.size();
   q.n_g = n_self;
+  q.batch_fwd = batch_fwd;
+  q.batch_inv = batch_inv;
   const size_t need_ctr = 1 + 2 * (size_t)C + (size_t)n_self;
   if (need_ctr > p->ctr_cap) {
     void* c = nullptr;
@@ -423,8 +499,9 @@ ffst_status build_queue(ffst_plan* p, int batch, Queue** out) {
   API_CUDA(cudaMemcpy(q.d_fwd, fwd.data(), fwd.size() * sizeof(ItemDev), cudaMemcpyHostToDevice), "queue upload");
   API_CUDA(cudaMemcpy(q.d_inv, inv.data(), inv.size() * sizeof(ItemDev), cudaMemcpyHostToDevice), "queue upload");
   if (std::getenv("FFST_VERBOSE"))
-    std::fprintf(stderr, "[ffst] batch=%d chunks=%d (per image %d) D=%d R=%d Wg=%d slot=%.1f MB items fwd=%d inv=%d\n",
-                 batch, C, chunks_per_image, D, R, Wg, slot_elems * 2.0 * p->rsz / 1048576.0, q.n_fwd, q.n_inv);
+    std::fprintf(stderr, "[ffst] batch=%d chunks=%d (per image %d) D=%d R=%d Wg=%d slot=%.1f MB items fwd=%d inv=%d fetch batch %d/%d\n",
+                 batch, C, chunks_per_image, D, R, Wg, slot_elems * 2.0 * p->rsz / 1048576.0, q.n_fwd, q.n_inv,
+                 batch_fwd, batch_inv);
   auto res = p->queues.emplace(batch, q);
   *out = &res.first->second;
   return FFST_OK;
@@ -438,9 +515,11 @@ KParams base_params(ffst_plan* p) {
   k.nyq_planes = p->d_nyq;
   k.tw = p->d_tw;
   k.rtab = p->d_rtab;
+  k.colrec = p->d_colrec;
   k.F = p->F; k.Fscr = p->Fscr; k.A = p->A; k.W = p->W;
   k.nyq_fwd = p->nyq_fwd; k.nyq_S = p->nyq_S; k.nyq_T = p->nyq_T; k.corr = p->corr;
   k.n_rowitems = p->n_rowitems;
+  if (const char* d = std::getenv("FFST_DBG")) k.dbg = std::atoi(d);
   return k;
 }
 
@@ -503,6 +582,7 @@ ffst_status forward_impl(ffst_plan* p, const void* img, void* coeff, int batch, 
   k.chunks = q->d_chunks;
   k.items = q->d_fwd;
   k.n_items = q->n_fwd;
+  k.fetch_batch = q->batch_fwd;
   k.slot_elems = q->slot_elems;
   k.ctr = p->d_ctr;
   k.ctr_p1 = 1;
@@ -519,7 +599,9 @@ ffst_status forward_impl(ffst_plan* p, const void* img, void* coeff, int batch, 
   }
   API_CUDA(cudaMemsetAsync(p->d_ctr, 0, (1 + 2 * (size_t)q->n_chunks) * sizeof(int), s), "counter reset");
   if (p->timing) API_CUDA(cudaEventRecord(p->ev[1], s), "event");
-  API_CUDA(L_fwd_main(p, k, p->grid_fwd, s), "fwd_main kernel");
+  if (p->warp) API_CUDA(p->d.dtype == FFST_F32 ? launch_fwd_warp<float>(k, p->grid_fwd, s)
+                                               : launch_fwd_warp<double>(k, p->grid_fwd, s), "fwd_warp kernel");
+  else API_CUDA(L_fwd_main(p, k, p->grid_fwd, s), "fwd_main kernel");
   ++nl;
   if (p->timing) {
     API_CUDA(cudaEventRecord(p->ev[2], s), "event");
@@ -543,6 +625,7 @@ ffst_status inverse_impl(ffst_plan* p, const void* coeff, void* img_out, int bat
   k.chunks = q->d_chunks + q->n_chunks;
   k.items = q->d_inv;
   k.n_items = q->n_inv;
+  k.fetch_batch = q->batch_inv;
   k.slot_elems = q->slot_elems;
   k.ctr = p->d_ctr;
   k.ctr_p1 = 1;
@@ -553,7 +636,9 @@ ffst_status inverse_impl(ffst_plan* p, const void* coeff, void* img_out, int bat
   if (p->timing) API_CUDA(cudaEventRecord(p->ev[3], s), "event");
   API_CUDA(cudaMemsetAsync(p->d_ctr, 0, (1 + 2 * (size_t)q->n_chunks + q->n_g) * sizeof(int), s), "counter reset");
   if (p->timing) API_CUDA(cudaEventRecord(p->ev[4], s), "event");
-  API_CUDA(L_inv_main(p, k, p->grid_inv, s), "inv_main kernel");
+  if (p->warp) API_CUDA(p->d.dtype == FFST_F32 ? launch_inv_warp<float>(k, p->grid_inv, s)
+                                               : launch_inv_warp<double>(k, p->grid_inv, s), "inv_warp kernel");
+  else API_CUDA(L_inv_main(p, k, p->grid_inv, s), "inv_main kernel");
   ++nl;
   if (p->timing) API_CUDA(cudaEventRecord(p->ev[5], s), "event");
   if (!p->nyq.empty()) {
@@ -661,7 +746,12 @@ ffst_status ffst_plan_create(ffst_plan** out, const ffst_plan_desc* d) {
   p->n = d->n; p->j0 = j0; p->eta = eta; p->H = d->n / 2;
   p->rsz = d->dtype == FFST_F32 ? 4 : 8;
   p->delta = grid_delta(d->n, j0);
-  p->geo = d->dtype == FFST_F32 ? geometry<float>(d->n) : geometry<double>(d->n);
+  {
+    const char* path = std::getenv("FFST_PATH");   // "cta": force the CTA-item kernels (comparison)
+    p->warp = d->n >= 8 && d->n <= 512 && !(path && std::strcmp(path, "cta") == 0);
+  }
+  if (p->warp) p->geo = d->dtype == FFST_F32 ? geometry_warp<float>(d->n) : geometry_warp<double>(d->n);
+  else p->geo = d->dtype == FFST_F32 ? geometry<float>(d->n) : geometry<double>(d->n);
   const auto table = index_table(j0);
   for (int i = d->shard_rank; i < eta; i += d->shard_count) {
     PlaneDev P{};
@@ -669,7 +759,7 @@ ffst_status ffst_plan_create(ffst_plan** out, const ffst_plan_desc* d) {
     int lo, hi;
     plane_columns(d->n, j0, table[i], &lo, &hi);
     P.c_lo = lo; P.ncols = hi - lo + 1;
-    P.ncols_pad = (P.ncols + p->geo.gc - 1) / p->geo.gc * p->geo.gc;
+    P.ncols_pad = (P.ncols + p->geo.colpad - 1) / p->geo.colpad * p->geo.colpad;
     P.nyq = -1;
     if (plane_nyquist(d->n, j0, table[i])) {
       P.nyq = (int)p->nyq.size();
@@ -689,15 +779,21 @@ ffst_status ffst_plan_create(ffst_plan** out, const ffst_plan_desc* d) {
   int dev = d->device;
   e = cudaDeviceGetAttribute(&p->sm_count, cudaDevAttrMultiProcessorCount, dev);
   if (e != cudaSuccess) return cleanup(cuda_fail(e, "device query"));
-  const int af = d->dtype == FFST_F32 ? max_active_main<float>(d->n, dev, 0) : max_active_main<double>(d->n, dev, 0);
-  const int ai = d->dtype == FFST_F32 ? max_active_main<float>(d->n, dev, 1) : max_active_main<double>(d->n, dev, 1);
-  if (af < 1 || ai < 1) return cleanup(fail(FFST_ERR_CUDA, "persistent kernels cannot be made resident"));
-  p->grid_fwd = p->sm_count * af;
-  p->grid_inv = p->sm_count * ai;
+  if (p->warp) {
+    p->grid_fwd = p->grid_inv = p->sm_count;            // one CTA of worker warps per SM
+    p->workers = p->sm_count * p->geo.warps;
+  } else {
+    const int af = d->dtype == FFST_F32 ? max_active_main<float>(d->n, dev, 0) : max_active_main<double>(d->n, dev, 0);
+    const int ai = d->dtype == FFST_F32 ? max_active_main<float>(d->n, dev, 1) : max_active_main<double>(d->n, dev, 1);
+    if (af < 1 || ai < 1) return cleanup(fail(FFST_ERR_CUDA, "persistent kernels cannot be made resident"));
+    p->grid_fwd = p->sm_count * af;
+    p->grid_inv = p->sm_count * ai;
+    p->workers = std::max(p->grid_fwd, p->grid_inv);
+  }
 
   const size_t B = (size_t)d->batch, N = (size_t)d->n, H1 = N / 2 + 1;
   const size_t csz = 2 * p->rsz;
-  const size_t ncpf = (H1 + p->geo.gc - 1) / p->geo.gc * p->geo.gc;
+  const size_t ncpf = (size_t)p->geo.ncpf;          // row stride of the final column pass (aux kernels)
   // ring of intermediates: slot budget ~ L2 share, at least the largest plane
   long long maxplane = 0, image_total = 0;
   for (auto& P : p->planes) {
@@ -744,6 +840,23 @@ ffst_status ffst_plan_create(ffst_plan** out, const ffst_plan_desc* d) {
     } else if (e == cudaSuccess) {
       e = cudaMemcpy(p->d_rtab, rt.data(), rt.size() * sizeof(double), cudaMemcpyHostToDevice);
     }
+  }
+  if (e == cudaSuccess && p->warp) {
+    size_t bytes = 0;
+    std::vector<ColRec<float>> rf;
+    std::vector<ColRec<double>> rd;
+    if (d->dtype == FFST_F32) {
+      for (auto& P : p->planes) column_records<float>(d->n, j0, P, rf);
+      bytes = rf.size() * sizeof(ColRec<float>);
+    } else {
+      for (auto& P : p->planes) column_records<double>(d->n, j0, P, rd);
+      bytes = rd.size() * sizeof(ColRec<double>);
+    }
+    st = dalloc(p, &ptr, bytes);
+    if (st != FFST_OK) return cleanup(st);
+    p->d_colrec = ptr;
+    e = cudaMemcpy(p->d_colrec, d->dtype == FFST_F32 ? (const void*)rf.data() : (const void*)rd.data(), bytes,
+                   cudaMemcpyHostToDevice);
   }
   if (e == cudaSuccess) e = cudaMemcpy(p->d_planes, p->planes.data(), p->planes.size() * sizeof(PlaneDev), cudaMemcpyHostToDevice);
   if (e == cudaSuccess && !p->nyq.empty()) e = cudaMemcpy(p->d_nyq, p->nyq.data(), p->nyq.size() * sizeof(int), cudaMemcpyHostToDevice);

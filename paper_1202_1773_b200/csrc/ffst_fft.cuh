@@ -116,18 +116,24 @@ template <typename T, bool INV> struct DFT<T, 16, INV> {
 
 __host__ __device__ constexpr int ilog2(int x) { return x <= 1 ? 0 : 1 + ilog2(x >> 1); }
 
-template <typename T> struct Pad {
-  static constexpr int SH = sizeof(cpx<T>) == 8 ? 4 : 3;
+// Padded shared-memory index of a line: one pad element per 2^SH elements.  The Stockham write of
+// the first pass has lane stride R = EM: padding every EM (float2) elements makes it conflict-free.
+template <typename T, int EM = 16> struct Pad {
+  static constexpr int SH = sizeof(cpx<T>) == 8 ? (EM == 8 ? 3 : 4) : 3;
   static FFST_HD int at(int i) { return i + (i >> SH); }
   static constexpr int len(int L) { return L + (L >> SH) + 1; }
 };
 
-template <int L> struct RadixPlan {
+// Pass plan of a length-L line with EM (8 or 16) elements per thread: radix-EM passes with the
+// remainder radix in the middle pass.
+template <int L, int EM = 16> struct RadixPlan {
   static constexpr int M = ilog2(L);
-  static constexpr int E = L < 16 ? L : 16;
-  static constexpr int P = M <= 4 ? 1 : (M <= 8 ? 2 : 3);
+  static constexpr int LE = ilog2(EM);
+  static constexpr int E = L < EM ? L : EM;
+  static constexpr int P = M <= LE ? 1 : (M <= 2 * LE ? 2 : 3);
+  static_assert(M <= 3 * LE, "line too long for three passes");
   static constexpr int rad(int s) {
-    return P == 1 ? L : (P == 2 ? (s == 0 ? 16 : (1 << (M - 4))) : (s == 1 ? (1 << (M - 8)) : 16));
+    return P == 1 ? L : (P == 2 ? (s == 0 ? EM : (1 << (M - LE))) : (s == 1 ? (1 << (M - 2 * LE)) : EM));
   }
 };
 
@@ -138,12 +144,13 @@ template <int TH> struct SyncOf {
   }
 };
 
-template <typename T, int L, bool INV, int TWN>
+// TWS: the twiddle table is in shared memory (plain loads) instead of global (read-only path).
+template <typename T, int L, bool INV, int TWN, bool TWS = false, int EM = 16>
 struct LineFFT {
-  using RP = RadixPlan<L>;
+  using RP = RadixPlan<L, EM>;
   static constexpr int E = RP::E;
   static constexpr int TH = L / E;
-  static constexpr int SMLEN = Pad<T>::len(L);   // shared elements per line
+  static constexpr int SMLEN = Pad<T, EM>::len(L);   // shared elements per line
 
   template <int S, int NS>
   static __device__ __forceinline__ void pass(cpx<T> (&r)[E], cpx<T>* sm, int t, const cpx<T>* __restrict__ tw) {
@@ -161,7 +168,7 @@ struct LineFFT {
 #pragma unroll
       for (int b = 0; b < NB; ++b)
 #pragma unroll
-        for (int q = 0; q < R; ++q) x[b * R + q] = sm[Pad<T>::at(t + b * TH + q * (L / R))];
+        for (int q = 0; q < R; ++q) x[b * R + q] = sm[Pad<T, EM>::at(t + b * TH + q * (L / R))];
     }
 #pragma unroll
     for (int b = 0; b < NB; ++b) {
@@ -169,10 +176,21 @@ struct LineFFT {
       if constexpr (NS > 1) {
         const int v = t + b * TH;
         const int k = v & (NS - 1);
+        if constexpr (TWS) {
+          // one table read per butterfly, w^q by products (w^2q = (w^q)^2, w^(q+1) = w^q w):
+          // shared-memory bandwidth is the scarce resource on this path, the FMA pipe is not
+          cpx<T> wp[R];
+          wp[1] = tw[k * (TWN / (NS * R))];
 #pragma unroll
-        for (int q = 1; q < R; ++q) {
-          const cpx<T> w = __ldg(tw + (q * k) * (TWN / (NS * R)));
-          xb[q] = INV ? cmulc<T>(xb[q], w) : cmul<T>(xb[q], w);
+          for (int q = 2; q < R; ++q) wp[q] = (q & 1) ? cmul<T>(wp[q - 1], wp[1]) : cmul<T>(wp[q / 2], wp[q / 2]);
+#pragma unroll
+          for (int q = 1; q < R; ++q) xb[q] = INV ? cmulc<T>(xb[q], wp[q]) : cmul<T>(xb[q], wp[q]);
+        } else {
+#pragma unroll
+          for (int q = 1; q < R; ++q) {
+            const cpx<T> w = __ldg(tw + (q * k) * (TWN / (NS * R)));
+            xb[q] = INV ? cmulc<T>(xb[q], w) : cmul<T>(xb[q], w);
+          }
         }
       }
       DFT<T, R, INV>::run(xb);
@@ -190,7 +208,7 @@ struct LineFFT {
         const int k = v & (NS - 1);
         const int base = (v - k) * R + k;
 #pragma unroll
-        for (int q = 0; q < R; ++q) sm[Pad<T>::at(base + q * NS)] = x[b * R + q];
+        for (int q = 0; q < R; ++q) sm[Pad<T, EM>::at(base + q * NS)] = x[b * R + q];
       }
       SyncOf<TH>::sync();                            // writes visible to the next pass
       pass<S + 1, NS * R>(r, sm, t, tw);

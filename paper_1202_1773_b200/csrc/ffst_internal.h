@@ -30,7 +30,8 @@ struct __align__(16) ItemDev {
   int first;       // inverse pass 2: first chunk of the image (initialise A)
   int sig_ctr;     // counter incremented when done
   int sig2_ctr;    // second counter (inverse pass 2: own column-group flag), or -1
-  int pad0, pad1;
+  int pad0;        // inverse pass 2 (warp path): bit u set if plane u of the chunk touches the group
+  int pad1;
 };
 
 struct ChunkDev {
@@ -49,6 +50,7 @@ struct KParams {
   const int* nyq_planes;        // [n_nyq] local plane index of each Nyquist plane
   const void* tw;               // cpx<T>[n]: exp(-2 pi i m / n)
   const void* rtab;             // T[(j0+1)][n/2+1]: radial factors psi1(4^-j Delta a), varphi(Delta a)
+  const void* colrec;           // warp path: ColRec<T> per (local plane, column), PlaneDev.rec indexes it
   const void* img;              // [batch][n][n] T
   void* coeff;                  // [batch][eta_l][n][n] cpx<T>
   void* img_out;                // [batch][n][n] T
@@ -68,6 +70,8 @@ struct KParams {
   const UnitDev* units;
   int* ctr;                     // [0] dispatch; [ctr_p1 + c]; [ctr_p2 + c]; [ctr_g + item]
   int ctr_p1, ctr_p2, ctr_g;
+  int fetch_batch;              // warp path: consecutive items a CTA takes per global fetch
+  int dbg;                      // measurement only (FFST_DBG): bit 0 skip FFTs, bit 1 skip output stores
   unsigned long long* trace;    // optional: per item {smid, t_start, t_ready, t_end} (globaltimer ns)
 };
 
@@ -80,12 +84,18 @@ struct Geometry {
   int gr;            // inv pass 1: rows per tile
   int lpc;           // inv pass 2: columns per item
   size_t smem_fwd, smem_inv, smem_aux;   // dynamic shared bytes of the kernels
+  int warps;         // warp-worker path: worker warps per CTA (0: CTA-item path)
+  int colpad;        // forward intermediate: row stride = ncols rounded up to a multiple of colpad
+  int ncpf;          // final column pass (aux kernels, Geo): padded row stride of its output
 };
 
 // Launchers (defined per dtype in ffst_kern_f32.cu / ffst_kern_f64.cu).
 template <typename T> Geometry geometry(int n);
 template <typename T> cudaError_t launch_spectrum(const KParams& p, int batch, cudaStream_t s);
 template <typename T> cudaError_t launch_nyq_fwd(const KParams& p, int batch, cudaStream_t s);
+template <typename T> Geometry geometry_warp(int n);
+template <typename T> cudaError_t launch_fwd_warp(const KParams& p, int grid, cudaStream_t s);
+template <typename T> cudaError_t launch_inv_warp(const KParams& p, int grid, cudaStream_t s);
 template <typename T> cudaError_t launch_fwd_main(const KParams& p, int grid, cudaStream_t s);
 template <typename T> cudaError_t launch_inv_main(const KParams& p, int grid, cudaStream_t s);
 template <typename T> cudaError_t launch_nyq_inv(const KParams& p, int batch, cudaStream_t s);

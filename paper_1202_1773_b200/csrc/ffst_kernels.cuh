@@ -67,6 +67,14 @@ template <> __device__ __forceinline__ void store_pair_cs<double>(double2* dst, 
   __stcs(dst, a);
   __stcs(dst + 1, b);
 }
+template <typename T> __device__ __forceinline__ void store_pair_cg(cpx<T>* dst, cpx<T> a, cpx<T> b);
+template <> __device__ __forceinline__ void store_pair_cg<float>(float2* dst, float2 a, float2 b) {
+  __stcg(reinterpret_cast<float4*>(dst), make_float4(a.x, a.y, b.x, b.y));
+}
+template <> __device__ __forceinline__ void store_pair_cg<double>(double2* dst, double2 a, double2 b) {
+  __stcg(dst, a);
+  __stcg(dst + 1, b);
+}
 template <typename T> __device__ __forceinline__ void load_pair_cs(const cpx<T>* src, cpx<T>& a, cpx<T>& b);
 template <> __device__ __forceinline__ void load_pair_cs<float>(const float2* src, float2& a, float2& b) {
   const float4 v = __ldcs(reinterpret_cast<const float4*>(src));
@@ -525,7 +533,7 @@ __device__ __forceinline__ ItemDev load_item(const ItemDev* items, int it) {
 // forward pass 2, whose output -- the cube -- nobody reads inside the kernel).
 template <typename T, int N, bool FWD>
 __device__ __forceinline__ void persistent_loop(const KParams& p) {
-  extern __shared__ __align__(16) unsigned char smem_raw[];
+  extern __shared__ __align__(128) unsigned char smem_raw[];
   cpx<T>* smem = reinterpret_cast<cpx<T>*>(smem_raw);
   __shared__ int s_item[2];
   __shared__ PlaneDev s_planes[MAX_PLANES_SMEM];
@@ -586,7 +594,7 @@ __global__ void __launch_bounds__(256, 2) inv_main_kernel(KParams p) {
 // spectrum pass 1: rows of img[b] -> Fscr[b] column-major (all bins 0..H); grid (N/RPI, B)
 template <typename T, int N>
 __global__ void __launch_bounds__(256) spec_rows_kernel(KParams p) {
-  extern __shared__ __align__(16) unsigned char smem_raw[];
+  extern __shared__ __align__(128) unsigned char smem_raw[];
   using G = Geo<T, N>;
   const int b = blockIdx.y, g = blockIdx.x;
   const int r0 = g * G::RPI;
@@ -600,14 +608,14 @@ __global__ void __launch_bounds__(256) spec_rows_kernel(KParams p) {
 // spectrum pass 2: grid (ceil((H+1)/LPC), B)
 template <typename T, int N>
 __global__ void __launch_bounds__(256) spec_cols_kernel(KParams p) {
-  extern __shared__ __align__(16) unsigned char smem_raw[];
+  extern __shared__ __align__(128) unsigned char smem_raw[];
   K<T, N>::col_fft_plain(p, blockIdx.y, blockIdx.x, reinterpret_cast<cpx<T>*>(smem_raw));
 }
 
 // final pass 1: columns of A[b] -> Fscr[b] row-major (stride NCPF); grid (ceil((H+1)/GC), B)
 template <typename T, int N>
 __global__ void __launch_bounds__(256) fin_cols_kernel(KParams p) {
-  extern __shared__ __align__(16) unsigned char smem_raw[];
+  extern __shared__ __align__(128) unsigned char smem_raw[];
   using G = Geo<T, N>;
   const int b = blockIdx.y;
   const int c0 = blockIdx.x * G::GC;
@@ -622,7 +630,7 @@ __global__ void __launch_bounds__(256) fin_cols_kernel(KParams p) {
 // final pass 2: rows of Fscr[b] -> img_out[b] minus the Nyquist correction; grid (N/RP2, B)
 template <typename T, int N>
 __global__ void __launch_bounds__(256) fin_rows_kernel(KParams p) {
-  extern __shared__ __align__(16) unsigned char smem_raw[];
+  extern __shared__ __align__(128) unsigned char smem_raw[];
   using G = Geo<T, N>;
   const int b = blockIdx.y;
   const int r0 = blockIdx.x * G::RP2;
@@ -644,7 +652,7 @@ __global__ void __launch_bounds__(256) fin_rows_kernel(KParams p) {
 // Nyquist column.
 template <typename T, int N>
 __global__ void __launch_bounds__(256) nyq_fwd_kernel(KParams p) {
-  extern __shared__ __align__(16) unsigned char smem_raw[];
+  extern __shared__ __align__(128) unsigned char smem_raw[];
   using G = Geo<T, N>;
   using C = cpx<T>;
   constexpr int H = N / 2;
@@ -689,7 +697,7 @@ __global__ void __launch_bounds__(256) nyq_fwd_kernel(KParams p) {
 // l, l + LPC, ...; the per-line sums are added in fixed line order (deterministic).
 template <typename T, int N>
 __global__ void __launch_bounds__(256) nyq_inv_kernel(KParams p) {
-  extern __shared__ __align__(16) unsigned char smem_raw[];
+  extern __shared__ __align__(128) unsigned char smem_raw[];
   using G = Geo<T, N>;
   using C = cpx<T>;
   constexpr int H = N / 2;

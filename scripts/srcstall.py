@@ -1,0 +1,31 @@
+"""Per-source-line stall breakdown from an ncu 'source --print-source cuda,sass' CSV (SASS rows)."""
+import csv, gzip, sys, collections, re
+path = sys.argv[1]; top = int(sys.argv[2]) if len(sys.argv) > 2 else 20
+want = sys.argv[3].split(',') if len(sys.argv) > 3 else ['stall_long_sb', 'stall_short_sb', 'stall_no_inst', 'stall_wait', 'stall_selected']
+rows = list(csv.reader(gzip.open(path, 'rt') if path.endswith('.gz') else open(path)))
+hdr = None; func = None; cur = None; src = ''
+agg = collections.defaultdict(lambda: collections.Counter())
+srcs = {}
+for r in rows:
+    if not r: continue
+    if r[0] == 'Function Name': func = r[1]; continue
+    if r[0] == 'Line No': hdr = r; continue
+    if hdr is None: continue
+    if r[0].strip().isdigit() and r[1]:
+        cur = (func, r[0]); srcs[cur] = r[1].strip()[:90]; continue
+    d = dict(zip(hdr, r))
+    if not d.get('Address'): continue
+    for k in hdr:
+        if k.startswith('stall_') or k == 'Warp Stall Sampling (All Samples)':
+            try: agg[cur][k] += int(d[k] or 0)
+            except ValueError: pass
+for f in sorted(set(k[0] for k in agg)):
+    keys = [k for k in agg if k[0] == f]
+    tot = sum(agg[k]['Warp Stall Sampling (All Samples)'] for k in keys) or 1
+    print('==', f[:70], 'samples', tot)
+    for w in want:
+        wt = sum(agg[k][w] for k in keys)
+        print(f'  -- {w}: {100*wt/tot:.1f}% of samples')
+        for k in sorted(keys, key=lambda k: -agg[k][w])[:top]:
+            if agg[k][w] == 0: break
+            print(f'     {100*agg[k][w]/tot:5.1f}%  L{k[1]:>5} {srcs.get(k, "")}')
