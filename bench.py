@@ -215,6 +215,45 @@ def run_reference(args, cfg):
     return 0
 
 
+# ------------------------------------------------------------------------------ cuFFT comparison line
+
+def cufft_line(plan, x, steps: int, flush, stream):
+    """The paper's own formulation on cuFFT (torch.fft) as a COMPARISON LINE only (BASELINE.json
+    north_star): materialised spectra psi (exported once by the plan, natural bin order), forward
+    C_i = ifft2(psi_i * fft2(x)), inverse Re ifft2(sum_i psi_i * fft2(C_i)), planes in groups so
+    the temporaries stay bounded.  Returns (images/s, ms/step)."""
+    import torch
+    psi = plan.spectra(centred=False)                      # (eta, n, n) real, natural order
+    B, eta = x.shape[0], psi.shape[0]
+    group = max(1, min(eta, (2 << 30) // max(1, B * x.shape[-1] ** 2 * 16)))
+    cube = plan.empty_coeffs()
+
+    def step():
+        fx = torch.fft.fft2(x)
+        acc = torch.zeros_like(fx)
+        for i0 in range(0, eta, group):
+            p = psi[i0:i0 + group]
+            c = torch.fft.ifft2(p[None] * fx[:, None])
+            cube[:, i0:i0 + group] = c
+            acc += (p[None] * torch.fft.fft2(cube[:, i0:i0 + group])).sum(1)
+        return torch.fft.ifft2(acc).real
+
+    for _ in range(2):
+        step()
+    torch.cuda.synchronize()
+    e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    ms = 0.0
+    for _ in range(steps):
+        flush.zero_()
+        e0.record(stream)
+        step()
+        e1.record(stream)
+        torch.cuda.synchronize()
+        ms += e0.elapsed_time(e1)
+    del psi
+    return B * steps / (ms / 1000.0), ms / steps
+
+
 # ------------------------------------------------------------------------------ GPU arm
 
 def run_gpu(args, cfg):
@@ -338,6 +377,17 @@ def run_gpu(args, cfg):
         e2e = {"value": B * args.steps / (e_ms / 1000.0), "unit": "images/s",
                "h2d_bytes_per_step": B * N * N * rsz, "d2h_bytes_per_step": B * N * N * rsz}
 
+    cufft = None
+    if world == 1 and not args.no_cufft:
+        try:
+            v, ms = cufft_line(plan, x, max(2, min(args.steps, 5)), flush, stream)
+            cufft = {"value": v, "unit": "images/s", "ms_per_step": ms,
+                     "what": "comparison line only: torch.fft (cuFFT) with materialised spectra, "
+                             "fft2 / ifft2 per plane (the paper's formulation)"}
+        except Exception as exc:                               # e.g. out of memory at the largest n
+            cufft = {"unavailable": f"{type(exc).__name__}: {str(exc)[:120]}"}
+        torch.cuda.empty_cache()
+
     cpu = None
     if rank == 0 and world == 1 and not args.no_cpu_baseline:
         v, sample = oracle_images_per_s(cfg, budget_s=args.cpu_budget, max_images=max(cfg.batch, 4) * 4)
@@ -361,6 +411,7 @@ def run_gpu(args, cfg):
                          "bytes_per_launch": local_cube,
                          "kernel_ms": {"fwd_main": fm, "inv_main": im}},
             "cpu_baseline": cpu,
+            "cufft_line": cufft,
             "clocks": clocks,
             "e2e": e2e,
             "gpu_launches": (launches[0] + launches[1]) * args.steps,
@@ -381,6 +432,7 @@ def main():
     ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
     ap.add_argument("--cpu-budget", type=float, default=12.0)
     ap.add_argument("--no-cpu-baseline", action="store_true")
+    ap.add_argument("--no-cufft", action="store_true", help="skip the cuFFT comparison line")
     args = ap.parse_args()
     cfg = synth.config(args.config)
     if args.impl == "reference":

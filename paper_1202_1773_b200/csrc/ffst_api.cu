@@ -307,13 +307,15 @@ ffst_status build_queue(ffst_plan* p, int batch, Queue** out) {
   }
   avg_items /= (double)protos.size();
   const int grid = p->workers;
+  // Lookahead: at least ~3 waves of items, and as far as the ring allows (item counts
+  // under-estimate the lookahead when pass-1 items are few and long, e.g. n = 4096).
   int D = (int)std::ceil(3.0 * grid / std::max(1.0, avg_items));
-  D = std::max(1, std::min(D, (int)protos.size()));
   const long long slot_elems = (slot + 63) / 64 * 64;
   // slot reuse distance R - D = D + 2: a pass-1 item reuses the slot of a chunk whose
   // pass-2 items were queued ~D chunks earlier
   const int max_slots = (int)std::max(2LL, p->W_elems / slot_elems);
-  D = std::min(D, std::max(1, (max_slots - 2) / 2));
+  D = std::max(D, (max_slots - 2) / 2);
+  D = std::max(1, std::min(D, std::min((int)protos.size(), std::max(1, (max_slots - 2) / 2))));
   int R = std::min((int)protos.size(), std::min(max_slots, 2 * D + 2));
   if ((long long)R * slot_elems > p->W_elems) return fail(FFST_ERR_INVALID_ARG, "intermediate ring exceeds workspace");
   // ---- 2. interleaved chunk order
@@ -800,15 +802,17 @@ ffst_status ffst_plan_create(ffst_plan** out, const ffst_plan_desc* d) {
     maxplane = std::max(maxplane, (long long)N * P.ncols_pad);
     image_total += (long long)N * P.ncols_pad;
   }
-  const char* env = std::getenv("FFST_SLOT_MB");
-  const long long budget_bytes = (env ? std::atoll(env) : 4) * 1024LL * 1024LL;
+  const char* env = std::getenv("FFST_SLOT_KB");
+  const long long budget_bytes = (env ? std::atoll(env) : 4096) * 1024LL;
   p->slot_budget = std::max(maxplane, budget_bytes / (long long)csz);
   const char* envc = std::getenv("FFST_CHUNK_PLANES");
   p->chunk_planes = std::max(1, envc ? std::atoi(envc) : 4);
   const long long slot_max = std::min(image_total, std::max(maxplane, p->slot_budget)) + 64;
   const char* envr = std::getenv("FFST_RING_MB");
-  const long long ring_bytes = (envr ? std::atoll(envr) : 48) * 1024LL * 1024LL;
-  p->W_elems = std::max(3 * ((slot_max + 63) / 64 * 64), ring_bytes / (long long)csz);
+  const long long ring_bytes = (envr ? std::atoll(envr) : 96) * 1024LL * 1024LL;
+  // ring: the budget (L2-sized) or at least 12 slots when single planes are large (n >= 2048:
+  // the intermediates then live in HBM; a short ring would serialise the two passes)
+  p->W_elems = std::max(12 * ((slot_max + 63) / 64 * 64), ring_bytes / (long long)csz);
   p->n_rowitems = (int)((N + p->geo.rpi - 1) / p->geo.rpi);
   const size_t nn = std::max<size_t>(1, p->nyq.size());
 

@@ -41,7 +41,7 @@ struct Geo {
   static constexpr int GR = GR_ < N ? GR_ : N;
   static constexpr int TSTR = H + 1;           // odd: conflict-free column reads of the tile
   static constexpr int TILE_R = GR * TSTR;
-  static constexpr int RPI_ = (N / 16) > GR ? (N / 16) : GR;
+  static constexpr int RPI_ = (N >= 2048 ? 32 : N / 16) > GR ? (N >= 2048 ? 32 : N / 16) : GR;
   static constexpr int RPI = RPI_ < N ? RPI_ : N;
   // padded row stride of the final column pass output
   static constexpr int NCPF = ((H + 1 + GC - 1) / GC) * GC;
