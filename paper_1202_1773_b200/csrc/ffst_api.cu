@@ -749,8 +749,11 @@ ffst_status ffst_plan_create(ffst_plan** out, const ffst_plan_desc* d) {
   p->rsz = d->dtype == FFST_F32 ? 4 : 8;
   p->delta = grid_delta(d->n, j0);
   {
-    const char* path = std::getenv("FFST_PATH");   // "cta": force the CTA-item kernels (comparison)
-    p->warp = d->n >= 8 && d->n <= 512 && !(path && std::strcmp(path, "cta") == 0);
+    // Default: the CTA-item kernels (ffst_kernels.cuh) at every n -- measured faster on B200 with
+    // the full-ring lookahead.  FFST_PATH=warp selects the warp-worker kernels
+    // (ffst_warp.cuh, 8 <= n <= 512), kept as a tested alternative scheme.
+    const char* path = std::getenv("FFST_PATH");
+    p->warp = d->n >= 8 && d->n <= 512 && path && std::strcmp(path, "warp") == 0;
   }
   if (p->warp) p->geo = d->dtype == FFST_F32 ? geometry_warp<float>(d->n) : geometry_warp<double>(d->n);
   else p->geo = d->dtype == FFST_F32 ? geometry<float>(d->n) : geometry<double>(d->n);

@@ -55,9 +55,12 @@ def test_spectra_match_oracle(F, n, dtype):
 
 # ------------------------------------------------------------------ forward / inverse, small sizes
 
+@pytest.mark.parametrize("path", ["cta", "warp"])
 @pytest.mark.parametrize("n", [4, 8, 16, 32, 64, 128])
 @pytest.mark.parametrize("dtype", [torch.float64, torch.float32])
-def test_forward_inverse_small(F, n, dtype):
+def test_forward_inverse_small(F, n, dtype, path, monkeypatch):
+    # both execution schemes: CTA-item kernels (default) and warp-worker kernels (FFST_PATH=warp)
+    monkeypatch.setenv("FFST_PATH", path)
     batch = 3
     x, xo = images(2, batch, n, dtype)
     plan = F.Plan(n, batch, dtype)
@@ -183,8 +186,16 @@ def _check_forward_planes(c_gpu, x64, planes, tol, n):
     return max(errs)
 
 
-def test_config2_full(F):
-    # configs[1]: 256x256 float32 batch 16 — every plane of every image, and the inverse
+@pytest.mark.parametrize("path,env", [("cta", {}), ("warp", {}),
+                                      ("cta", {"FFST_RING_MB": "1", "FFST_CHUNK_PLANES": "2"}),
+                                      ("warp", {"FFST_RING_MB": "1", "FFST_CHUNK_PLANES": "2"})])
+def test_config2_full(F, path, env, monkeypatch):
+    # configs[1]: 256x256 float32 batch 16 — every plane of every image, and the inverse; both
+    # schemes, and a tiny intermediate ring (every slot reused many times: the ring-reuse and
+    # accumulation-chain dependencies of the persistent scheduler are exercised)
+    monkeypatch.setenv("FFST_PATH", path)
+    for k, v in env.items():
+        monkeypatch.setenv(k, v)
     cfg = synth.config(2)
     x, xo = images(2, cfg.batch, cfg.n, torch.float32)
     plan = F.Plan(cfg.n, cfg.batch, torch.float32)
