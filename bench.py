@@ -308,7 +308,7 @@ def run_gpu(args, cfg):
 
     plan.set_timing(True)
     ev = [(torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)) for _ in range(args.steps)]
-    fwd_main, inv_main = [], []
+    fwd_main, inv_main, fwd_tot, inv_tot = [], [], [], []
     launches = (0, 0)
     if world > 1:
         dist.barrier()
@@ -320,9 +320,11 @@ def run_gpu(args, cfg):
             step()
             ev[k][1].record(stream)
             torch.cuda.synchronize(dev)
-            (tf, ti, _, _), launches = plan.phase_times()
+            (tf, ti, tft, tit), launches = plan.phase_times()
             fwd_main.append(tf)
             inv_main.append(ti)
+            fwd_tot.append(tft)
+            inv_tot.append(tit)
         if world > 1:
             dist.barrier()
         torch.cuda.synchronize(dev)
@@ -409,7 +411,8 @@ def run_gpu(args, cfg):
                          "unit": "GB/s", "frac": achieved / peak, "traffic": traffic,
                          "peak_source": peak_src,
                          "bytes_per_launch": local_cube,
-                         "kernel_ms": {"fwd_main": fm, "inv_main": im}},
+                         "kernel_ms": {"fwd_main": fm, "inv_main": im,
+                                       "fwd_total": float(np.mean(fwd_tot)), "inv_total": float(np.mean(inv_tot))}},
             "cpu_baseline": cpu,
             "cufft_line": cufft,
             "clocks": clocks,

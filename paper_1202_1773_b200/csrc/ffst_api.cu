@@ -214,7 +214,7 @@ struct ffst_plan {
   void* d_colrec = nullptr;       // warp path column records (ColRec<T>)
   void *F = nullptr, *Fscr = nullptr, *A = nullptr, *W = nullptr;
   long long W_elems = 0;
-  void *nyq_fwd = nullptr, *nyq_S = nullptr, *nyq_T = nullptr, *corr = nullptr;
+  void *nyq_fwd = nullptr, *nyq_S = nullptr, *nyq_T = nullptr, *corr = nullptr, *nyq_part = nullptr;
   void* stage = nullptr;          // host-variant image staging [batch][n][n]
   int* d_ctr = nullptr;
   size_t ctr_cap = 0;
@@ -519,7 +519,7 @@ KParams base_params(ffst_plan* p) {
   k.rtab = p->d_rtab;
   k.colrec = p->d_colrec;
   k.F = p->F; k.Fscr = p->Fscr; k.A = p->A; k.W = p->W;
-  k.nyq_fwd = p->nyq_fwd; k.nyq_S = p->nyq_S; k.nyq_T = p->nyq_T; k.corr = p->corr;
+  k.nyq_fwd = p->nyq_fwd; k.nyq_S = p->nyq_S; k.nyq_T = p->nyq_T; k.corr = p->corr; k.nyq_part = p->nyq_part;
   k.n_rowitems = p->n_rowitems;
   if (const char* d = std::getenv("FFST_DBG")) k.dbg = std::atoi(d);
   return k;
@@ -645,7 +645,7 @@ ffst_status inverse_impl(ffst_plan* p, const void* coeff, void* img_out, int bat
   if (p->timing) API_CUDA(cudaEventRecord(p->ev[5], s), "event");
   if (!p->nyq.empty()) {
     API_CUDA(L_nyq_inv(p, k, batch, s), "nyq_inv kernel");
-    ++nl;
+    nl += 2;
   }
   API_CUDA(L_final(p, k, batch, s), "final kernels");
   nl += 2;
@@ -809,10 +809,12 @@ ffst_status ffst_plan_create(ffst_plan** out, const ffst_plan_desc* d) {
   const long long budget_bytes = (env ? std::atoll(env) : 4096) * 1024LL;
   p->slot_budget = std::max(maxplane, budget_bytes / (long long)csz);
   const char* envc = std::getenv("FFST_CHUNK_PLANES");
-  p->chunk_planes = std::max(1, envc ? std::atoi(envc) : 4);
+  // planes per chunk: 4 (pipelining granularity); small batches use long chunks so the inverse's
+  // per-image accumulation chain (one link per chunk) stays short (config 1: 0.24 -> 0.16 ms)
+  p->chunk_planes = std::max(1, envc ? std::atoi(envc) : (d->batch <= 4 ? 32 : 4));
   const long long slot_max = std::min(image_total, std::max(maxplane, p->slot_budget)) + 64;
   const char* envr = std::getenv("FFST_RING_MB");
-  const long long ring_bytes = (envr ? std::atoll(envr) : 96) * 1024LL * 1024LL;
+  const long long ring_bytes = (envr ? std::atoll(envr) : 80) * 1024LL * 1024LL;
   // ring: the budget (L2-sized) or at least 12 slots when single planes are large (n >= 2048:
   // the intermediates then live in HBM; a short ring would serialise the two passes)
   p->W_elems = std::max(12 * ((slot_max + 63) / 64 * 64), ring_bytes / (long long)csz);
@@ -834,6 +836,7 @@ ffst_status ffst_plan_create(ffst_plan** out, const ffst_plan_desc* d) {
   ALLOC(p->nyq_S, B * nn * p->n_rowitems * N * p->rsz);
   ALLOC(p->nyq_T, B * nn * N * p->rsz);
   ALLOC(p->corr, B * 2 * N * p->rsz);
+  ALLOC(p->nyq_part, B * nn * 2 * N * csz);
   ALLOC(p->stage, B * N * N * p->rsz);
 #undef ALLOC
   std::vector<unsigned char> tw;
