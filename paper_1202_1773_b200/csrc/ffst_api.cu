@@ -183,6 +183,7 @@ struct Queue {
   int batch = 0;
   int n_chunks = 0, n_fwd = 0, n_inv = 0, n_g = 0;
   int batch_fwd = 1, batch_inv = 1;   // largest safe per-CTA fetch batch (dependency distance)
+  int a_lanes = 1;                    // accumulator lanes of the inverse (copies of A summed at the end)
   long long slot_elems = 0;
   int nslots = 0;
   UnitDev* d_units = nullptr;
@@ -206,6 +207,7 @@ struct ffst_plan {
   int workers = 0;                // concurrent item consumers (warps or CTAs) of the persistent kernels
   long long slot_budget = 0;
   int chunk_planes = 4;           // max planes per chunk (pipelining granularity of the passes)
+  int acc_lanes = 4;              // max accumulator lanes of the inverse (FFST_ACC_LANES)
   // device memory
   PlaneDev* d_planes = nullptr;
   int* d_nyq = nullptr;
@@ -327,9 +329,14 @@ ffst_status build_queue(ffst_plan* p, int batch, Queue** out) {
       for (int b = b0; b < b1; ++b) order.push_back(b * chunks_per_image + ci);
   }
   const int C = (int)order.size();
+  // accumulator lanes: consecutive chunks of an image accumulate into different copies of A
+  // (chunk index mod K), summed in lane order by the final pass -- the inverse's accumulation
+  // chain then links chunks K apart instead of neighbours (deterministic, no atomics)
+  const int K = std::max(1, std::min(p->acc_lanes, chunks_per_image));
   std::vector<UnitDev> units;
   std::vector<ChunkDev> chunks(C);
-  std::vector<int> last_chunk_of_image(batch, -1);
+  std::vector<int> chunk_lane(C, 0);
+  std::vector<int> last_chunk_of_lane((size_t)batch * K, -1);
   for (int c = 0; c < C; ++c) {
     const Proto& pr = protos[order[c]];
     ChunkDev& ch = chunks[c];
@@ -338,8 +345,10 @@ ffst_status build_queue(ffst_plan* p, int batch, Queue** out) {
     ch.nunits = pr.np;
     ch.slot = c % R;
     ch.prev_slot_chunk = c - R >= 0 ? c - R : -1;
-    ch.first_of_image = last_chunk_of_image[pr.b] < 0 ? 1 : 0;
-    last_chunk_of_image[pr.b] = c;
+    const int lane = (order[c] % chunks_per_image) % K;
+    chunk_lane[c] = lane;
+    ch.first_of_image = last_chunk_of_lane[(size_t)pr.b * K + lane] < 0 ? 1 : 0;   // first of its lane
+    last_chunk_of_lane[(size_t)pr.b * K + lane] = c;
     long long used = 0;
     for (int lp = pr.lp0; lp < pr.lp0 + pr.np; ++lp) {
       UnitDev u{};
@@ -352,7 +361,7 @@ ffst_status build_queue(ffst_plan* p, int batch, Queue** out) {
   //      [1 + 2C + g] inverse column-group flags)
   std::vector<std::vector<ItemDev>> f1(C), f2(C), i1(C), i2(C);
   const int ngroups = (H + 1 + g.lpc - 1) / g.lpc;
-  std::vector<int> last_self((size_t)batch * ngroups, -1);
+  std::vector<int> last_self((size_t)batch * K * ngroups, -1);
   int n_self = 0;
   auto mk_item = [](int type, int c, int group, int b, int pl, int np, int woff, int slot) {
     ItemDev it{};
@@ -379,9 +388,10 @@ ffst_status build_queue(ffst_plan* p, int batch, Queue** out) {
         if (g1 > P.c_lo && g0 < P.c_lo + P.ncols) touched = true;
       }
       if (!touched) continue;
-      int& last = last_self[(size_t)ch.b * ngroups + gg];
+      int& last = last_self[((size_t)ch.b * K + chunk_lane[c]) * ngroups + gg];
       ItemDev it = mk_item(1, c, gg, ch.b, units[ch.unit0].p, ch.nunits, units[ch.unit0].woff, ch.slot);
       it.first = ch.first_of_image;
+      it.pad1 = chunk_lane[c];
       for (int u = ch.unit0; u < ch.unit0 + ch.nunits; ++u) {
         const PlaneDev& P = p->planes[units[u].p];
         if (g1 > P.c_lo && g0 < P.c_lo + P.ncols) it.pad0 |= 1 << (u - ch.unit0);
@@ -478,6 +488,7 @@ ffst_status build_queue(ffst_plan* p, int batch, Queue** out) {
   q.n_g = n_self;
   q.batch_fwd = batch_fwd;
   q.batch_inv = batch_inv;
+  q.a_lanes = K;
   const size_t need_ctr = 1 + 2 * (size_t)C + (size_t)n_self;
   if (need_ctr > p->ctr_cap) {
     void* c = nullptr;
@@ -521,6 +532,7 @@ KParams base_params(ffst_plan* p) {
   k.F = p->F; k.Fscr = p->Fscr; k.A = p->A; k.W = p->W;
   k.nyq_fwd = p->nyq_fwd; k.nyq_S = p->nyq_S; k.nyq_T = p->nyq_T; k.corr = p->corr; k.nyq_part = p->nyq_part;
   k.n_rowitems = p->n_rowitems;
+  k.a_lane_elems = (long long)p->d.batch * (p->n / 2 + 1) * p->n;
   if (const char* d = std::getenv("FFST_DBG")) k.dbg = std::atoi(d);
   return k;
 }
@@ -627,6 +639,7 @@ ffst_status inverse_impl(ffst_plan* p, const void* coeff, void* img_out, int bat
   k.chunks = q->d_chunks + q->n_chunks;
   k.items = q->d_inv;
   k.n_items = q->n_inv;
+  k.a_lanes = q->a_lanes;
   k.fetch_batch = q->batch_inv;
   k.slot_elems = q->slot_elems;
   k.ctr = p->d_ctr;
@@ -812,6 +825,13 @@ ffst_status ffst_plan_create(ffst_plan** out, const ffst_plan_desc* d) {
   // planes per chunk: 4 (pipelining granularity); small batches use long chunks so the inverse's
   // per-image accumulation chain (one link per chunk) stays short (config 1: 0.24 -> 0.16 ms)
   p->chunk_planes = std::max(1, envc ? std::atoi(envc) : (d->batch <= 4 ? 32 : 4));
+  {
+    // accumulator lanes: up to 4 while the lanes of A stay L2-sized (<= 32 MB); above that the
+    // final pass's extra reads would go to HBM (configs 3-5: one lane)
+    const long long a_bytes = (long long)d->batch * (d->n / 2 + 1) * d->n * 2 * (long long)p->rsz;
+    p->acc_lanes = (int)std::max(1LL, std::min(4LL, (32LL << 20) / std::max(1LL, a_bytes)));
+    if (const char* el = std::getenv("FFST_ACC_LANES")) p->acc_lanes = std::max(1, std::min(16, std::atoi(el)));
+  }
   const long long slot_max = std::min(image_total, std::max(maxplane, p->slot_budget)) + 64;
   const char* envr = std::getenv("FFST_RING_MB");
   const long long ring_bytes = (envr ? std::atoll(envr) : 80) * 1024LL * 1024LL;
@@ -830,7 +850,7 @@ ffst_status ffst_plan_create(ffst_plan** out, const ffst_plan_desc* d) {
   ALLOC(p->d_rtab, (size_t)(j0 + 1) * H1 * p->rsz);
   ALLOC(p->F, B * H1 * N * csz);
   ALLOC(p->Fscr, B * std::max(H1 * N, N * ncpf) * csz);
-  ALLOC(p->A, B * H1 * N * csz);
+  ALLOC(p->A, (size_t)p->acc_lanes * B * H1 * N * csz);
   ALLOC(p->W, (size_t)p->W_elems * csz);
   ALLOC(p->nyq_fwd, B * nn * 2 * N * p->rsz);
   ALLOC(p->nyq_S, B * nn * p->n_rowitems * N * p->rsz);

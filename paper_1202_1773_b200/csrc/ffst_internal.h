@@ -31,7 +31,7 @@ struct __align__(16) ItemDev {
   int sig_ctr;     // counter incremented when done
   int sig2_ctr;    // second counter (inverse pass 2: own column-group flag), or -1
   int pad0;        // inverse pass 2 (warp path): bit u set if plane u of the chunk touches the group
-  int pad1;
+  int pad1;        // inverse pass 2: accumulator lane of the chunk (copy of A it accumulates into)
 };
 
 struct ChunkDev {
@@ -56,7 +56,9 @@ struct KParams {
   void* img_out;                // [batch][n][n] T
   void* F;                      // [batch][n/2+1][n] cpx<T>: image spectrum, column-major half (F[b][u1][u2])
   void* Fscr;                   // [batch][n/2+1][n] cpx<T>: scratch (row-pass output)
-  void* A;                      // [batch][n/2+1][n] cpx<T>: adjoint accumulator, same layout as F
+  void* A;                      // [lanes][batch][n/2+1][n] cpx<T>: adjoint accumulators, same layout as F
+  long long a_lane_elems;       // elements per accumulator lane
+  int a_lanes;                  // lanes in use (the final pass sums them in lane order)
   void* W;                      // ring of intermediates, slot s at W + s * slot_elems
   long long slot_elems;
   void* nyq_fwd;                // [batch][n_nyq][2][n] T: forward Nyquist terms G(m1), H(r)

@@ -54,6 +54,8 @@ struct Geo {
   static constexpr size_t SMEM_AUX = SMEM_FWD > SMEM_INV ? SMEM_FWD : SMEM_INV;
   static constexpr size_t SMEM_NYQ = (size_t)(SCR_C + NT * EC) * ESZ;
   static_assert(RPI % GR == 0, "RPI must be a multiple of GR");
+  static_assert(THC <= 32 ? (32 / THC) * SMC * ESZ >= 64 * EC : SMC * ESZ >= (THC / 32) * 64 * EC,
+                "candidate lists must fit the warp's FFT scratch");
   static_assert(GC % LPC == 0 || LPC > GC, "GC vs LPC");
 };
 
@@ -113,6 +115,45 @@ struct K {
   static constexpr int H = N / 2;
   static constexpr int NT = G::NT;
 
+  // Window sym_i of the CTA's column lines into wbuf[q * NT + tid] (thread tid's element q = row
+  // t + q THC of column cb0 + tid / THC).  The support is ~10 % of the rows: each warp first
+  // compacts its candidate elements (exact integer prefilter, ballot + prefix count) into `list`,
+  // then evaluates them converged, 32 at a time -- instead of every lane paying the divergent
+  // window code on every element.  All threads of the CTA call it; act = the thread's column is
+  // one to window.
+  // The lists live in the FFT scratch of the warp's own line(s) (used only by that warp's FFT,
+  // after this call; lines longer than a warp are separated by a CTA barrier at the end).
+  static __device__ __forceinline__ void window_lines(const PlaneDev& P, int cb0, bool act, T* wbuf, C* scr,
+                                                      const Radial<T>& R, T delta) {
+    const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5, t = tid % G::THC;
+    const int cb = cb0 + tid / G::THC;
+    const int u1 = cb == H ? -H : cb;
+    const int w0 = warp * 32;    // first thread of the warp
+    unsigned short* wl = reinterpret_cast<unsigned short*>(scr + (w0 / G::THC) * G::SMC) +
+                         ((w0 % G::THC) / 32) * (32 * G::EC);
+    ColBounds bnd{1, 0, 1, 0};
+    if (act) bnd = col_bounds<T>(P, u1, H, delta);
+    int count = 0;
+#pragma unroll
+    for (int q = 0; q < G::EC; ++q) {
+      const int rb = t + q * G::THC;
+      const bool cand = act && (cb == H || rb == H || col_candidate(bnd, centred(rb, N)));
+      wbuf[q * NT + tid] = T(0);
+      const unsigned m = __ballot_sync(0xffffffffu, cand);
+      if (cand) wl[count + __popc(m & ((1u << lane) - 1u))] = (unsigned short)((q << 5) | lane);
+      count += __popc(m);
+    }
+    __syncwarp();
+#pragma unroll 1
+    for (int k = lane; k < count; k += 32) {
+      const int e = wl[k];
+      const int q = e >> 5, tid2 = warp * 32 + (e & 31);
+      const int cb2 = cb0 + tid2 / G::THC, rb2 = tid2 % G::THC + q * G::THC;
+      wbuf[q * NT + tid2] = window_sym<T>(P, cb2 == H ? -H : cb2, centred(rb2, N), H, R);
+    }
+    SyncOf<G::THC>::sync();
+  }
+
   // ------------------------------------------------------------------ column IFFT item
   // MAIN: forward pass 1 — column bins [c0, c0+cnt) of plane P: X(u) = sym_P(u) F(u),
   //       IFFT along u2, rows -> W (row-major, stride P.ncols_pad, column c - P.c_lo).
@@ -138,22 +179,22 @@ struct K {
       C r[G::EC];
       if constexpr (MODE == MODE_MAIN) {
         T* wbuf = reinterpret_cast<T*>(tile + G::TILE_C);
-        const ColBounds bnd = col_bounds<T>(P, u1, H, delta);
-#pragma unroll 2
-        for (int q = 0; q < G::EC; ++q) {
-          const int rb = t + q * G::THC, u2 = centred(rb, N);
-          const bool cand = act && (cb == H || rb == H || col_candidate(bnd, u2));
-          wbuf[q * NT + tid] = cand ? window_sym<T>(P, u1, u2, H, R) : T(0);
-        }
+        window_lines(P, c0 + rd * G::LPC, act, wbuf, scr, R, delta);
         if (rd == 0) FFST_PROBE(p, 0);
 #pragma unroll
         for (int q = 0; q < G::EC; ++q) {
           const T w = wbuf[q * NT + tid];
           r[q] = w != T(0) ? cscale<T>(__ldg(col + t + q * G::THC), w) : czero<T>();
         }
-      } else {
+      } else {   // final pass: the accumulator lanes of A summed in lane order
 #pragma unroll
         for (int q = 0; q < G::EC; ++q) r[q] = act ? __ldcg(col + t + q * G::THC) : czero<T>();
+        for (int l = 1; l < p.a_lanes; ++l) {
+          const C* cl = col + (size_t)l * p.a_lane_elems;
+#pragma unroll
+          for (int q = 0; q < G::EC; ++q)
+            if (act) r[q] = cadd<T>(r[q], __ldcg(cl + t + q * G::THC));
+        }
       }
       if (rd == 0) FFST_PROBE(p, 1);
       LineFFT<T, N, true, N>::run(r, scr + line * G::SMC, t, tw);
@@ -415,15 +456,7 @@ struct K {
       C r[G::EC];
 #pragma unroll
       for (int q = 0; q < G::EC; ++q) r[q] = in ? __ldcg(col + t + q * G::THC) : czero<T>();
-      if (in) {
-        const ColBounds bnd = col_bounds<T>(P, u1, H, delta);
-#pragma unroll 2
-        for (int q = 0; q < G::EC; ++q) {
-          const int rb = t + q * G::THC, u2 = centred(rb, N);
-          const bool cand = cb == H || rb == H || col_candidate(bnd, u2);
-          wbuf[q * NT + tid] = cand ? window_sym<T>(P, u1, u2, H, R) : T(0);
-        }
-      }
+      window_lines(P, g0, in, wbuf, scr, R, delta);
       LineFFT<T, N, false, N>::run(r, scr + line * G::SMC, t, tw);
       if (in) {
 #pragma unroll
@@ -436,7 +469,7 @@ struct K {
       SyncOf<G::THC>::sync();
     }
     if (act) {
-      C* a = static_cast<C*>(p.A) + ((size_t)I.b * (H + 1) + cb) * N;
+      C* a = static_cast<C*>(p.A) + (size_t)I.pad1 * p.a_lane_elems + ((size_t)I.b * (H + 1) + cb) * N;
 #pragma unroll
       for (int q = 0; q < G::EC; ++q) {
         const int idx = t + q * G::THC;

@@ -527,7 +527,7 @@ struct WK {
     }
     const int cb = I.group * G::LPC + line;
     if (cb <= H) {
-      C* a = static_cast<C*>(p.A) + ((size_t)I.b * (H + 1) + cb) * N;
+      C* a = static_cast<C*>(p.A) + (size_t)I.pad1 * p.a_lane_elems + ((size_t)I.b * (H + 1) + cb) * N;
 #pragma unroll
       for (int q = 0; q < G::EC; ++q) {
         const int idx = t + q * G::THC;
