@@ -216,7 +216,7 @@ struct ffst_plan {
   void* d_colrec = nullptr;       // warp path column records (ColRec<T>)
   void *F = nullptr, *Fscr = nullptr, *A = nullptr, *W = nullptr;
   long long W_elems = 0;
-  void *nyq_fwd = nullptr, *nyq_S = nullptr, *nyq_T = nullptr, *corr = nullptr, *nyq_part = nullptr;
+  void *nyq_fwd = nullptr, *nyq_S = nullptr, *nyq_T = nullptr, *corr = nullptr, *nyq_anti = nullptr;
   void* stage = nullptr;          // host-variant image staging [batch][n][n]
   int* d_ctr = nullptr;
   size_t ctr_cap = 0;
@@ -530,7 +530,7 @@ KParams base_params(ffst_plan* p) {
   k.rtab = p->d_rtab;
   k.colrec = p->d_colrec;
   k.F = p->F; k.Fscr = p->Fscr; k.A = p->A; k.W = p->W;
-  k.nyq_fwd = p->nyq_fwd; k.nyq_S = p->nyq_S; k.nyq_T = p->nyq_T; k.corr = p->corr; k.nyq_part = p->nyq_part;
+  k.nyq_fwd = p->nyq_fwd; k.nyq_S = p->nyq_S; k.nyq_T = p->nyq_T; k.corr = p->corr; k.nyq_anti = p->nyq_anti;
   k.n_rowitems = p->n_rowitems;
   k.a_lane_elems = (long long)p->d.batch * (p->n / 2 + 1) * p->n;
   if (const char* d = std::getenv("FFST_DBG")) k.dbg = std::atoi(d);
@@ -658,7 +658,7 @@ ffst_status inverse_impl(ffst_plan* p, const void* coeff, void* img_out, int bat
   if (p->timing) API_CUDA(cudaEventRecord(p->ev[5], s), "event");
   if (!p->nyq.empty()) {
     API_CUDA(L_nyq_inv(p, k, batch, s), "nyq_inv kernel");
-    nl += 2;
+    ++nl;
   }
   API_CUDA(L_final(p, k, batch, s), "final kernels");
   nl += 2;
@@ -856,7 +856,7 @@ ffst_status ffst_plan_create(ffst_plan** out, const ffst_plan_desc* d) {
   ALLOC(p->nyq_S, B * nn * p->n_rowitems * N * p->rsz);
   ALLOC(p->nyq_T, B * nn * N * p->rsz);
   ALLOC(p->corr, B * 2 * N * p->rsz);
-  ALLOC(p->nyq_part, B * nn * 2 * N * csz);
+  ALLOC(p->nyq_anti, nn * 2 * N * p->rsz);
   ALLOC(p->stage, B * N * N * p->rsz);
 #undef ALLOC
   std::vector<unsigned char> tw;
@@ -887,6 +887,27 @@ ffst_status ffst_plan_create(ffst_plan** out, const ffst_plan_desc* d) {
     p->d_colrec = ptr;
     e = cudaMemcpy(p->d_colrec, d->dtype == FFST_F32 ? (const void*)rf.data() : (const void*)rd.data(), bytes,
                    cudaMemcpyHostToDevice);
+  }
+  if (e == cudaSuccess && !p->nyq.empty()) {
+    // anti part of each Nyquist plane on the Nyquist row / column (2n values per plane)
+    const std::vector<double> tab = radial_table(d->n, j0);
+    const Radial<double> R{tab.data(), (int)H1, j0};
+    const int Hh = d->n / 2;
+    std::vector<double> anti(p->nyq.size() * 2 * N);
+    for (size_t q = 0; q < p->nyq.size(); ++q) {
+      const PlaneDev& P = p->planes[p->nyq[q]];
+      for (int bin = 0; bin < d->n; ++bin) {
+        const int u = bin < Hh ? bin : bin - d->n;
+        anti[(q * 2 + 0) * N + bin] = window_anti<double>(P, u, -Hh, Hh, R);
+        anti[(q * 2 + 1) * N + bin] = window_anti<double>(P, -Hh, u, Hh, R);
+      }
+    }
+    if (d->dtype == FFST_F32) {
+      std::vector<float> af(anti.begin(), anti.end());
+      e = cudaMemcpy(p->nyq_anti, af.data(), af.size() * sizeof(float), cudaMemcpyHostToDevice);
+    } else {
+      e = cudaMemcpy(p->nyq_anti, anti.data(), anti.size() * sizeof(double), cudaMemcpyHostToDevice);
+    }
   }
   if (e == cudaSuccess) e = cudaMemcpy(p->d_planes, p->planes.data(), p->planes.size() * sizeof(PlaneDev), cudaMemcpyHostToDevice);
   if (e == cudaSuccess && !p->nyq.empty()) e = cudaMemcpy(p->d_nyq, p->nyq.data(), p->nyq.size() * sizeof(int), cudaMemcpyHostToDevice);

@@ -706,10 +706,10 @@ __global__ void __launch_bounds__(256) nyq_fwd_kernel(KParams p) {
     if (act) {
       const int u = centred(bin, N);
       if (which == 0) {
-        const T a = window_anti<T>(P, u, -H, H, R);
+        const T a = static_cast<const T*>(p.nyq_anti)[((size_t)nq * 2 + 0) * N + bin];
         if (a != T(0)) v = cscale<T>(bin <= H ? F[(size_t)bin * N + H] : conj_<T>(F[(size_t)(N - bin) * N + H]), a);
       } else {
-        const T a = window_anti<T>(P, -H, u, H, R);
+        const T a = static_cast<const T*>(p.nyq_anti)[((size_t)nq * 2 + 1) * N + bin];
         if (a != T(0)) v = cscale<T>(F[(size_t)H * N + bin], a);
       }
     }
@@ -766,15 +766,10 @@ __global__ void __launch_bounds__(256) nyq_inv_kernel(KParams p) {
     }
     LineFFT<T, N, false, N>::run(r, scr, t, tw);
     if (act) {
-      const PlaneDev P = p.planes[p.nyq_planes[nq]];
-#pragma unroll 1
-      for (int q = 0; q < G::EC; ++q) {
-        const int u = centred(t + q * G::THC, N);
-        stage[q * G::NT + tid].x = which == 0 ? window_anti<T>(P, u, -H, H, R) : window_anti<T>(P, -H, u, H, R);
-      }
+      const T* anti = static_cast<const T*>(p.nyq_anti) + ((size_t)nq * 2 + which) * N;
 #pragma unroll
       for (int q = 0; q < G::EC; ++q) {
-        const T a = stage[q * G::NT + tid].x;
+        const T a = anti[t + q * G::THC];
         acc[q].x += a * r[q].x;
         acc[q].y += a * r[q].y;
       }
@@ -801,67 +796,6 @@ __global__ void __launch_bounds__(256) nyq_inv_kernel(KParams p) {
 #pragma unroll
     for (int q = 0; q < G::EC; ++q) out[t + q * G::THC] = acc[q].y * s;
   }
-}
-
-// inverse Nyquist correction, parallel form: stage a, grid (n_nyq, B), one CTA of two lines per
-// Nyquist plane (line 0: the alternating column sums s(m1) -> DFT -> * anti on the Nyquist row;
-// line 1: the alternating row sums t(r) -> DFT -> * anti on the Nyquist column) -> nyq_part;
-// stage b, grid (2, B): the per-plane parts summed in plane order (deterministic), inverse DFT ->
-// corr.  Same arithmetic as nyq_inv_kernel, 2 n_nyq B lines in parallel instead
-// of 2 B CTAs looping over the planes.
-template <typename T, int N>
-__global__ void nyq_inv_a_kernel(KParams p) {
-  extern __shared__ __align__(128) unsigned char smem_raw[];
-  using G = Geo<T, N>;
-  using C = cpx<T>;
-  constexpr int H = N / 2;
-  const int nq = blockIdx.x, b = blockIdx.y;
-  const int which = threadIdx.x / G::THC, t = threadIdx.x % G::THC;
-  C* scr = reinterpret_cast<C*>(smem_raw) + which * G::SMC;
-  const Radial<T> R{static_cast<const T*>(p.rtab), N / 2 + 1, p.j0};
-  const PlaneDev P = p.planes[p.nyq_planes[nq]];
-  C r[G::EC];
-#pragma unroll
-  for (int q = 0; q < G::EC; ++q) {
-    const int m = t + q * G::THC;
-    T s = T(0);
-    if (which == 0) {
-      const T* ps = static_cast<const T*>(p.nyq_S) + ((size_t)b * p.n_nyq + nq) * p.n_rowitems * N + m;
-      for (int g = 0; g < p.n_rowitems; ++g) s += ps[(size_t)g * N];
-    } else {
-      s = static_cast<const T*>(p.nyq_T)[((size_t)b * p.n_nyq + nq) * N + m];
-    }
-    r[q] = mk<T>(s, T(0));
-  }
-  LineFFT<T, N, false, N>::run(r, scr, t, static_cast<const C*>(p.tw));
-  C* out = static_cast<C*>(p.nyq_part) + (((size_t)b * p.n_nyq + nq) * 2 + which) * N;
-#pragma unroll
-  for (int q = 0; q < G::EC; ++q) {
-    const int u = centred(t + q * G::THC, N);
-    const T a = which == 0 ? window_anti<T>(P, u, -H, H, R) : window_anti<T>(P, -H, u, H, R);
-    out[t + q * G::THC] = cscale<T>(r[q], a);
-  }
-}
-
-template <typename T, int N>
-__global__ void nyq_inv_b_kernel(KParams p) {
-  extern __shared__ __align__(128) unsigned char smem_raw[];
-  using G = Geo<T, N>;
-  using C = cpx<T>;
-  const int which = blockIdx.x, b = blockIdx.y, t = threadIdx.x;
-  C acc[G::EC];
-#pragma unroll
-  for (int q = 0; q < G::EC; ++q) acc[q] = czero<T>();
-  const C* part = static_cast<const C*>(p.nyq_part) + (size_t)b * p.n_nyq * 2 * N + (size_t)which * N;
-#pragma unroll 1
-  for (int nq = 0; nq < p.n_nyq; ++nq)
-#pragma unroll
-    for (int q = 0; q < G::EC; ++q) acc[q] = cadd<T>(acc[q], part[(size_t)nq * 2 * N + t + q * G::THC]);
-  LineFFT<T, N, true, N>::run(acc, reinterpret_cast<C*>(smem_raw), t, static_cast<const C*>(p.tw));
-  T* out = static_cast<T*>(p.corr) + ((size_t)b * 2 + which) * N;
-  const T s = T(1) / (T(N) * T(N));
-#pragma unroll
-  for (int q = 0; q < G::EC; ++q) out[t + q * G::THC] = acc[q].y * s;
 }
 
 // materialise spectra (tests only): psi[i][row][col], grid-stride

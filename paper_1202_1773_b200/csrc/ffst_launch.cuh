@@ -82,13 +82,8 @@ template <typename T, int N> struct Launch {
     return cudaGetLastError();
   }
   static cudaError_t nyq_inv(const KParams& p, int batch, cudaStream_t s) {
-    // parallel form: one CTA of two lines per (Nyquist plane, image), then a per-image sum
-    const size_t sa = (size_t)2 * G::SMC * sizeof(cpx<T>), sb = (size_t)G::SMC * sizeof(cpx<T>);
-    FFST_CHECK(set_smem(nyq_inv_a_kernel<T, N>, sa));
-    nyq_inv_a_kernel<T, N><<<dim3(p.n_nyq, batch), 2 * G::THC, sa, s>>>(p);
-    FFST_CHECK(cudaGetLastError());
-    FFST_CHECK(set_smem(nyq_inv_b_kernel<T, N>, sb));
-    nyq_inv_b_kernel<T, N><<<dim3(2, batch), G::THC, sb, s>>>(p);
+    FFST_CHECK(set_smem(nyq_inv_kernel<T, N>, G::SMEM_NYQ));
+    nyq_inv_kernel<T, N><<<dim3(2, batch), G::NT, G::SMEM_NYQ, s>>>(p);
     return cudaGetLastError();
   }
   static cudaError_t final_(const KParams& p, int batch, cudaStream_t s) {
