@@ -29,6 +29,13 @@ struct Geo {
   static constexpr int ER = RadixPlan<H>::E, THR = H / ER, LPR = NT / THR;
   static constexpr int SMC = Pad<T>::len(N), SMR = Pad<T>::len(H);
   static constexpr int SCR_C = LPC * SMC, SCR_R = LPR * SMR;
+  // row passes as row PAIRS on length-N lines ("two-for-one", one complex FFT per two real rows)
+  // when a round holds the same rows either way (E = 16 for both line lengths)
+  static constexpr bool PAIR = 2 * LPC == LPR;
+  // measured: the pair form wins for the inverse row pass (configs 2-5) and loses for the forward
+  // one at n >= 512 (its stores are 8-byte instead of 16-byte per lane): inverse only
+  static constexpr bool PAIR_FWD = false, PAIR_INV = PAIR;
+  static constexpr int SCRX = SCR_C > SCR_R ? SCR_C : SCR_R;
   // forward pass 1: columns per item (>= 32-byte row segments of the intermediate)
   static constexpr int GC = LPC > (32 / ESZ) ? LPC : (32 / ESZ);
   static constexpr int GCP = GC + 1;
@@ -49,11 +56,13 @@ struct Geo {
   // arithmetic is not unrolled into the FFT's register footprint
   static constexpr int WBUF = NT * EC * (int)sizeof(T) / ESZ;      // in complex elements
   static constexpr int NYQB = (N + RP2) * (int)sizeof(T) / ESZ + 1;   // staged Nyquist terms (complex units)
-  static constexpr size_t SMEM_FWD = (size_t)((SCR_C + TILE_C + WBUF) > (SCR_R + NYQB) ? (SCR_C + TILE_C + WBUF) : (SCR_R + NYQB)) * ESZ;
-  static constexpr size_t SMEM_INV = (size_t)((SCR_R + TILE_R) > (SCR_C + WBUF) ? (SCR_R + TILE_R) : (SCR_C + WBUF)) * ESZ + 256;
+  static constexpr size_t SMEM_FWD = (size_t)((SCR_C + TILE_C + WBUF) > (SCRX + NYQB) ? (SCR_C + TILE_C + WBUF) : (SCRX + NYQB)) * ESZ;
+  static constexpr size_t SMEM_INV = (size_t)((SCRX + TILE_R) > (SCR_C + WBUF) ? (SCRX + TILE_R) : (SCR_C + WBUF)) * ESZ + 256;
   static constexpr size_t SMEM_AUX = SMEM_FWD > SMEM_INV ? SMEM_FWD : SMEM_INV;
   static constexpr size_t SMEM_NYQ = (size_t)(SCR_C + NT * EC) * ESZ;
   static_assert(RPI % GR == 0, "RPI must be a multiple of GR");
+  static_assert(!PAIR || (GR % (2 * LPC) == 0 || GR < 2 * LPC), "row-pair rounds must tile GR");
+  static_assert(SCR_C * ESZ >= LPC * N * (int)sizeof(T), "row-pair column-sum scratch");
   static_assert(THC <= 32 ? (32 / THC) * SMC * ESZ >= 64 * EC : SMC * ESZ >= (THC / 32) * 64 * EC,
                 "candidate lists must fit the warp's FFT scratch");
   static_assert(GC % LPC == 0 || LPC > GC, "GC vs LPC");
@@ -232,7 +241,7 @@ struct K {
     const T scale = T(1) / (T(N) * T(N));
     constexpr int ROUNDS = G::RP2 / G::LPR > 0 ? G::RP2 / G::LPR : 1;
     // Nyquist terms of this item staged in shared memory: G(m1) for all m1, H(r) for its rows
-    T* sG = reinterpret_cast<T*>(smem + G::SCR_R);
+    T* sG = reinterpret_cast<T*>(smem + G::SCRX);
     T* sH = sG + N;
     if (nyqG != nullptr) {
       for (int m = tid; m < N; m += NT) sG[m] = nyqG[m];
@@ -305,7 +314,7 @@ struct K {
                                  int c_lo, int ncols, int r0, int cnt, C* dst, int nyq_b, int nyq_idx,
                                  int nyq_group, C* smem, const int* dep = nullptr, int dep_target = 0) {
     C* scr = smem;
-    C* tile = smem + G::SCR_R;
+    C* tile = smem + G::SCRX;
     const int tid = threadIdx.x, line = tid / G::THR, t = tid % G::THR;
     const C* tw = static_cast<const C*>(p.tw);
     const bool nyq = MODE == MODE_MAIN && nyq_idx >= 0;
@@ -425,6 +434,197 @@ struct K {
     }
   }
 
+
+  // ------------------------------------------------------------------ row passes, two rows per line
+  // Forward pass 2 (PAIR): rows ra, ra+1 of the intermediate are Hermitian (sym part); one complex
+  // inverse FFT of Z = Ta + i Tb over all N bins (bins above H from the mirror) gives the two real
+  // rows -- no half-length pre-processing twiddles.  Same output and Nyquist term as row_c2r.
+  static __device__ void row_c2r_pair(const KParams& p, const C* __restrict__ src, int stride, int c_lo, int ncols,
+                                      int r0, int cnt, C* out_c, const T* nyqG, const T* nyqH, C* smem) {
+    C* scr = smem;
+    const int tid = threadIdx.x, line = tid / G::THC, t = tid % G::THC;
+    const C* tw = static_cast<const C*>(p.tw);
+    const T scale = T(1) / (T(N) * T(N));
+    constexpr int RPR = 2 * G::LPC;
+    T* sG = reinterpret_cast<T*>(smem + G::SCRX);
+    T* sH = sG + N;
+    if (nyqG != nullptr) {
+      for (int m = tid; m < N; m += NT) sG[m] = nyqG[m];
+      for (int i = tid; i < cnt; i += NT) sH[i] = nyqH[r0 + i];
+      __syncthreads();
+    }
+    const unsigned nc = (unsigned)ncols;
+#pragma unroll 1
+    for (int rd = 0; rd * RPR < cnt; ++rd) {
+      const int ri = rd * RPR + 2 * line;
+      const bool act = ri < cnt;
+      const int ra = r0 + ri;
+      const C* wa = src + (size_t)ra * stride - c_lo;
+      const C* wb = wa + stride;
+      C z[G::EC];
+#pragma unroll
+      for (int q = 0; q < G::EC; ++q) {
+        const int c = t + q * G::THC;
+        const bool up = c > H;
+        const int k = up ? N - c : c;
+        C a = czero<T>(), b = czero<T>();
+        if (act && (unsigned)(k - c_lo) < nc) {
+          a = __ldcg(wa + k);
+          b = __ldcg(wb + k);
+        }
+        z[q] = up ? mk<T>(a.x + b.y, b.x - a.y) : mk<T>(a.x - b.y, a.y + b.x);
+      }
+      if (rd == 0) FFST_PROBE(p, 0);
+      LineFFT<T, N, true, N>::run(z, scr + line * G::SMC, t, tw);
+      if (rd == 0) FFST_PROBE(p, 1);
+      if (act) {
+        C* oa = out_c + (size_t)ra * N;
+        C* ob = oa + N;
+        if (nyqG != nullptr) {
+          const T sa = (ra & 1) ? T(-1) : T(1);
+          const T ha = sH[ri], hb = sH[ri + 1];
+#pragma unroll
+          for (int q = 0; q < G::EC; ++q) {
+            const int m1 = t + q * G::THC;
+            const T sm = (m1 & 1) ? T(-1) : T(1);
+            const T g = sG[m1];
+            __stcs(oa + m1, mk<T>(z[q].x * scale, sa * g + sm * ha));
+            __stcs(ob + m1, mk<T>(z[q].y * scale, -sa * g + sm * hb));
+          }
+        } else {
+#pragma unroll
+          for (int q = 0; q < G::EC; ++q) {
+            const int m1 = t + q * G::THC;
+            __stcs(oa + m1, mk<T>(z[q].x * scale, T(0)));
+            __stcs(ob + m1, mk<T>(z[q].y * scale, T(0)));
+          }
+        }
+      }
+      SyncOf<G::THC>::sync();
+    }
+  }
+
+  // Inverse pass 1 (PAIR): Z = Re c(ra, .) + i Re c(ra+1, .), one forward FFT; the rows' spectra
+  // Xa[k] = (Z[k] + conj Z[N-k])/2, Xb[k] = (Z[k] - conj Z[N-k])/(2i) for the plane's bins -> tile
+  // -> W (column-major), plus the alternating sums of Im c for Nyquist planes.  Same results as
+  // row_r2c<MODE_MAIN>.
+  static __device__ void row_r2c_pair(const KParams& p, const C* __restrict__ src_c, int c_lo, int ncols, int r0,
+                                      int cnt, C* dst, int nyq_b, int nyq_idx, int nyq_group, C* smem,
+                                      const int* dep = nullptr, int dep_target = 0) {
+    C* scr = smem;
+    C* tile = smem + G::SCRX;
+    T* red = reinterpret_cast<T*>(tile + G::TILE_R);        // NT/32 scalars past the tile
+    const int tid = threadIdx.x, line = tid / G::THC, t = tid % G::THC;
+    const C* tw = static_cast<const C*>(p.tw);
+    const bool nyq = nyq_idx >= 0;
+    constexpr int RPR = 2 * G::LPC;
+    T sacc[G::EC];
+#pragma unroll
+    for (int q = 0; q < G::EC; ++q) sacc[q] = T(0);
+    constexpr int ROUNDS = G::GR / RPR > 0 ? G::GR / RPR : 1;
+    const int ntiles = (cnt + G::GR - 1) / G::GR;
+#pragma unroll 1
+    for (int ti = 0; ti < ntiles; ++ti) {
+      const int rt0 = r0 + ti * G::GR;
+#pragma unroll 1
+      for (int rd = 0; rd < ROUNDS; ++rd) {
+        const int ri = rd * RPR + 2 * line;              // first row of the pair inside the tile
+        const bool act = ri < G::GR && ti * G::GR + ri < cnt;
+        const int ra = rt0 + ri;
+        const C* rowa = src_c + (size_t)ra * N;
+        const C* rowb = rowa + N;
+        C z[G::EC];
+        T ta = T(0), tb = T(0);
+        const T sa = (ra & 1) ? T(-1) : T(1);
+#pragma unroll
+        for (int q = 0; q < G::EC; ++q) {
+          const int m = t + q * G::THC;
+          C va = czero<T>(), vb = czero<T>();
+          if (act) {
+            va = __ldcs(rowa + m);
+            vb = __ldcs(rowb + m);
+          }
+          z[q] = mk<T>(va.x, vb.x);
+          if (nyq) {
+            const T sm = (m & 1) ? T(-1) : T(1);
+            sacc[q] += sa * (va.y - vb.y);
+            ta += sm * va.y;
+            tb += sm * vb.y;
+          }
+        }
+        if (ti == 0 && rd == 0) FFST_PROBE(p, 0);
+        C* sl = scr + line * G::SMC;
+        LineFFT<T, N, false, N>::run(z, sl, t, tw);
+        if (ti == 0 && rd == 0) FFST_PROBE(p, 1);
+        if (nyq) {   // alternating row sums t(r) = sum_m1 (-1)^m1 Im c(r, m1) over the line's lanes
+#pragma unroll
+          for (int o = (G::THC < 32 ? G::THC : 32) / 2; o > 0; o >>= 1) {
+            ta += __shfl_xor_sync(0xffffffffu, ta, o);
+            tb += __shfl_xor_sync(0xffffffffu, tb, o);
+          }
+          if constexpr (G::THC > 32) {
+            __syncthreads();
+            if ((tid & 31) == 0) { red[(tid >> 5) * 2] = ta; red[(tid >> 5) * 2 + 1] = tb; }
+            __syncthreads();
+            if (t == 0) {
+              ta = tb = T(0);
+              for (int w = 0; w < G::THC / 32; ++w) {
+                ta += red[((line * G::THC) / 32 + w) * 2];
+                tb += red[((line * G::THC) / 32 + w) * 2 + 1];
+              }
+            }
+          }
+          if (t == 0 && act) {
+            T* tt = static_cast<T*>(p.nyq_T) + ((size_t)nyq_b * p.n_nyq + nyq_idx) * N + ra;
+            tt[0] = ta;
+            tt[1] = tb;
+          }
+        }
+        SyncOf<G::THC>::sync();
+#pragma unroll
+        for (int q = 0; q < G::EC; ++q) sl[Pad<T>::at(t + q * G::THC)] = z[q];
+        SyncOf<G::THC>::sync();
+        if (act) {
+#pragma unroll 2
+          for (int kk = t; kk < ncols; kk += G::THC) {
+            const int k = c_lo + kk;                         // 0..H
+            const C zk = sl[Pad<T>::at(k)];
+            const C zm = sl[Pad<T>::at(k == 0 ? 0 : N - k)];
+            tile[ri * G::TSTR + kk] = mk<T>(T(0.5) * (zk.x + zm.x), T(0.5) * (zk.y - zm.y));
+            tile[(ri + 1) * G::TSTR + kk] = mk<T>(T(0.5) * (zk.y + zm.y), T(0.5) * (zm.x - zk.x));
+          }
+        }
+        SyncOf<G::THC>::sync();
+        if (ti == 0 && rd == 0) FFST_PROBE(p, 2);
+      }
+      if (dep != nullptr && ti == 0 && tid == 0) spin_wait(dep, dep_target);   // slot reuse: before the first write
+      __syncthreads();
+      const int rows_here = cnt - ti * G::GR < G::GR ? cnt - ti * G::GR : G::GR;
+#pragma unroll 1
+      for (int e = tid; e < ncols * G::GR; e += NT) {
+        const int kk = e / G::GR, ri = e - kk * G::GR;
+        if (ri < rows_here) dst[(size_t)kk * N + rt0 + ri] = tile[ri * G::TSTR + kk];
+      }
+      __syncthreads();
+      if (ti == 0) FFST_PROBE(p, 3);
+    }
+    if (nyq) {
+      // partial alternating column sums s(m1) over this item's rows: lines summed in fixed order
+      T* rs = reinterpret_cast<T*>(scr);                    // [LPC][N] scalars (fits SCR_C)
+#pragma unroll
+      for (int q = 0; q < G::EC; ++q) rs[line * N + t + q * G::THC] = sacc[q];
+      __syncthreads();
+      T* outp = static_cast<T*>(p.nyq_S) + (((size_t)nyq_b * p.n_nyq + nyq_idx) * p.n_rowitems + nyq_group) * N;
+#pragma unroll 1
+      for (int m = tid; m < N; m += NT) {
+        T v = T(0);
+        for (int l = 0; l < G::LPC; ++l) v += rs[l * N + m];
+        outp[m] = v;
+      }
+      __syncthreads();
+    }
+  }
+
   // ------------------------------------------------------------------ column FFT items
   // inverse pass 2: columns [g0, g0+LPC) of image b over the planes of one chunk:
   // FFT along r of W, * sym_i, summed over planes, written / accumulated into A[b].
@@ -522,7 +722,8 @@ struct K {
         nyqH = nyqG + N;
       }
       C* out = static_cast<C*>(p.coeff) + ((size_t)I.b * p.eta_l + I.p) * N * N;
-      row_c2r<MODE_MAIN>(p, w, P.ncols_pad, P.c_lo, P.ncols, r0, cnt, out, nullptr, nyqG, nyqH, smem);
+      if constexpr (G::PAIR_FWD) row_c2r_pair(p, w, P.ncols_pad, P.c_lo, P.ncols, r0, cnt, out, nyqG, nyqH, smem);
+      else row_c2r<MODE_MAIN>(p, w, P.ncols_pad, P.c_lo, P.ncols, r0, cnt, out, nullptr, nyqG, nyqH, smem);
     }
   }
 
@@ -533,7 +734,11 @@ struct K {
       const int r0 = I.group * G::RPI;
       const int cnt = N - r0 < G::RPI ? N - r0 : G::RPI;
       const C* src = static_cast<const C*>(p.coeff) + ((size_t)I.b * p.eta_l + I.p) * N * N;
-      row_r2c<MODE_MAIN>(p, src, nullptr, P.c_lo, P.ncols, r0, cnt, w, I.b, P.nyq, I.group, smem,
+      if constexpr (G::PAIR_INV)
+        row_r2c_pair(p, src, P.c_lo, P.ncols, r0, cnt, w, I.b, P.nyq, I.group, smem,
+                     I.wait_ctr >= 0 ? p.ctr + I.wait_ctr : nullptr, I.wait_tgt);
+      else
+        row_r2c<MODE_MAIN>(p, src, nullptr, P.c_lo, P.ncols, r0, cnt, w, I.b, P.nyq, I.group, smem,
                          I.wait_ctr >= 0 ? p.ctr + I.wait_ctr : nullptr, I.wait_tgt);
     } else {
       col_fft_acc(p, I, splanes, smem);
