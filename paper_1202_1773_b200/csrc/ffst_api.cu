@@ -217,6 +217,7 @@ struct ffst_plan {
   void *F = nullptr, *Fscr = nullptr, *A = nullptr, *W = nullptr;
   long long W_elems = 0;
   void *nyq_fwd = nullptr, *nyq_S = nullptr, *nyq_T = nullptr, *corr = nullptr, *nyq_anti = nullptr;
+  void* nyq_part = nullptr;
   void* stage = nullptr;          // host-variant image staging [batch][n][n]
   int* d_ctr = nullptr;
   size_t ctr_cap = 0;
@@ -530,7 +531,7 @@ KParams base_params(ffst_plan* p) {
   k.rtab = p->d_rtab;
   k.colrec = p->d_colrec;
   k.F = p->F; k.Fscr = p->Fscr; k.A = p->A; k.W = p->W;
-  k.nyq_fwd = p->nyq_fwd; k.nyq_S = p->nyq_S; k.nyq_T = p->nyq_T; k.corr = p->corr; k.nyq_anti = p->nyq_anti;
+  k.nyq_fwd = p->nyq_fwd; k.nyq_S = p->nyq_S; k.nyq_T = p->nyq_T; k.corr = p->corr; k.nyq_anti = p->nyq_anti; k.nyq_part = p->nyq_part;
   k.n_rowitems = p->n_rowitems;
   k.a_lane_elems = (long long)p->d.batch * (p->n / 2 + 1) * p->n;
   if (const char* d = std::getenv("FFST_DBG")) k.dbg = std::atoi(d);
@@ -657,8 +658,8 @@ ffst_status inverse_impl(ffst_plan* p, const void* coeff, void* img_out, int bat
   ++nl;
   if (p->timing) API_CUDA(cudaEventRecord(p->ev[5], s), "event");
   if (!p->nyq.empty()) {
-    API_CUDA(L_nyq_inv(p, k, batch, s), "nyq_inv kernel");
-    ++nl;
+    API_CUDA(L_nyq_inv(p, k, batch, s), "nyq_inv kernels");
+    nl += 2;
   }
   API_CUDA(L_final(p, k, batch, s), "final kernels");
   nl += 2;
@@ -857,6 +858,7 @@ ffst_status ffst_plan_create(ffst_plan** out, const ffst_plan_desc* d) {
   ALLOC(p->nyq_T, B * nn * N * p->rsz);
   ALLOC(p->corr, B * 2 * N * p->rsz);
   ALLOC(p->nyq_anti, nn * 2 * N * p->rsz);
+  ALLOC(p->nyq_part, B * 2 * std::min<size_t>(nn, 64) * N * csz);
   ALLOC(p->stage, B * N * N * p->rsz);
 #undef ALLOC
   std::vector<unsigned char> tw;

@@ -65,6 +65,7 @@ struct KParams {
   void* nyq_S;                  // [batch][n_nyq][n_rowitems][n] T: partial alternating column sums
   void* nyq_T;                  // [batch][n_nyq][n] T: alternating row sums
   void* corr;                   // [batch][2][n] T: inverse Nyquist corrections
+  void* nyq_part;               // [batch][2][<=64][n] cpx<T>: partial Nyquist spectra (stage 1 -> 2)
   const void* nyq_anti;         // [n_nyq][2][n] T: anti part of each Nyquist plane on the Nyquist row (0) /
                                 //   column (1), natural bin order (plan table)
   int n_rowitems;               // inverse pass-1 items per plane (row groups)

@@ -931,8 +931,10 @@ __global__ void __launch_bounds__(256) nyq_fwd_kernel(KParams p) {
   }
 }
 
-// inverse Nyquist correction: grid (2, B).  Line l accumulates the Nyquist planes
-// l, l + LPC, ...; the per-line sums are added in fixed line order (deterministic).
+// inverse Nyquist correction, stage 1: grid (2, B, G).  CTA g takes the rounds g, g + G, ... of
+// LPC Nyquist planes (line l: plane round * LPC + l); its per-line sums are added in fixed line
+// order and written as partial spectrum g; stage 2 (nyq_fin_kernel) adds the G partials in order
+// and synthesises the correction (deterministic; G > 1 spreads the planes over the GPU at large n).
 template <typename T, int N>
 __global__ void __launch_bounds__(256) nyq_inv_kernel(KParams p) {
   extern __shared__ __align__(128) unsigned char smem_raw[];
@@ -951,7 +953,7 @@ __global__ void __launch_bounds__(256) nyq_inv_kernel(KParams p) {
   for (int q = 0; q < G::EC; ++q) acc[q] = czero<T>();
   const int rounds = (p.n_nyq + G::LPC - 1) / G::LPC;
 #pragma unroll 1
-  for (int rd = 0; rd < rounds; ++rd) {
+  for (int rd = blockIdx.z; rd < rounds; rd += gridDim.z) {
     const int nq = rd * G::LPC + line;
     const bool act = nq < p.n_nyq;
     C r[G::EC];
@@ -993,14 +995,37 @@ __global__ void __launch_bounds__(256) nyq_inv_kernel(KParams p) {
       acc[q] = s;
     }
   }
-  __syncthreads();
-  LineFFT<T, N, true, N>::run(acc, scr, t, tw);
   if (line == 0) {
-    T* out = static_cast<T*>(p.corr) + ((size_t)b * 2 + which) * N;
-    const T s = T(1) / (T(N) * T(N));
+    C* part = static_cast<C*>(p.nyq_part) + (((size_t)b * 2 + which) * gridDim.z + blockIdx.z) * N;
 #pragma unroll
-    for (int q = 0; q < G::EC; ++q) out[t + q * G::THC] = acc[q].y * s;
+    for (int q = 0; q < G::EC; ++q) part[t + q * G::THC] = acc[q];
   }
+}
+
+// inverse Nyquist correction, stage 2: grid (2, B); the G partial spectra summed in order, inverse
+// DFT, imaginary part scaled -> corr
+template <typename T, int N>
+__global__ void __launch_bounds__(256) nyq_fin_kernel(KParams p, int groups) {
+  extern __shared__ __align__(128) unsigned char smem_raw[];
+  using G = Geo<T, N>;
+  using C = cpx<T>;
+  const int which = blockIdx.x, b = blockIdx.y;
+  const int tid = threadIdx.x, line = tid / G::THC, t = tid % G::THC;
+  // every line computes the same result (a CTA is at least a warp); line 0 stores it
+  const C* part = static_cast<const C*>(p.nyq_part) + ((size_t)b * 2 + which) * groups * N;
+  C acc[G::EC];
+#pragma unroll
+  for (int q = 0; q < G::EC; ++q) acc[q] = czero<T>();
+#pragma unroll 1
+  for (int g = 0; g < groups; ++g)
+#pragma unroll
+    for (int q = 0; q < G::EC; ++q) acc[q] = cadd<T>(acc[q], part[(size_t)g * N + t + q * G::THC]);
+  LineFFT<T, N, true, N>::run(acc, reinterpret_cast<C*>(smem_raw) + line * G::SMC, t, static_cast<const C*>(p.tw));
+  if (line > 0) return;
+  T* out = static_cast<T*>(p.corr) + ((size_t)b * 2 + which) * N;
+  const T s = T(1) / (T(N) * T(N));
+#pragma unroll
+  for (int q = 0; q < G::EC; ++q) out[t + q * G::THC] = acc[q].y * s;
 }
 
 // materialise spectra (tests only): psi[i][row][col], grid-stride

@@ -4,6 +4,8 @@
 
 namespace ffst {
 
+constexpr int NYQ_GROUPS_MAX = 64;   // stage-1 CTAs per (direction, image) of the Nyquist correction
+
 template <typename T> struct MaxN;
 template <> struct MaxN<float> { static constexpr int v = 4096; };
 template <> struct MaxN<double> { static constexpr int v = 2048; };
@@ -82,8 +84,16 @@ template <typename T, int N> struct Launch {
     return cudaGetLastError();
   }
   static cudaError_t nyq_inv(const KParams& p, int batch, cudaStream_t s) {
+    const int rounds = (p.n_nyq + G::LPC - 1) / G::LPC;
+    const int groups = rounds < NYQ_GROUPS_MAX ? rounds : NYQ_GROUPS_MAX;
     FFST_CHECK(set_smem(nyq_inv_kernel<T, N>, G::SMEM_NYQ));
-    nyq_inv_kernel<T, N><<<dim3(2, batch), G::NT, G::SMEM_NYQ, s>>>(p);
+    nyq_inv_kernel<T, N><<<dim3(2, batch, groups), G::NT, G::SMEM_NYQ, s>>>(p);
+    FFST_CHECK(cudaGetLastError());
+    // stage 2: one line per CTA (THC threads; at least a warp)
+    const int nt = G::THC < 32 ? 32 : G::THC;
+    const size_t sm = (size_t)(nt / G::THC) * G::SMC * sizeof(cpx<T>);
+    FFST_CHECK(set_smem(nyq_fin_kernel<T, N>, sm));
+    nyq_fin_kernel<T, N><<<dim3(2, batch), nt, sm, s>>>(p, groups);
     return cudaGetLastError();
   }
   static cudaError_t final_(const KParams& p, int batch, cudaStream_t s) {
