@@ -34,7 +34,7 @@ struct Geo {
   static constexpr bool PAIR = 2 * LPC == LPR;
   // measured: the pair form wins for the inverse row pass (configs 2-5) and loses for the forward
   // one at n >= 512 (its stores are 8-byte instead of 16-byte per lane): inverse only
-  static constexpr bool PAIR_FWD = false, PAIR_INV = PAIR;
+  static constexpr bool PAIR_FWD = false, PAIR_INV = PAIR && sizeof(T) == 4;   // float64: registers
   static constexpr int SCRX = SCR_C > SCR_R ? SCR_C : SCR_R;
   // forward pass 1: columns per item (>= 32-byte row segments of the intermediate)
   static constexpr int GC = LPC > (32 / ESZ) ? LPC : (32 / ESZ);
@@ -78,6 +78,15 @@ template <> __device__ __forceinline__ void store_pair_cs<double>(double2* dst, 
   __stcs(dst, a);
   __stcs(dst + 1, b);
 }
+// fire-and-forget accumulation in L2 (the accumulation chain orders the additions: deterministic)
+template <typename T> __device__ __forceinline__ void red_add(cpx<T>* dst, cpx<T> v);
+template <> __device__ __forceinline__ void red_add<float>(float2* dst, float2 v) {
+  asm volatile("red.relaxed.gpu.global.add.v2.f32 [%0], {%1, %2};" ::"l"(dst), "f"(v.x), "f"(v.y) : "memory");
+}
+template <> __device__ __forceinline__ void red_add<double>(double2* dst, double2 v) {
+  asm volatile("red.relaxed.gpu.global.add.f64 [%0], %1;" ::"l"(&dst->x), "d"(v.x) : "memory");
+  asm volatile("red.relaxed.gpu.global.add.f64 [%0], %1;" ::"l"(&dst->y), "d"(v.y) : "memory");
+}
 template <typename T> __device__ __forceinline__ void store_pair_cg(cpx<T>* dst, cpx<T> a, cpx<T> b);
 template <> __device__ __forceinline__ void store_pair_cg<float>(float2* dst, float2 a, float2 b) {
   __stcg(reinterpret_cast<float4*>(dst), make_float4(a.x, a.y, b.x, b.y));
@@ -111,10 +120,19 @@ __device__ __forceinline__ unsigned smid() {
 __shared__ unsigned long long s_probe[4];   // intra-item probes (trace mode)
 #define FFST_PROBE(p, i) do { if ((p).trace != nullptr && threadIdx.x == 0) s_probe[i] = gtimer(); } while (0)
 
+// Dependency counters.  The data behind a counter is read only through L2 (ld.global.cg, TMA),
+// so the waiting side needs no L1 invalidation: relaxed (volatile) polls.  The publishing side uses
+// red.release (MEMBAR.ALL.GPU + RED) -- __threadfence would add CCTL.IVALL, flushing the L1 copies
+// of the twiddle and radial tables on every item.
 __device__ __forceinline__ void spin_wait(const int* ctr, int target) {
   const volatile int* v = ctr;
   while (*v < target) __nanosleep(40);
-  __threadfence();
+}
+__device__ __forceinline__ void red_release(int* ctr, int v) {
+  asm volatile("red.release.gpu.global.add.s32 [%0], %1;" ::"l"(ctr), "r"(v) : "memory");
+}
+__device__ __forceinline__ void red_relaxed(int* ctr, int v) {
+  asm volatile("red.relaxed.gpu.global.add.s32 [%0], %1;" ::"l"(ctr), "r"(v) : "memory");
 }
 
 template <typename T, int N>
@@ -536,13 +554,27 @@ struct K {
         C z[G::EC];
         T ta = T(0), tb = T(0);
         const T sa = (ra & 1) ? T(-1) : T(1);
+        // float32: every load of the round in flight before any use (float64: registers too scarce)
+        constexpr int PH = sizeof(T) == 4 ? G::EC : 1;
+        C va_[PH], vb_[PH];
+        if constexpr (PH > 1) {
+#pragma unroll
+          for (int q = 0; q < G::EC; ++q) {
+            const int m = t + q * G::THC;
+            va_[q] = act ? __ldcs(rowa + m) : czero<T>();
+            vb_[q] = act ? __ldcs(rowb + m) : czero<T>();
+          }
+        }
 #pragma unroll
         for (int q = 0; q < G::EC; ++q) {
           const int m = t + q * G::THC;
-          C va = czero<T>(), vb = czero<T>();
-          if (act) {
-            va = __ldcs(rowa + m);
-            vb = __ldcs(rowb + m);
+          C va, vb;
+          if constexpr (PH > 1) {
+            va = va_[q];
+            vb = vb_[q];
+          } else {
+            va = act ? __ldcs(rowa + m) : czero<T>();
+            vb = act ? __ldcs(rowb + m) : czero<T>();
           }
           z[q] = mk<T>(va.x, vb.x);
           if (nyq) {
@@ -673,12 +705,8 @@ struct K {
 #pragma unroll
       for (int q = 0; q < G::EC; ++q) {
         const int idx = t + q * G::THC;
-        if (I.first) {
-          a[idx] = acc[q];
-        } else {
-          const C o = __ldcg(a + idx);
-          a[idx] = mk<T>(o.x + acc[q].x, o.y + acc[q].y);
-        }
+        if (I.first) __stcg(a + idx, acc[q]);
+        else red_add<T>(a + idx, acc[q]);          // no read-modify-write latency
       }
     }
   }
@@ -801,9 +829,9 @@ __device__ __forceinline__ void persistent_loop(const KParams& p) {
     else K<T, N>::inv_item(p, I, s_planes, smem);
     __syncthreads();
     if (threadIdx.x == 0) {
-      if (!FWD || I.type == 0) __threadfence();
-      atomicAdd(p.ctr + I.sig_ctr, 1);
-      if (I.sig2_ctr >= 0) atomicAdd(p.ctr + I.sig2_ctr, 1);
+      if (!FWD || I.type == 0) red_release(p.ctr + I.sig_ctr, 1);   // another item reads what this one wrote
+      else red_relaxed(p.ctr + I.sig_ctr, 1);                         // forward pass 2: reads only (WAR)
+      if (I.sig2_ctr >= 0) red_release(p.ctr + I.sig2_ctr, 1);
     }
     if (p.trace != nullptr && threadIdx.x == 0) {
       unsigned long long* tr = p.trace + 8 * (size_t)it;

@@ -63,12 +63,6 @@ __device__ __forceinline__ bool ctr_reached(const int* ctr, int target) {
 __device__ __forceinline__ void spin_until(const int* ctr, int target) {
   while (!ctr_reached(ctr, target)) __nanosleep(64);
 }
-__device__ __forceinline__ void red_release(int* ctr, int v) {
-  asm volatile("red.release.gpu.global.add.s32 [%0], %1;" ::"l"(ctr), "r"(v) : "memory");
-}
-__device__ __forceinline__ void red_relaxed(int* ctr, int v) {
-  asm volatile("red.relaxed.gpu.global.add.s32 [%0], %1;" ::"l"(ctr), "r"(v) : "memory");
-}
 
 // per-warp intra-item probes (trace mode, first stage of an item only)
 __shared__ unsigned long long s_wprobe[32][4];
