@@ -107,6 +107,18 @@ ffst_status ffst_plane_is_nyquist(int n, int j0, int index, int* is_nyquist);
 
 /* ---- plans ------------------------------------------------------------- */
 
+/* Create a plan: all tables (index order, pruning ranges, radial factors, Nyquist anti-window
+ * edges, work queues) and all device workspace are built here; transforms allocate nothing.
+ * Errors: INVALID_SIZE (n < 4 or above the built sizes), UNSUPPORTED (n not a power of two,
+ * variant != CLASSIC, more than 256 local planes), INVALID_ARG, OOM, CUDA.
+ * Environment (read here, tuning only; results are identical up to rounding order):
+ *   FFST_PATH=warp      warp-worker kernels for 8 <= n <= 512 (default: CTA-item kernels)
+ *   FFST_RING_MB        intermediate ring budget (default 80; at least 12 slots)
+ *   FFST_CHUNK_PLANES   planes per chunk (default 4; 32 for batch <= 4)
+ *   FFST_SLOT_KB        chunk byte budget (default 4096)
+ *   FFST_ACC_LANES      accumulator lanes of the inverse (default: up to 4 while <= 32 MB)
+ *   FFST_VERBOSE        print the queue geometry
+ * Measurement only (results are WRONG): FFST_QUEUE_ONLY=1|2 (one pass type), FFST_DBG bits. */
 ffst_status ffst_plan_create(ffst_plan** out, const ffst_plan_desc* desc);
 ffst_status ffst_plan_destroy(ffst_plan* plan);
 

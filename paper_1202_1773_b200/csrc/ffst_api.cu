@@ -229,6 +229,8 @@ struct ffst_plan {
   int trace_items[2] = {0, 0};
   bool tracing = false;
   cudaEvent_t ev[8] = {};
+  cudaStream_t aux = nullptr;     // side stream of the inverse (Nyquist correction beside the final column pass)
+  cudaEvent_t fork[2] = {};
   int launches[2] = {0, 0};
   std::vector<void*> allocs;
 };
@@ -558,8 +560,8 @@ cudaError_t L_inv_main(ffst_plan* p, const KParams& k, int g, cudaStream_t s) {
 cudaError_t L_nyq_inv(ffst_plan* p, const KParams& k, int b, cudaStream_t s) {
   return p->d.dtype == FFST_F32 ? launch_nyq_inv<float>(k, b, s) : launch_nyq_inv<double>(k, b, s);
 }
-cudaError_t L_final(ffst_plan* p, const KParams& k, int b, cudaStream_t s) {
-  return p->d.dtype == FFST_F32 ? launch_final<float>(k, b, s) : launch_final<double>(k, b, s);
+cudaError_t L_final(ffst_plan* p, const KParams& k, int b, int which, cudaStream_t s) {
+  return p->d.dtype == FFST_F32 ? launch_final<float>(k, b, which, s) : launch_final<double>(k, b, which, s);
 }
 
 bool aligned16(const void* ptr) { return (reinterpret_cast<uintptr_t>(ptr) & 15u) == 0; }
@@ -658,10 +660,16 @@ ffst_status inverse_impl(ffst_plan* p, const void* coeff, void* img_out, int bat
   ++nl;
   if (p->timing) API_CUDA(cudaEventRecord(p->ev[5], s), "event");
   if (!p->nyq.empty()) {
-    API_CUDA(L_nyq_inv(p, k, batch, s), "nyq_inv kernels");
+    // fork: the Nyquist correction (needed only by the final row pass) beside the column pass
+    API_CUDA(cudaEventRecord(p->fork[0], s), "event");
+    API_CUDA(cudaStreamWaitEvent(p->aux, p->fork[0], 0), "stream wait");
+    API_CUDA(L_nyq_inv(p, k, batch, p->aux), "nyq_inv kernels");
+    API_CUDA(cudaEventRecord(p->fork[1], p->aux), "event");
     nl += 2;
   }
-  API_CUDA(L_final(p, k, batch, s), "final kernels");
+  API_CUDA(L_final(p, k, batch, 0, s), "final column pass");
+  if (!p->nyq.empty()) API_CUDA(cudaStreamWaitEvent(s, p->fork[1], 0), "stream wait");
+  API_CUDA(L_final(p, k, batch, 1, s), "final row pass");
   nl += 2;
   if (p->timing) API_CUDA(cudaEventRecord(p->ev[6], s), "event");
   p->launches[1] = nl;
@@ -734,6 +742,9 @@ ffst_status ffst_plan_destroy(ffst_plan* p) {
   for (void* a : p->allocs) cudaFree(a);
   for (auto& e : p->ev)
     if (e) cudaEventDestroy(e);
+  for (auto& e : p->fork)
+    if (e) cudaEventDestroy(e);
+  if (p->aux) cudaStreamDestroy(p->aux);
   if (cur >= 0) cudaSetDevice(cur);
   delete p;
   return FFST_OK;
@@ -920,6 +931,12 @@ ffst_status ffst_plan_create(ffst_plan** out, const ffst_plan_desc* d) {
     e = cudaEventCreate(&ev);
     if (e != cudaSuccess) return cleanup(cuda_fail(e, "event create"));
   }
+  for (auto& ev : p->fork) {
+    e = cudaEventCreateWithFlags(&ev, cudaEventDisableTiming);
+    if (e != cudaSuccess) return cleanup(cuda_fail(e, "event create"));
+  }
+  e = cudaStreamCreateWithFlags(&p->aux, cudaStreamNonBlocking);
+  if (e != cudaSuccess) return cleanup(cuda_fail(e, "stream create"));
   Queue* q = nullptr;
   st = build_queue(p, d->batch, &q);
   if (st != FFST_OK) return cleanup(st);

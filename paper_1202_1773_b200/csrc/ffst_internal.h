@@ -104,7 +104,7 @@ template <typename T> cudaError_t launch_inv_warp(const KParams& p, int grid, cu
 template <typename T> cudaError_t launch_fwd_main(const KParams& p, int grid, cudaStream_t s);
 template <typename T> cudaError_t launch_inv_main(const KParams& p, int grid, cudaStream_t s);
 template <typename T> cudaError_t launch_nyq_inv(const KParams& p, int batch, cudaStream_t s);
-template <typename T> cudaError_t launch_final(const KParams& p, int batch, cudaStream_t s);
+template <typename T> cudaError_t launch_final(const KParams& p, int batch, int which, cudaStream_t s);
 template <typename T> cudaError_t launch_spectra_export(const KParams& p, void* psi, int centred, cudaStream_t s);
 template <typename T> int max_active_main(int n, int device, int which);   // CTAs/SM of fwd (0) / inv (1)
 

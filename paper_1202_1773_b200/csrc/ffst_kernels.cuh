@@ -43,6 +43,7 @@ struct Geo {
   // forward pass 2 / final rows: rows per item (~128 KB of output)
   static constexpr int RP2_ = (131072 / (N * ESZ)) > LPR ? (131072 / (N * ESZ)) : LPR;
   static constexpr int RP2 = RP2_ < N ? RP2_ : N;
+  static constexpr int RPF = LPR < N ? LPR : N;     // final row pass: one round per CTA (more CTAs)
   // inverse pass 1: rows per tile and per item
   static constexpr int GR_ = LPR > (32 / ESZ) ? LPR : (32 / ESZ);
   static constexpr int GR = GR_ < N ? GR_ : N;
@@ -258,6 +259,7 @@ struct K {
     const C* tw = static_cast<const C*>(p.tw);
     const T scale = T(1) / (T(N) * T(N));
     constexpr int ROUNDS = G::RP2 / G::LPR > 0 ? G::RP2 / G::LPR : 1;
+    const int rounds = (cnt + G::LPR - 1) / G::LPR < ROUNDS ? (cnt + G::LPR - 1) / G::LPR : ROUNDS;
     // Nyquist terms of this item staged in shared memory: G(m1) for all m1, H(r) for its rows
     T* sG = reinterpret_cast<T*>(smem + G::SCRX);
     T* sH = sG + N;
@@ -267,7 +269,7 @@ struct K {
       __syncthreads();
     }
 #pragma unroll 1
-    for (int rd = 0; rd < ROUNDS; ++rd) {
+    for (int rd = 0; rd < rounds; ++rd) {
       const int ri = rd * G::LPR + line;
       const bool act = ri < cnt;
       const int r = r0 + ri;
@@ -899,8 +901,8 @@ __global__ void __launch_bounds__(256) fin_rows_kernel(KParams p) {
   extern __shared__ __align__(128) unsigned char smem_raw[];
   using G = Geo<T, N>;
   const int b = blockIdx.y;
-  const int r0 = blockIdx.x * G::RP2;
-  const int cnt = N - r0 < G::RP2 ? N - r0 : G::RP2;
+  const int r0 = blockIdx.x * G::RPF;
+  const int cnt = N - r0 < G::RPF ? N - r0 : G::RPF;
   const cpx<T>* src = static_cast<const cpx<T>*>(p.Fscr) + (size_t)b * N * G::NCPF;
   T* out = static_cast<T*>(p.img_out) + (size_t)b * N * N;
   const T* cg = nullptr;

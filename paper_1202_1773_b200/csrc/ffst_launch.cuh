@@ -96,12 +96,16 @@ template <typename T, int N> struct Launch {
     nyq_fin_kernel<T, N><<<dim3(2, batch), nt, sm, s>>>(p, groups);
     return cudaGetLastError();
   }
-  static cudaError_t final_(const KParams& p, int batch, cudaStream_t s) {
-    FFST_CHECK(set_smem(fin_cols_kernel<T, N>, G::SMEM_FWD));
-    fin_cols_kernel<T, N><<<dim3((N / 2 + 1 + G::GC - 1) / G::GC, batch), G::NT, G::SMEM_FWD, s>>>(p);
-    FFST_CHECK(cudaGetLastError());
+  // final pass, split so the Nyquist correction can run beside the column pass (it is only
+  // needed by the row pass): which = 0 column pass, 1 row pass
+  static cudaError_t final_(const KParams& p, int batch, int which, cudaStream_t s) {
+    if (which == 0) {
+      FFST_CHECK(set_smem(fin_cols_kernel<T, N>, G::SMEM_FWD));
+      fin_cols_kernel<T, N><<<dim3((N / 2 + 1 + G::GC - 1) / G::GC, batch), G::NT, G::SMEM_FWD, s>>>(p);
+      return cudaGetLastError();
+    }
     FFST_CHECK(set_smem(fin_rows_kernel<T, N>, G::SMEM_FWD));
-    fin_rows_kernel<T, N><<<dim3((N + G::RP2 - 1) / G::RP2, batch), G::NT, G::SMEM_FWD, s>>>(p);
+    fin_rows_kernel<T, N><<<dim3((N + G::RPF - 1) / G::RPF, batch), G::NT, G::SMEM_FWD, s>>>(p);
     return cudaGetLastError();
   }
   static cudaError_t spectra(const KParams& p, void* psi, int centred, cudaStream_t s) {
@@ -159,8 +163,8 @@ template <typename T, int N> struct Launch {
     FFST_DISPATCH(T, p.n, inv_main(p, g, s), cudaErrorInvalidValue) }                                          \
   template <> cudaError_t launch_nyq_inv<T>(const KParams& p, int b, cudaStream_t s) {                         \
     FFST_DISPATCH(T, p.n, nyq_inv(p, b, s), cudaErrorInvalidValue) }                                           \
-  template <> cudaError_t launch_final<T>(const KParams& p, int b, cudaStream_t s) {                           \
-    FFST_DISPATCH(T, p.n, final_(p, b, s), cudaErrorInvalidValue) }                                            \
+  template <> cudaError_t launch_final<T>(const KParams& p, int b, int which, cudaStream_t s) {                \
+    FFST_DISPATCH(T, p.n, final_(p, b, which, s), cudaErrorInvalidValue) }                                            \
   template <> cudaError_t launch_spectra_export<T>(const KParams& p, void* psi, int c, cudaStream_t s) {       \
     FFST_DISPATCH(T, p.n, spectra(p, psi, c, s), cudaErrorInvalidValue) }                                      \
   template <> int max_active_main<T>(int n, int device, int which) {                                           \
