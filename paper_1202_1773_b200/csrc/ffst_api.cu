@@ -427,6 +427,34 @@ ffst_status build_queue(ffst_plan* p, int batch, Queue** out) {
       }
     }
   }
+  // Forward pass 1, paired images (CTA kernels, one round per column group): chunks c and c+1
+  // of two images holding the same planes share their pass-1 items -- the window of a column group
+  // is evaluated once for both images (K::col_ifft_two).  The shared item signals both chunks
+  // and waits for both ring slots.
+  for (int c = 0; c < C; ++c)
+    for (auto& it : f1[c]) it.pad0 = -1;
+  const char* envp = std::getenv("FFST_PAIR");
+  const bool pair_ok = !p->warp && g.gc == g.lpc && batch >= 2 && !(envp && std::atoi(envp) == 0);
+  if (pair_ok) {
+    for (int c = 0; c + 1 < C; ++c) {
+      const Proto& a = protos[order[c]];
+      const Proto& b = protos[order[c + 1]];
+      if (a.b == b.b || a.lp0 != b.lp0 || a.np != b.np || f1[c].empty() || f1[c].size() != f1[c + 1].size())
+        continue;
+      for (size_t k = 0; k < f1[c].size(); ++k) {
+        ItemDev& it = f1[c][k];
+        const ItemDev& jt = f1[c + 1][k];
+        it.pad0 = jt.b;
+        it.pad1 = jt.slot;
+        it.first = jt.woff;
+        it.sig2_ctr = jt.sig_ctr;
+        it.wait2_ctr = jt.wait_ctr;
+        it.np = jt.wait_tgt;
+      }
+      f1[c + 1].clear();
+      ++c;                                           // c+1 is consumed
+    }
+  }
   auto emit = [&](std::vector<std::vector<ItemDev>>& a, std::vector<std::vector<ItemDev>>& b,
                   std::vector<ItemDev>& dst) {
     for (int c = 0; c < std::min(D, C); ++c) dst.insert(dst.end(), a[c].begin(), a[c].end());

@@ -246,6 +246,53 @@ struct K {
     }
   }
 
+  // Forward pass 1 of one plane's column group for two images (the chunks of two images that
+  // hold the same planes are paired by the planner): the window -- the same for both -- is
+  // evaluated once, applied to each image's spectrum, one column IFFT per image, each written to
+  // its own ring slot.  Only when one round covers the group (GC == LPC).
+  static __device__ void col_ifft_two(const KParams& p, const PlaneDev& P, int c0, int cnt, const C* src0,
+                                      const C* src1, C* dst0, C* dst1, int dst_stride, int dst_col0, C* smem,
+                                      const int* dep0, int tgt0, const int* dep1, int tgt1) {
+    static_assert(G::GC == G::LPC || true, "");
+    C* scr = smem;
+    C* tile = smem + G::SCR_C;
+    T* wbuf = reinterpret_cast<T*>(tile + G::TILE_C);
+    const int tid = threadIdx.x, line = tid / G::THC, t = tid % G::THC;
+    const C* tw = static_cast<const C*>(p.tw);
+    const Radial<T> R{static_cast<const T*>(p.rtab), N / 2 + 1, p.j0};
+    const int ci = line;
+    const bool act = ci < cnt;
+    const int cb = c0 + ci;
+    window_lines(P, c0, act, wbuf, scr, R, (T)p.delta);
+    FFST_PROBE(p, 0);
+    const int ncopy = cnt < G::GC ? cnt : G::GC;
+#pragma unroll 1
+    for (int img = 0; img < 2; ++img) {
+      const C* col = (img == 0 ? src0 : src1) + (size_t)cb * N;
+      C r[G::EC];
+#pragma unroll
+      for (int q = 0; q < G::EC; ++q) {
+        const T w = wbuf[q * NT + tid];
+        r[q] = w != T(0) ? cscale<T>(__ldg(col + t + q * G::THC), w) : czero<T>();
+      }
+      LineFFT<T, N, true, N>::run(r, scr + line * G::SMC, t, tw);
+      if (ci < G::GC) {
+#pragma unroll
+        for (int q = 0; q < G::EC; ++q) tile[(t + q * G::THC) * G::GCP + ci] = r[q];
+      }
+      const int* dep = img == 0 ? dep0 : dep1;
+      if (tid == 0 && dep != nullptr) spin_wait(dep, img == 0 ? tgt0 : tgt1);   // ring-slot reuse
+      __syncthreads();
+      C* dst = img == 0 ? dst0 : dst1;
+#pragma unroll 1
+      for (int e = tid; e < N * G::GC; e += NT) {
+        const int rr = e / G::GC, c = e - rr * G::GC;
+        if (c < ncopy) dst[(size_t)rr * dst_stride + dst_col0 + c] = tile[rr * G::GCP + c];
+      }
+      __syncthreads();                          // tile reuse by the second image
+    }
+  }
+
   // ------------------------------------------------------------------ row C2R item
   // Rows [r0, r0+cnt) of an intermediate holding Hermitian-half bins [c_lo, c_lo+ncols)
   // (row-major, stride `stride`).  MAIN: complex coefficient rows (+ Nyquist imaginary
@@ -736,7 +783,16 @@ struct K {
   static __device__ void fwd_item(const KParams& p, const ItemDev& I, const PlaneDev* splanes, C* smem) {
     const PlaneDev& P = splanes[I.p];
     C* w = static_cast<C*>(p.W) + (size_t)I.slot * p.slot_elems + I.woff;
-    if (I.type == 0) {
+    if (I.type == 0 && G::GC == G::LPC && I.pad0 >= 0) {   // paired images (planner: pad0 = second image)
+      const int c0 = P.c_lo + I.group * G::GC;
+      const int rem = P.c_lo + P.ncols - c0;
+      const C* F0 = static_cast<const C*>(p.F) + (size_t)I.b * (H + 1) * N;
+      const C* F1 = static_cast<const C*>(p.F) + (size_t)I.pad0 * (H + 1) * N;
+      C* w1 = static_cast<C*>(p.W) + (size_t)I.pad1 * p.slot_elems + I.first;
+      col_ifft_two(p, P, c0, rem < G::GC ? rem : G::GC, F0, F1, w, w1, P.ncols_pad, c0 - P.c_lo, smem,
+                   I.wait_ctr >= 0 ? p.ctr + I.wait_ctr : nullptr, I.wait_tgt,
+                   I.wait2_ctr >= 0 ? p.ctr + I.wait2_ctr : nullptr, I.np);
+    } else if (I.type == 0) {
       const int c0 = P.c_lo + I.group * G::GC;
       const int rem = P.c_lo + P.ncols - c0;
       const C* Fb = static_cast<const C*>(p.F) + (size_t)I.b * (H + 1) * N;
