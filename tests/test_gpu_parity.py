@@ -135,6 +135,28 @@ def test_batch_subset_and_determinism(F):
     assert torch.equal(r1, r2)
 
 
+@pytest.mark.parametrize("path", ["cta", "warp"])
+def test_determinism_config2(F, path, monkeypatch):
+    # at the bench's launch configuration (paired forward items, accumulator lanes, the side stream
+    # of the Nyquist correction): bitwise reproducible, and each image's result independent of the
+    # batch it is computed in (same arithmetic, same summation order)
+    monkeypatch.setenv("FFST_PATH", path)
+    cfg = synth.config(2)
+    x, _ = images(2, cfg.batch, cfg.n, torch.float32)
+    xd = x.cuda()
+    plan = F.Plan(cfg.n, cfg.batch, torch.float32)
+    c1 = plan.forward(xd).clone()
+    c2 = plan.forward(xd)
+    assert torch.equal(c1, c2)
+    r1 = plan.inverse(c1).clone()
+    r2 = plan.inverse(c1)
+    assert torch.equal(r1, r2)
+    c_sub = plan.forward(xd[5:8])
+    assert torch.equal(c1[5:8], c_sub)
+    r_sub = plan.inverse(c1[5:8].contiguous())
+    assert torch.equal(r1[5:8], r_sub)
+
+
 def test_shards_sum_to_full(F):
     # eta-sharding: each shard's cube holds its planes; partial images sum to the full inverse
     n, batch, shards = 64, 2, 3
