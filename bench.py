@@ -379,6 +379,34 @@ def run_gpu(args, cfg):
         e2e = {"value": B * args.steps / (e_ms / 1000.0), "unit": "images/s",
                "h2d_bytes_per_step": B * N * N * rsz, "d2h_bytes_per_step": B * N * N * rsz}
 
+    # compact coefficient format: real parts + Nyquist vectors, half the cube bytes
+    compact = None
+    if world == 1:
+        try:
+            re_c, gh_c = plan.forward_compact(x)
+            for _ in range(2):
+                plan.forward_compact(x, out=re_c, gh=gh_c)
+                plan.inverse_compact(re_c, gh_c, out=rec)
+            torch.cuda.synchronize(dev)
+            e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+            c_ms = 0.0
+            for _ in range(args.steps):
+                flush.zero_()
+                e0.record(stream)
+                plan.forward_compact(x, out=re_c, gh=gh_c)
+                plan.inverse_compact(re_c, gh_c, out=rec)
+                e1.record(stream)
+                torch.cuda.synchronize(dev)
+                c_ms += e0.elapsed_time(e1)
+            c_rt = float((rec - x).abs().max() / x.abs().max())
+            compact = {"value": B * args.steps / (c_ms / 1000.0), "unit": "images/s",
+                       "ms_per_step": c_ms / args.steps, "roundtrip_max_rel_err": c_rt,
+                       "what": "same step with the lossless compact cube (real parts + Nyquist vectors, "
+                               "half the bytes), include/ffst.h"}
+            del re_c, gh_c
+        except Exception as exc:
+            compact = {"unavailable": f"{type(exc).__name__}: {str(exc)[:120]}"}
+
     cufft = None
     if world == 1 and not args.no_cufft:
         try:
@@ -415,6 +443,7 @@ def run_gpu(args, cfg):
                                        "fwd_total": float(np.mean(fwd_tot)), "inv_total": float(np.mean(inv_tot))}},
             "cpu_baseline": cpu,
             "cufft_line": cufft,
+            "compact_line": compact,
             "clocks": clocks,
             "e2e": e2e,
             "gpu_launches": (launches[0] + launches[1]) * args.steps,

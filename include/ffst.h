@@ -154,6 +154,22 @@ ffst_status ffst_inversesheartrans_host(ffst_plan* plan, const void* coeff, void
 
 /* ---- instrumentation ----------------------------------------------------- */
 
+/* ---- compact coefficient format ---------------------------
+ * For even n the forward's complex cube is c_i = x_i + i y_i with x_i real and y_i of rank <= 2,
+ * y_i(r, m1) = (-1)^r G_i(m1) + (-1)^m1 H_i(r), non-zero only for the plan's Nyquist planes
+ * (DESIGN.md 6.2).  The compact format stores x as [batch][eta_local][n][n] reals and (G_i, H_i)
+ * as nyq_gh [batch][n_nyq][2][n] reals (Nyquist planes in the order of
+ * ffst_plan_nyquist_planes): half the bytes of the complex cube, lossless for every cube the
+ * forward produces (an arbitrary complex cube, e.g. after thresholding, is not representable:
+ * use the complex entry points).  Same validation, streams and errors as the complex calls;
+ * UNSUPPORTED with FFST_PATH=warp. */
+ffst_status ffst_sheartrans_compact(ffst_plan* plan, const void* img, void* coeff_re, void* nyq_gh, int batch,
+                                    void* stream);
+ffst_status ffst_inversesheartrans_compact(ffst_plan* plan, const void* coeff_re, const void* nyq_gh, void* img_out,
+                                           int batch, void* stream);
+/* The local Nyquist planes: count and (if local_indices != NULL) their local plane indices. */
+ffst_status ffst_plan_nyquist_planes(const ffst_plan* plan, int* count, int* local_indices);
+
 /* enable != 0: record CUDA events around each internal kernel phase (on the
  * call's stream).  ffst_plan_phase_times returns the durations (ms) of the last
  * call of each direction: times[0] = forward main kernel, [1] = inverse main

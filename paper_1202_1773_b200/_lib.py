@@ -64,6 +64,9 @@ _SIGS = {
     "ffst_inversesheartrans_batch": (_i, [_vp, _vp, _vp, _i, _vp]),
     "ffst_sheartrans_host": (_i, [_vp, _vp, _vp, _i, _vp]),
     "ffst_inversesheartrans_host": (_i, [_vp, _vp, _vp, _i, _vp]),
+    "ffst_sheartrans_compact": (_i, [_vp, _vp, _vp, _vp, _i, _vp]),
+    "ffst_inversesheartrans_compact": (_i, [_vp, _vp, _vp, _vp, _i, _vp]),
+    "ffst_plan_nyquist_planes": (_i, [_vp, _p, _p]),
     "ffst_plan_set_timing": (_i, [_vp, _i]),
     "ffst_plan_phase_times": (_i, [_vp, C.POINTER(C.c_float), _p]),
     "ffst_plan_set_trace": (_i, [_vp, _i]),

@@ -612,8 +612,11 @@ ffst_status trace_buffer(ffst_plan* p, int which, int n_items, KParams* k) {
   return FFST_OK;
 }
 
-ffst_status forward_impl(ffst_plan* p, const void* img, void* coeff, int batch, cudaStream_t s) {
+// nyq_gh != nullptr: compact (f1) format -- coeff holds the real parts, nyq_gh the Nyquist vectors
+ffst_status forward_impl(ffst_plan* p, const void* img, void* coeff, int batch, cudaStream_t s,
+                         void* nyq_gh = nullptr) {
   if (!img || !coeff) return fail(FFST_ERR_INVALID_ARG, "null buffer");
+  if (nyq_gh != nullptr && p->warp) return fail(FFST_ERR_UNSUPPORTED, "compact format: CTA-item kernels only");
   if (batch < 1 || batch > p->d.batch) return fail(FFST_ERR_INVALID_ARG, "batch outside 1..plan batch");
   if (!aligned16(img) || !aligned16(coeff)) return fail(FFST_ERR_ALIGNMENT, "buffers must be 16-byte aligned");
   TRY(set_device(p));
@@ -623,6 +626,10 @@ ffst_status forward_impl(ffst_plan* p, const void* img, void* coeff, int batch, 
   k.batch = batch;
   k.img = img;
   k.coeff = coeff;
+  if (nyq_gh != nullptr) {
+    k.compact = 1;
+    k.nyq_fwd = nyq_gh;          // nyq_fwd writes G, H straight into the caller's buffer
+  }
   k.units = q->d_units;
   k.chunks = q->d_chunks;
   k.items = q->d_fwd;
@@ -655,8 +662,10 @@ ffst_status forward_impl(ffst_plan* p, const void* img, void* coeff, int batch, 
   return FFST_OK;
 }
 
-ffst_status inverse_impl(ffst_plan* p, const void* coeff, void* img_out, int batch, cudaStream_t s) {
+ffst_status inverse_impl(ffst_plan* p, const void* coeff, void* img_out, int batch, cudaStream_t s,
+                         const void* nyq_gh = nullptr) {
   if (!img_out || !coeff) return fail(FFST_ERR_INVALID_ARG, "null buffer");
+  if (nyq_gh != nullptr && p->warp) return fail(FFST_ERR_UNSUPPORTED, "compact format: CTA-item kernels only");
   if (batch < 1 || batch > p->d.batch) return fail(FFST_ERR_INVALID_ARG, "batch outside 1..plan batch");
   if (!aligned16(img_out) || !aligned16(coeff)) return fail(FFST_ERR_ALIGNMENT, "buffers must be 16-byte aligned");
   TRY(set_device(p));
@@ -666,6 +675,11 @@ ffst_status inverse_impl(ffst_plan* p, const void* coeff, void* img_out, int bat
   k.batch = batch;
   k.coeff = const_cast<void*>(coeff);
   k.img_out = img_out;
+  if (nyq_gh != nullptr) {
+    k.compact = 1;
+    k.nyq_fwd = const_cast<void*>(nyq_gh);
+    k.n_rowitems = 1;            // the alternating sums come whole from (G, H)
+  }
   k.units = q->d_units;
   k.chunks = q->d_chunks + q->n_chunks;
   k.items = q->d_inv;
@@ -691,6 +705,9 @@ ffst_status inverse_impl(ffst_plan* p, const void* coeff, void* img_out, int bat
     // fork: the Nyquist correction (needed only by the final row pass) beside the column pass
     API_CUDA(cudaEventRecord(p->fork[0], s), "event");
     API_CUDA(cudaStreamWaitEvent(p->aux, p->fork[0], 0), "stream wait");
+    if (k.compact)
+      API_CUDA(p->d.dtype == FFST_F32 ? launch_nyq_compact_sums<float>(k, batch, p->aux)
+                                      : launch_nyq_compact_sums<double>(k, batch, p->aux), "nyq_compact_sums kernel");
     API_CUDA(L_nyq_inv(p, k, batch, p->aux), "nyq_inv kernels");
     API_CUDA(cudaEventRecord(p->fork[1], p->aux), "event");
     nl += 2;
@@ -1044,6 +1061,28 @@ ffst_status ffst_inversesheartrans_host(ffst_plan* p, const void* coeff, void* i
   TRY(inverse_impl(p, coeff, p->stage, batch, s));
   const size_t bytes = (size_t)batch * p->n * p->n * p->rsz;
   API_CUDA(cudaMemcpyAsync(img_host, p->stage, bytes, cudaMemcpyDeviceToHost, s), "D2H image copy");
+  return FFST_OK;
+}
+
+ffst_status ffst_sheartrans_compact(ffst_plan* p, const void* img, void* coeff_re, void* nyq_gh, int batch,
+                                    void* stream) {
+  if (!p || !nyq_gh) return fail(FFST_ERR_INVALID_ARG, "null argument");
+  if (!aligned16(nyq_gh)) return fail(FFST_ERR_ALIGNMENT, "buffers must be 16-byte aligned");
+  return forward_impl(p, img, coeff_re, batch, static_cast<cudaStream_t>(stream), nyq_gh);
+}
+
+ffst_status ffst_inversesheartrans_compact(ffst_plan* p, const void* coeff_re, const void* nyq_gh, void* img,
+                                           int batch, void* stream) {
+  if (!p || !nyq_gh) return fail(FFST_ERR_INVALID_ARG, "null argument");
+  if (!aligned16(nyq_gh)) return fail(FFST_ERR_ALIGNMENT, "buffers must be 16-byte aligned");
+  return inverse_impl(p, coeff_re, img, batch, static_cast<cudaStream_t>(stream), nyq_gh);
+}
+
+ffst_status ffst_plan_nyquist_planes(const ffst_plan* p, int* count, int* local_indices) {
+  if (!p || !count) return fail(FFST_ERR_INVALID_ARG, "null argument");
+  *count = (int)p->nyq.size();
+  if (local_indices)
+    for (size_t i = 0; i < p->nyq.size(); ++i) local_indices[i] = p->nyq[i];
   return FFST_OK;
 }
 

@@ -76,6 +76,7 @@ struct KParams {
   int* ctr;                     // [0] dispatch; [ctr_p1 + c]; [ctr_p2 + c]; [ctr_g + item]
   int ctr_p1, ctr_p2, ctr_g;
   int fetch_batch;              // warp path: consecutive items a CTA takes per global fetch
+  int compact;                  // f1 compact format: cube of reals + Nyquist vectors (G, H) in nyq_fwd
   int dbg;                      // measurement only (FFST_DBG): bit 0 skip FFTs, bit 1 skip output stores
   unsigned long long* trace;    // optional: per item {smid, t_start, t_ready, t_end} (globaltimer ns)
 };
@@ -104,6 +105,7 @@ template <typename T> cudaError_t launch_inv_warp(const KParams& p, int grid, cu
 template <typename T> cudaError_t launch_fwd_main(const KParams& p, int grid, cudaStream_t s);
 template <typename T> cudaError_t launch_inv_main(const KParams& p, int grid, cudaStream_t s);
 template <typename T> cudaError_t launch_nyq_inv(const KParams& p, int batch, cudaStream_t s);
+template <typename T> cudaError_t launch_nyq_compact_sums(const KParams& p, int batch, cudaStream_t s);
 template <typename T> cudaError_t launch_final(const KParams& p, int batch, int which, cudaStream_t s);
 template <typename T> cudaError_t launch_spectra_export(const KParams& p, void* psi, int centred, cudaStream_t s);
 template <typename T> int max_active_main(int n, int device, int which);   // CTAs/SM of fwd (0) / inv (1)

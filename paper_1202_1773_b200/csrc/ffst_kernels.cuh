@@ -69,7 +69,7 @@ struct Geo {
   static_assert(GC % LPC == 0 || LPC > GC, "GC vs LPC");
 };
 
-enum { MODE_MAIN = 0, MODE_AUX = 1 };
+enum { MODE_MAIN = 0, MODE_AUX = 1, MODE_COMPACT = 2 };   // COMPACT: forward rows as reals (f1 format)
 
 template <typename T> __device__ __forceinline__ void store_pair_cs(cpx<T>* dst, cpx<T> a, cpx<T> b);
 template <> __device__ __forceinline__ void store_pair_cs<float>(float2* dst, float2 a, float2 b) {
@@ -356,6 +356,8 @@ struct K {
               i1 = sr * sG[m1 + 1] - hr;
             }
             store_pair_cs<T>(out_c + (size_t)r * N + m1, mk<T>(x0, i0), mk<T>(x1, i1));
+          } else if constexpr (MODE == MODE_COMPACT) {   // real part only; the Nyquist term is (G, H)
+            __stcs(reinterpret_cast<cpx<T>*>(out_r + (size_t)r * N + m1), mk<T>(x0, x1));
           } else {
             T c0 = T(0), c1 = T(0);
             if (nyqG != nullptr) {
@@ -575,6 +577,8 @@ struct K {
   // Xa[k] = (Z[k] + conj Z[N-k])/2, Xb[k] = (Z[k] - conj Z[N-k])/(2i) for the plane's bins -> tile
   // -> W (column-major), plus the alternating sums of Im c for Nyquist planes.  Same results as
   // row_r2c<MODE_MAIN>.
+  // REAL: the rows are reals (compact format, f1): src_c is read as T rows, no Nyquist sums.
+  template <bool REAL = false>
   static __device__ void row_r2c_pair(const KParams& p, const C* __restrict__ src_c, int c_lo, int ncols, int r0,
                                       int cnt, C* dst, int nyq_b, int nyq_idx, int nyq_group, C* smem,
                                       const int* dep = nullptr, int dep_target = 0) {
@@ -583,7 +587,7 @@ struct K {
     T* red = reinterpret_cast<T*>(tile + G::TILE_R);        // NT/32 scalars past the tile
     const int tid = threadIdx.x, line = tid / G::THC, t = tid % G::THC;
     const C* tw = static_cast<const C*>(p.tw);
-    const bool nyq = nyq_idx >= 0;
+    const bool nyq = !REAL && nyq_idx >= 0;
     constexpr int RPR = 2 * G::LPC;
     T sacc[G::EC];
 #pragma unroll
@@ -604,9 +608,17 @@ struct K {
         T ta = T(0), tb = T(0);
         const T sa = (ra & 1) ? T(-1) : T(1);
         // float32: every load of the round in flight before any use (float64: registers too scarce)
-        constexpr int PH = sizeof(T) == 4 ? G::EC : 1;
+        constexpr int PH = (REAL || sizeof(T) == 4) ? G::EC : 1;
         C va_[PH], vb_[PH];
-        if constexpr (PH > 1) {
+        if constexpr (REAL) {          // compact rows: reals, row ra at src + ra N (T units)
+          const T* ra_ = reinterpret_cast<const T*>(src_c) + (size_t)ra * N;
+#pragma unroll
+          for (int q = 0; q < G::EC; ++q) {
+            const int m = t + q * G::THC;
+            va_[q] = mk<T>(act ? __ldcs(ra_ + m) : T(0), T(0));
+            vb_[q] = mk<T>(act ? __ldcs(ra_ + N + m) : T(0), T(0));
+          }
+        } else if constexpr (PH > 1) {
 #pragma unroll
           for (int q = 0; q < G::EC; ++q) {
             const int m = t + q * G::THC;
@@ -618,7 +630,7 @@ struct K {
         for (int q = 0; q < G::EC; ++q) {
           const int m = t + q * G::THC;
           C va, vb;
-          if constexpr (PH > 1) {
+          if constexpr (REAL || PH > 1) {
             va = va_[q];
             vb = vb_[q];
           } else {
@@ -807,6 +819,11 @@ struct K {
         nyqG = static_cast<const T*>(p.nyq_fwd) + ((size_t)I.b * p.n_nyq + P.nyq) * 2 * N;
         nyqH = nyqG + N;
       }
+      if (p.compact) {   // f1 format: real rows; the Nyquist term stays as (G, H) vectors
+        T* outr = static_cast<T*>(p.coeff) + ((size_t)I.b * p.eta_l + I.p) * N * N;
+        row_c2r<MODE_COMPACT>(p, w, P.ncols_pad, P.c_lo, P.ncols, r0, cnt, nullptr, outr, nullptr, nullptr, smem);
+        return;
+      }
       C* out = static_cast<C*>(p.coeff) + ((size_t)I.b * p.eta_l + I.p) * N * N;
       if constexpr (G::PAIR_FWD) row_c2r_pair(p, w, P.ncols_pad, P.c_lo, P.ncols, r0, cnt, out, nyqG, nyqH, smem);
       else row_c2r<MODE_MAIN>(p, w, P.ncols_pad, P.c_lo, P.ncols, r0, cnt, out, nullptr, nyqG, nyqH, smem);
@@ -819,6 +836,16 @@ struct K {
       C* w = static_cast<C*>(p.W) + (size_t)I.slot * p.slot_elems + I.woff;
       const int r0 = I.group * G::RPI;
       const int cnt = N - r0 < G::RPI ? N - r0 : G::RPI;
+      if (p.compact) {   // f1 format: real rows; the Nyquist sums come from (G, H) (nyq_compact_sums)
+        const T* srcr = static_cast<const T*>(p.coeff) + ((size_t)I.b * p.eta_l + I.p) * N * N;
+        if constexpr (G::PAIR_INV)
+          row_r2c_pair<true>(p, reinterpret_cast<const C*>(srcr), P.c_lo, P.ncols, r0, cnt, w, I.b, -1, I.group, smem,
+                             I.wait_ctr >= 0 ? p.ctr + I.wait_ctr : nullptr, I.wait_tgt);
+        else
+          row_r2c<MODE_AUX>(p, nullptr, srcr, P.c_lo, P.ncols, r0, cnt, w, I.b, -1, I.group, smem,
+                            I.wait_ctr >= 0 ? p.ctr + I.wait_ctr : nullptr, I.wait_tgt);
+        return;
+      }
       const C* src = static_cast<const C*>(p.coeff) + ((size_t)I.b * p.eta_l + I.p) * N * N;
       if constexpr (G::PAIR_INV)
         row_r2c_pair(p, src, P.c_lo, P.ncols, r0, cnt, w, I.b, P.nyq, I.group, smem,
@@ -1112,6 +1139,43 @@ __global__ void __launch_bounds__(256) nyq_fin_kernel(KParams p, int groups) {
   const T s = T(1) / (T(N) * T(N));
 #pragma unroll
   for (int q = 0; q < G::EC; ++q) out[t + q * G::THC] = acc[q].y * s;
+}
+
+// Compact format (f1), inverse: the alternating sums of Im c from the forward's Nyquist vectors,
+// Im c(r, m1) = (-1)^r G(m1) + (-1)^m1 H(r)  =>
+//   s(m1) = sum_r (-1)^r Im c(r, m1) = n G(m1) + (-1)^m1 sum_r (-1)^r H(r)   -> nyq_S (one partial)
+//   t(r)  = sum_m1 (-1)^m1 Im c(r, m1) = (-1)^r sum_m1 (-1)^m1 G(m1) + n H(r) -> nyq_T
+// grid (n_nyq, B), 256 threads; fixed-order reductions (deterministic).
+template <typename T, int N>
+__global__ void __launch_bounds__(256) nyq_compact_sums_kernel(KParams p) {
+  __shared__ T red[2][256];
+  const int nq = blockIdx.x, b = blockIdx.y, tid = threadIdx.x;
+  const T* g = static_cast<const T*>(p.nyq_fwd) + ((size_t)b * p.n_nyq + nq) * 2 * N;
+  const T* h = g + N;
+  T sg = T(0), sh = T(0);
+  for (int m = tid; m < N; m += 256) {
+    const T sgn = (m & 1) ? T(-1) : T(1);
+    sg += sgn * g[m];
+    sh += sgn * h[m];
+  }
+  red[0][tid] = sg;
+  red[1][tid] = sh;
+  __syncthreads();
+  for (int o = 128; o > 0; o >>= 1) {
+    if (tid < o) {
+      red[0][tid] += red[0][tid + o];
+      red[1][tid] += red[1][tid + o];
+    }
+    __syncthreads();
+  }
+  const T SG = red[0][0], SH = red[1][0];
+  T* s = static_cast<T*>(p.nyq_S) + ((size_t)b * p.n_nyq + nq) * N;       // n_rowitems = 1
+  T* tt = static_cast<T*>(p.nyq_T) + ((size_t)b * p.n_nyq + nq) * N;
+  for (int m = tid; m < N; m += 256) {
+    const T sgn = (m & 1) ? T(-1) : T(1);
+    s[m] = T(N) * g[m] + sgn * SH;
+    tt[m] = sgn * SG + T(N) * h[m];
+  }
 }
 
 // materialise spectra (tests only): psi[i][row][col], grid-stride

@@ -98,6 +98,10 @@ template <typename T, int N> struct Launch {
   }
   // final pass, split so the Nyquist correction can run beside the column pass (it is only
   // needed by the row pass): which = 0 column pass, 1 row pass
+  static cudaError_t nyq_compact_sums(const KParams& p, int batch, cudaStream_t s) {
+    nyq_compact_sums_kernel<T, N><<<dim3(p.n_nyq, batch), 256, 0, s>>>(p);
+    return cudaGetLastError();
+  }
   static cudaError_t final_(const KParams& p, int batch, int which, cudaStream_t s) {
     if (which == 0) {
       FFST_CHECK(set_smem(fin_cols_kernel<T, N>, G::SMEM_FWD));
@@ -161,6 +165,8 @@ template <typename T, int N> struct Launch {
     FFST_DISPATCH(T, p.n, fwd_main(p, g, s), cudaErrorInvalidValue) }                                          \
   template <> cudaError_t launch_inv_main<T>(const KParams& p, int g, cudaStream_t s) {                        \
     FFST_DISPATCH(T, p.n, inv_main(p, g, s), cudaErrorInvalidValue) }                                          \
+  template <> cudaError_t launch_nyq_compact_sums<T>(const KParams& p, int b, cudaStream_t s) {                \
+    FFST_DISPATCH(T, p.n, nyq_compact_sums(p, b, s), cudaErrorInvalidValue) }                                  \
   template <> cudaError_t launch_nyq_inv<T>(const KParams& p, int b, cudaStream_t s) {                         \
     FFST_DISPATCH(T, p.n, nyq_inv(p, b, s), cudaErrorInvalidValue) }                                           \
   template <> cudaError_t launch_final<T>(const KParams& p, int b, int which, cudaStream_t s) {                \

@@ -159,6 +159,51 @@ class Plan:
                                               _stream_handle(stream, self.device)), "ffst_inversesheartrans_host")
         return out_host
 
+    # -------------------------------------------------------------- compact format (f1)
+    def nyquist_planes(self):
+        """Local indices of the plan's Nyquist planes (the order of the compact format's G, H)."""
+        cnt = C.c_int()
+        check(lib.ffst_plan_nyquist_planes(self._h, C.byref(cnt), None), "ffst_plan_nyquist_planes")
+        idx = (C.c_int * max(1, cnt.value))()
+        check(lib.ffst_plan_nyquist_planes(self._h, C.byref(cnt), idx), "ffst_plan_nyquist_planes")
+        return [idx[i] for i in range(cnt.value)]
+
+    def forward_compact(self, x, out=None, gh=None, stream=None):
+        """Forward in the compact format: (real parts (B, eta_local, n, n), Nyquist vectors
+        gh (B, n_nyq, 2, n)) -- half the bytes of the complex cube, lossless for the forward's
+        output (include/ffst.h "compact coefficient format")."""
+        x = self._check_images(x)
+        b = x.shape[0]
+        nn = max(1, len(self.nyquist_planes()))
+        out = torch.empty((b, self.eta_local, self.n, self.n), dtype=self.dtype, device=self.device) if out is None else out
+        gh = torch.zeros((b, nn, 2, self.n), dtype=self.dtype, device=self.device) if gh is None else gh
+        check(lib.ffst_sheartrans_compact(self._h, C.c_void_p(x.data_ptr()), C.c_void_p(out.data_ptr()),
+                                          C.c_void_p(gh.data_ptr()), b, _stream_handle(stream, self.device)),
+              "ffst_sheartrans_compact")
+        return out, gh
+
+    def inverse_compact(self, re, gh, out=None, stream=None):
+        """Inverse from the compact format (see forward_compact)."""
+        re = re.contiguous()
+        gh = gh.contiguous()
+        b = re.shape[0]
+        out = self.empty_images(b) if out is None else out
+        check(lib.ffst_inversesheartrans_compact(self._h, C.c_void_p(re.data_ptr()), C.c_void_p(gh.data_ptr()),
+                                                 C.c_void_p(out.data_ptr()), b, _stream_handle(stream, self.device)),
+              "ffst_inversesheartrans_compact")
+        return out
+
+    def expand_compact(self, re, gh):
+        """The complex cube of a compact one: Im c_i(r, m1) = (-1)^r G_i(m1) + (-1)^m1 H_i(r) on the
+        Nyquist planes, 0 elsewhere (a format conversion with torch ops; not on the transform path)."""
+        c = torch.complex(re, torch.zeros_like(re))
+        sgn = 1.0 - 2.0 * (torch.arange(self.n, device=re.device) % 2).to(re.dtype)
+        for q, pl in enumerate(self.nyquist_planes()):
+            g, h = gh[:, q, 0], gh[:, q, 1]
+            im = sgn[None, :, None] * g[:, None, :] + sgn[None, None, :] * h[:, :, None]
+            c[:, pl] = torch.complex(re[:, pl], im)
+        return c
+
     def spectra(self, centred: bool = True, stream=None):
         """The local spectra psi_hat_i as (eta_local, n, n) real (tests / diagnostics)."""
         psi = torch.empty((self.eta_local, self.n, self.n), dtype=self.dtype, device=self.device)

@@ -290,3 +290,37 @@ def test_config5_sampled(F):
         g = c[0, i].cpu().numpy()
         ref = O.forward_plane(x64, i + 1, f_hat=f_hat)
         assert plane_err(g, ref, np.max(np.abs(x64))) <= 1e-4, i
+
+
+# ------------------------------------------------------------------ compact format
+
+@pytest.mark.parametrize("n,dtype,batch", [(8, torch.float64, 2), (64, torch.float64, 3), (32, torch.float32, 3),
+                                           (256, torch.float32, 16), (512, torch.float32, 4)])
+def test_compact_format(F, n, dtype, batch):
+    # the compact cube (real parts + Nyquist vectors) expands to the complex forward's cube, its
+    # inverse equals the complex inverse of that cube, and the round trip is exact
+    x, xo = images(2, batch, n, dtype)
+    xd = x.cuda()
+    plan = F.Plan(n, batch, dtype)
+    c = plan.forward(xd)
+    re, gh = plan.forward_compact(xd)
+    ce = plan.expand_compact(re, gh)
+    scale = c.abs().amax(dim=(2, 3), keepdim=True).clamp_min(1e-30)
+    tol = 1e-5 if dtype == torch.float32 else 1e-12
+    assert float(((ce - c).abs() / scale).max()) <= tol
+    r_compact = plan.inverse_compact(re, gh)
+    r_complex = plan.inverse(ce)
+    assert float((r_compact - r_complex).abs().max() / r_complex.abs().max()) <= tol
+    assert plane_err(r_compact.cpu().numpy(), xo).max() <= TOL[dtype]
+    # against the oracle on one image
+    psi = O.shearlet_spectra(n)
+    ref = O.forward(xo[0], psi=psi)
+    assert plane_err(ce[0].cpu().numpy(), ref, np.max(np.abs(xo[0]))).max() <= TOL[dtype]
+
+
+def test_compact_warp_path_unsupported(F, monkeypatch):
+    monkeypatch.setenv("FFST_PATH", "warp")
+    plan = F.Plan(64, 1, torch.float32)
+    x = torch.zeros(1, 64, 64, device="cuda")
+    with pytest.raises(F.FFSTError):
+        plan.forward_compact(x)

@@ -370,3 +370,22 @@ def test_adjoint_identity(n):
     lhs = np.real(np.sum(O.forward(f) * np.conj(z)))
     rhs = np.sum(f * O.inverse(z).real)
     assert abs(lhs - rhs) < 1e-12 * max(1.0, abs(lhs))
+
+
+@pytest.mark.parametrize("n", [16, 32])
+def test_imaginary_part_rank_two(n):
+    # SURVEY 8(a) / DESIGN 6.2: for even n, Im c_i = (-1)^r G_i(m1) + (-1)^m1 H_i(r) (rank <= 2):
+    # the compact coefficient format (real part + two n-vectors per plane) is lossless for
+    # the forward's output.  Pinned here on the oracle's cube of a random image.
+    f = synth.uniform_image(n, seed=11)
+    c = O.forward(f)
+    m = np.arange(n)
+    sgn = (-1.0) ** m
+    for i in range(c.shape[0]):
+        y = c[i].imag
+        # G, H from row 0 / column 0 up to the gauge (G + a(-1)^m1, H - a(-1)^r)
+        g = y[0, :] - 0.0
+        h = (y[:, 0] - sgn * g[0]) * sgn[0]
+        rec = sgn[:, None] * g[None, :] + sgn[None, :] * h[:, None]
+        assert np.max(np.abs(rec - y)) <= 1e-12 * max(1.0, np.max(np.abs(c[i])))
+        assert np.linalg.matrix_rank(y, tol=1e-10 * max(1.0, np.max(np.abs(y)))) <= 2
