@@ -57,12 +57,16 @@ typedef enum {
   FFST_ERR_OOM = 6,            /* workspace allocation failed at plan creation */
   FFST_ERR_CUDA = 7,           /* CUDA runtime error (see ffst_last_error_detail) */
   FFST_ERR_NCCL = 8,           /* reserved */
-  FFST_ERR_UNSUPPORTED = 9     /* n not a power of two, or variant not built */
+  FFST_ERR_UNSUPPORTED = 9     /* n not a power of two, or more local planes than built */
 } ffst_status;
 
 typedef enum { FFST_F32 = 0, FFST_F64 = 1 } ffst_dtype;
 
-/* FFST_CLASSIC: meyerShearletSpect, eq:Psi1/eq:Psi2. */
+/* FFST_CLASSIC: meyerShearletSpect, eq:Psi1/eq:Psi2.
+ * FFST_SMOOTH: meyerNewShearletSpect, the smooth system of Sec. smoothShearlets
+ * (P:L1766-1820): low-pass Phi(w) = varphi(w1) varphi(w2) (eq:Phi), cone shearlets
+ * Psi1(4^-j w) psi2(2^j w_b/w_a + k) with Psi1 = sqrt(Phi^2(w/4) - Phi^2(w)) (eq:newPsi1,
+ * eq:smoothPsi), same cones, seams and index order; isotropic dilation (reading A18). */
 typedef enum { FFST_CLASSIC = 0, FFST_SMOOTH = 1 } ffst_variant;
 
 /* Shearlet kinds of the flat index (Sec. 3.5.1): low-pass, horizontal cone,
@@ -101,8 +105,9 @@ ffst_status ffst_params_to_index(int j0, int kind, int j, int k, int* index);
  * (used for pruning the first FFT pass; a superset of the true support). */
 ffst_status ffst_plane_support(int n, int j0, int index, int* col_lo, int* col_hi);
 
-/* 1 if plane `index` is not point-symmetric on the even grid (non-zero
- * anti-symmetric part on the Nyquist row/column), else 0. */
+/* 1 if plane `index` of the CLASSIC system is not point-symmetric on the even grid (non-zero
+ * anti-symmetric part on the Nyquist row/column), else 0.  A plan's own list, for either
+ * variant: ffst_plan_nyquist_planes. */
 ffst_status ffst_plane_is_nyquist(int n, int j0, int index, int* is_nyquist);
 
 /* ---- plans ------------------------------------------------------------- */
@@ -110,7 +115,8 @@ ffst_status ffst_plane_is_nyquist(int n, int j0, int index, int* is_nyquist);
 /* Create a plan: all tables (index order, pruning ranges, radial factors, Nyquist anti-window
  * edges, work queues) and all device workspace are built here; transforms allocate nothing.
  * Errors: INVALID_SIZE (n < 4 or above the built sizes), UNSUPPORTED (n not a power of two,
- * variant != CLASSIC, more than 256 local planes), INVALID_ARG, OOM, CUDA.
+ * more than 256 local planes), INVALID_ARG (incl. an unknown variant), OOM, CUDA.
+ * FFST_SMOOTH plans always run the CTA-item kernels (FFST_PATH=warp is ignored for them).
  * Environment (read here, tuning only; results are identical up to rounding order):
  *   FFST_PATH=warp      warp-worker kernels for 8 <= n <= 512 (default: CTA-item kernels)
  *   FFST_RING_MB        intermediate ring budget (default 80; at least 12 slots)

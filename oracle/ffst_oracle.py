@@ -37,7 +37,7 @@ __all__ = [
     "scaling_varphi", "scales_for_size", "num_shearlets", "index_to_params",
     "params_to_index", "frequency_grid", "shearlet_spectrum", "shearlet_spectra",
     "dft2_centred", "idft2_centred", "dft2_direct", "idft2_direct",
-    "forward", "forward_plane", "inverse", "KIND_S", "KIND_H", "KIND_V", "KIND_X",
+    "forward", "forward_plane", "inverse", "tensor_scaling_Phi", "smooth_psi1", "KIND_S", "KIND_H", "KIND_V", "KIND_X",
 ]
 
 KIND_S, KIND_H, KIND_V, KIND_X = 0, 1, 2, 3   # low-pass, horizontal, vertical, seam ("h x v")
@@ -95,6 +95,19 @@ def scaling_varphi(omega):
     a = np.abs(np.asarray(omega, dtype=np.float64))
     return np.where(a <= 0.5, 1.0,
                     np.where(a < 1.0, np.cos(np.pi / 2.0 * meyer_aux(2.0 * a - 1.0)), 0.0))
+
+
+def tensor_scaling_Phi(omega1, omega2):
+    """Tensor-product scaling function, eq:Phi: Phi(w) = varphi(w1) varphi(w2).
+    The low-pass of the smooth construction (Sec. smoothShearlets)."""
+    return scaling_varphi(omega1) * scaling_varphi(omega2)
+
+
+def smooth_psi1(omega1, omega2):
+    """eq:newPsi1: Psi1(w) = sqrt(Phi^2(w/4) - Phi^2(w)), written out as printed
+    (clipped at 0 against rounding).  Supported in [-4,4]^2 minus [-1/2,1/2]^2."""
+    d = tensor_scaling_Phi(omega1 / 4.0, omega2 / 4.0) ** 2 - tensor_scaling_Phi(omega1, omega2) ** 2
+    return np.sqrt(np.maximum(d, 0.0))
 
 
 # ---------------------------------------------------------------------------
@@ -179,10 +192,31 @@ def _cone_shearlet(omega_a, omega_b, j, k):
     return np.where(omega_a != 0.0, value, 0.0)
 
 
-def _spectrum_on_grid(w1, w2, kind, j, k):
+def _smooth_cone_shearlet(omega_a, omega_b, j, k):
+    """Smooth shearlet eq:smoothPsi at scale j, shear k:
+    Psi1(4^-j w_a, 4^-j w_b) psi2_hat(2^j w_b/w_a + k) -- the corona function dilated
+    isotropically so that sum_j Psi1^2(4^-j w) telescopes (P:L1795-1806) [reading A18];
+    0 where w_a = 0 [reading A5]."""
+    with np.errstate(divide="ignore", invalid="ignore"):
+        ratio = np.where(omega_a != 0.0, omega_b / np.where(omega_a != 0.0, omega_a, 1.0), 0.0)
+        value = smooth_psi1(4.0 ** (-j) * omega_a, 4.0 ** (-j) * omega_b) * psi2_hat(2.0 ** j * ratio + k)
+    return np.where(omega_a != 0.0, value, 0.0)
+
+
+def _spectrum_on_grid(w1, w2, kind, j, k, variant="classic"):
     """One spectrum psi_hat_{j,k,0}^kappa on the meshgrid (w1 = omega_1 columns,
-    w2 = omega_2 rows), eq:shearletTransform's four cases."""
+    w2 = omega_2 rows), eq:shearletTransform's four cases.  variant "smooth":
+    the construction of Sec. smoothShearlets: low-pass Phi (eq:Phi), cone
+    shearlets from Psi1 (eq:newPsi1, eq:smoothPsi); cones and seam gluing unchanged."""
     a1, a2 = np.abs(w1), np.abs(w2)
+    if variant == "smooth":
+        if kind == KIND_S:
+            return tensor_scaling_Phi(w1, w2)
+        cone = _smooth_cone_shearlet
+    elif variant == "classic":
+        cone = _cone_shearlet
+    else:
+        raise ValueError(f"unknown variant {variant}")
     if kind == KIND_S:
         # eq:phi (P:L705-711): varphi(w1) on |w1|<1, |w2|<=|w1|; varphi(w2) on |w2|<1, |w1|<|w2|
         return np.where((a1 < 1.0) & (a2 <= a1), scaling_varphi(w1),
@@ -191,17 +225,17 @@ def _spectrum_on_grid(w1, w2, kind, j, k):
     chi_v = (a2 >= 0.5) & (a2 > a1)                    # C^v
     chi_x = (a1 >= 0.5) & (a2 >= 0.5) & (a1 == a2)     # C^x, the seam [reading A6]
     if kind == KIND_H:                                 # eq:horizontalShearlet
-        return _cone_shearlet(w1, w2, j, k) * chi_h
+        return cone(w1, w2, j, k) * chi_h
     if kind == KIND_V:                                 # eq:verticalShearlet
-        return _cone_shearlet(w2, w1, j, k) * chi_v
+        return cone(w2, w1, j, k) * chi_v
     if kind == KIND_X:                                 # glued h + v + x, |k| = 2^j
-        horizontal = _cone_shearlet(w1, w2, j, k)
-        return (horizontal * chi_h + _cone_shearlet(w2, w1, j, k) * chi_v
+        horizontal = cone(w1, w2, j, k)
+        return (horizontal * chi_h + cone(w2, w1, j, k) * chi_v
                 + horizontal * chi_x)                  # seam uses the horizontal formula (eq:seamlineShearlet)
     raise ValueError(f"unknown kind {kind}")
 
 
-def shearlet_spectrum(n: int, i: int, j0: int | None = None):
+def shearlet_spectrum(n: int, i: int, j0: int | None = None, variant: str = "classic"):
     """Spectrum of flat index i (1-based) on the N x N centred grid, float64.
 
     Evaluated on the odd lattice Xi of Sec. 3.5.2; for even N the last row and
@@ -212,15 +246,16 @@ def shearlet_spectrum(n: int, i: int, j0: int | None = None):
     axis, n_odd, _, _ = frequency_grid(n, j0)
     w1, w2 = np.meshgrid(axis, axis)          # w1 varies along columns, w2 along rows
     kind, j, k = index_to_params(j0, i)
-    spec = _spectrum_on_grid(w1, w2, kind, j, k)
+    spec = _spectrum_on_grid(w1, w2, kind, j, k, variant)
     return spec[:n, :n]
 
 
-def shearlet_spectra(n: int, j0: int | None = None):
-    """All eta spectra, shape (eta, N, N) ("Psi")."""
+def shearlet_spectra(n: int, j0: int | None = None, variant: str = "classic"):
+    """All eta spectra, shape (eta, N, N) ("Psi"); variant "classic"
+    (meyerShearletSpect) or "smooth" (meyerNewShearletSpect, P:L2209-2210)."""
     if j0 is None:
         j0 = scales_for_size(n)
-    return np.stack([shearlet_spectrum(n, i, j0) for i in range(1, num_shearlets(j0) + 1)])
+    return np.stack([shearlet_spectrum(n, i, j0, variant) for i in range(1, num_shearlets(j0) + 1)])
 
 
 # ---------------------------------------------------------------------------
@@ -262,30 +297,31 @@ def idft2_direct(g):
 # 3.1 / 3.3  Forward and inverse transform
 # ---------------------------------------------------------------------------
 
-def forward(f, psi=None, j0: int | None = None, direct: bool = False):
+def forward(f, psi=None, j0: int | None = None, direct: bool = False, variant: str = "classic"):
     """Discrete shearlet transform, eq:shearletTransform:
     SH(f)(i) = ifft2(psi_hat_i * f_hat), one complex N x N plane per index i
     [reading A8: coefficients are complex].  Returns shape (eta, N, N) complex."""
     f = np.asarray(f, dtype=np.float64)
     n = f.shape[-1]
     if psi is None:
-        psi = shearlet_spectra(n, j0)
+        psi = shearlet_spectra(n, j0, variant)
     dft, idft = (dft2_direct, idft2_direct) if direct else (dft2_centred, idft2_centred)
     f_hat = dft(f)
     return np.stack([idft(p * f_hat) for p in psi])
 
 
-def forward_plane(f, i: int, j0: int | None = None, f_hat=None):
+def forward_plane(f, i: int, j0: int | None = None, f_hat=None, variant: str = "classic"):
     """One plane of the forward transform (flat index i, 1-based), for sampled
     parity at sizes where the whole cube does not fit the host."""
     f = np.asarray(f, dtype=np.float64)
     n = f.shape[-1]
     if f_hat is None:
         f_hat = dft2_centred(f)
-    return idft2_centred(shearlet_spectrum(n, i, j0) * f_hat)
+    return idft2_centred(shearlet_spectrum(n, i, j0, variant) * f_hat)
 
 
-def inverse(coeffs, psi=None, j0: int | None = None, direct: bool = False, planes=None):
+def inverse(coeffs, psi=None, j0: int | None = None, direct: bool = False, planes=None,
+            variant: str = "classic"):
     """Inverse transform, eq:inverseShearletTransform:
     f_hat = sum_i fft2(c_i) * psi_hat_i;  f = ifft2(f_hat).
 
@@ -301,6 +337,6 @@ def inverse(coeffs, psi=None, j0: int | None = None, direct: bool = False, plane
     dft, idft = (dft2_direct, idft2_direct) if direct else (dft2_centred, idft2_centred)
     acc = np.zeros((n, n), dtype=np.complex128)
     for slot, i in enumerate(planes):
-        p = psi[i - 1] if psi is not None else shearlet_spectrum(n, i, j0)
+        p = psi[i - 1] if psi is not None else shearlet_spectrum(n, i, j0, variant)
         acc += dft(coeffs[slot]) * p
     return idft(acc)

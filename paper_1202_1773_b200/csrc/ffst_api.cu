@@ -136,6 +136,60 @@ std::vector<double> radial_table(int n, int j0) {
   return t;
 }
 
+// Smooth-variant rows appended to the radial table (Sec. smoothShearlets):
+// B_j(a) = varphi^2(4^-j Delta a), j = 0..j0+1, then D_j(a) = varphi^2(4^-(j+1) Delta a) -
+// varphi^2(4^-j Delta a), j = 0..j0, each written piecewise from eq:varphi so that
+// no difference of nearly equal numbers is formed: with x = 4^-j Delta a, D = 0 (x <= 1/2),
+// sin^2(pi/2 v(2x-1)) (1/2 < x < 1), 1 (1 <= x <= 2), cos^2(pi/2 v(x/2-1)) (2 < x < 4), 0 (x >= 4).
+std::vector<double> smooth_rows(int n, int j0) {
+  const int H = n / 2;
+  const double delta = grid_delta(n, j0);
+  const double pi = 3.14159265358979323846;
+  auto v = [](double x) {
+    if (x <= 0) return 0.0;
+    if (x >= 1) return 1.0;
+    const bool refl = x > 0.5;
+    const double y = refl ? 1 - x : x, y2 = y * y;
+    const double p = y2 * y2 * (35 + y * (-84 + y * (70 - 20 * y)));
+    return refl ? 1 - p : p;
+  };
+  auto phi2 = [&](double x) {
+    if (x <= 0.5) return 1.0;
+    if (x >= 1) return 0.0;
+    const double c = std::cos(pi / 2 * v(2 * x - 1));
+    return c * c;
+  };
+  auto dif = [&](double x) {
+    if (x <= 0.5 || x >= 4) return 0.0;
+    if (x < 1) { const double s = std::sin(pi / 2 * v(2 * x - 1)); return s * s; }
+    if (x <= 2) return 1.0;
+    const double c = std::cos(pi / 2 * v(x / 2 - 1));
+    return c * c;
+  };
+  std::vector<double> t((size_t)(2 * j0 + 3) * (H + 1));
+  for (int j = 0; j <= j0 + 1; ++j)
+    for (int a = 0; a <= H; ++a) t[(size_t)j * (H + 1) + a] = phi2(std::ldexp(delta * a, -2 * j));
+  for (int j = 0; j <= j0; ++j)
+    for (int a = 0; a <= H; ++a) t[(size_t)(j0 + 2 + j) * (H + 1) + a] = dif(std::ldexp(delta * a, -2 * j));
+  return t;
+}
+
+// The plan's whole radial table: classic rows, then the smooth rows when variant == FFST_SMOOTH.
+std::vector<double> radial_all(int n, int j0, int variant) {
+  std::vector<double> t = radial_table(n, j0);
+  if (variant == FFST_SMOOTH) {
+    const std::vector<double> s = smooth_rows(n, j0);
+    t.insert(t.end(), s.begin(), s.end());
+  }
+  return t;
+}
+
+Radial<double> host_radial(const std::vector<double>& tab, int n, int j0, int variant) {
+  Radial<double> R{tab.data(), n / 2 + 1, j0};
+  if (variant == FFST_SMOOTH) R.smooth = tab.data() + (size_t)(j0 + 1) * (n / 2 + 1);
+  return R;
+}
+
 // Column records of the warp path (ColRec, ffst_math.cuh): hulls of the rows where sym_i is
 // non-zero in each Hermitian-half column of the plane, found by evaluating the window (float64)
 // on the whole column, widened by one row; plus the horizontal radial factor and 1/|u1|.
@@ -166,12 +220,12 @@ void column_records(int n, int j0, PlaneDev& P, std::vector<ColRec<T>>& out) {
   }
 }
 
-bool plane_nyquist(int n, int j0, const Triple& tr) {
+bool plane_nyquist(int n, int j0, const Triple& tr, int variant) {
   PlaneDev P{};
   P.kind = tr.kind; P.j = tr.j; P.k = tr.k;
   const int H = n / 2;
-  const std::vector<double> tab = radial_table(n, j0);
-  const Radial<double> R{tab.data(), H + 1, j0};
+  const std::vector<double> tab = radial_all(n, j0, variant);
+  const Radial<double> R = host_radial(tab, n, j0, variant);
   for (int u = -H; u < H; ++u) {
     if (window_anti<double>(P, u, -H, H, R) != 0.0) return true;
     if (window_anti<double>(P, -H, u, H, R) != 0.0) return true;
@@ -555,6 +609,7 @@ KParams base_params(ffst_plan* p) {
   KParams k{};
   k.n = p->n; k.j0 = p->j0; k.batch = p->d.batch; k.eta_l = p->eta_l; k.n_nyq = (int)p->nyq.size();
   k.delta = p->delta;
+  k.variant = p->d.variant == FFST_SMOOTH ? 1 : 0;
   k.planes = p->d_planes;
   k.nyq_planes = p->d_nyq;
   k.tw = p->d_tw;
@@ -775,7 +830,7 @@ ffst_status ffst_plane_is_nyquist(int n, int j0, int index, int* is_nyquist) {
   if (j0 == 0) j0 = default_j0(n);
   if (j0 < 1 || j0 > 12) return fail(FFST_ERR_INVALID_ARG, "j0 outside 1..12");
   if (index < 0 || index >= ffst_num_shearlets(j0)) return fail(FFST_ERR_INDEX, "index outside 0..eta-1");
-  *is_nyquist = plane_nyquist(n, j0, index_table(j0)[index]) ? 1 : 0;
+  *is_nyquist = plane_nyquist(n, j0, index_table(j0)[index], FFST_CLASSIC) ? 1 : 0;
   return FFST_OK;
 }
 
@@ -803,7 +858,7 @@ ffst_status ffst_plan_create(ffst_plan** out, const ffst_plan_desc* d) {
   const int maxn = d->dtype == FFST_F32 ? 4096 : 2048;
   if (d->n > maxn) return fail(FFST_ERR_INVALID_SIZE, "n above the largest built size (4096 f32, 2048 f64)");
   if (!is_pow2(d->n)) return fail(FFST_ERR_UNSUPPORTED, "n must be a power of two in this build");
-  if (d->variant != FFST_CLASSIC) return fail(FFST_ERR_UNSUPPORTED, "only the classic variant is built");
+  if (d->variant != FFST_CLASSIC && d->variant != FFST_SMOOTH) return fail(FFST_ERR_INVALID_ARG, "unknown variant");
   if (d->batch < 1) return fail(FFST_ERR_INVALID_ARG, "batch < 1");
   if (d->shard_count < 1 || d->shard_rank < 0 || d->shard_rank >= d->shard_count)
     return fail(FFST_ERR_INVALID_ARG, "bad shard_rank / shard_count");
@@ -823,7 +878,8 @@ ffst_status ffst_plan_create(ffst_plan** out, const ffst_plan_desc* d) {
     // the full-ring lookahead.  FFST_PATH=warp selects the warp-worker kernels
     // (ffst_warp.cuh, 8 <= n <= 512), kept as a tested alternative scheme.
     const char* path = std::getenv("FFST_PATH");
-    p->warp = d->n >= 8 && d->n <= 512 && path && std::strcmp(path, "warp") == 0;
+    // (the warp path hoists a per-column radial factor: classic system only)
+    p->warp = d->n >= 8 && d->n <= 512 && d->variant == FFST_CLASSIC && path && std::strcmp(path, "warp") == 0;
   }
   if (p->warp) p->geo = d->dtype == FFST_F32 ? geometry_warp<float>(d->n) : geometry_warp<double>(d->n);
   else p->geo = d->dtype == FFST_F32 ? geometry<float>(d->n) : geometry<double>(d->n);
@@ -836,7 +892,7 @@ ffst_status ffst_plan_create(ffst_plan** out, const ffst_plan_desc* d) {
     P.c_lo = lo; P.ncols = hi - lo + 1;
     P.ncols_pad = (P.ncols + p->geo.colpad - 1) / p->geo.colpad * p->geo.colpad;
     P.nyq = -1;
-    if (plane_nyquist(d->n, j0, table[i])) {
+    if (plane_nyquist(d->n, j0, table[i], d->variant)) {
       P.nyq = (int)p->nyq.size();
       p->nyq.push_back((int)p->planes.size());
     }
@@ -904,7 +960,7 @@ ffst_status ffst_plan_create(ffst_plan** out, const ffst_plan_desc* d) {
   ALLOC(p->d_planes, p->planes.size() * sizeof(PlaneDev));
   ALLOC(p->d_nyq, nn * sizeof(int));
   ALLOC(p->d_tw, N * csz);
-  ALLOC(p->d_rtab, (size_t)(j0 + 1) * H1 * p->rsz);
+  ALLOC(p->d_rtab, (size_t)(d->variant == FFST_SMOOTH ? 3 * j0 + 4 : j0 + 1) * H1 * p->rsz);
   ALLOC(p->F, B * H1 * N * csz);
   ALLOC(p->Fscr, B * std::max(H1 * N, N * ncpf) * csz);
   ALLOC(p->A, (size_t)p->acc_lanes * B * H1 * N * csz);
@@ -921,7 +977,7 @@ ffst_status ffst_plan_create(ffst_plan** out, const ffst_plan_desc* d) {
   if (d->dtype == FFST_F32) fill_twiddles<float>(tw, d->n); else fill_twiddles<double>(tw, d->n);
   e = cudaMemcpy(p->d_tw, tw.data(), tw.size(), cudaMemcpyHostToDevice);
   {
-    const std::vector<double> rt = radial_table(d->n, j0);
+    const std::vector<double> rt = radial_all(d->n, j0, d->variant);
     if (d->dtype == FFST_F32) {
       std::vector<float> rf(rt.begin(), rt.end());
       if (e == cudaSuccess) e = cudaMemcpy(p->d_rtab, rf.data(), rf.size() * sizeof(float), cudaMemcpyHostToDevice);
@@ -948,8 +1004,8 @@ ffst_status ffst_plan_create(ffst_plan** out, const ffst_plan_desc* d) {
   }
   if (e == cudaSuccess && !p->nyq.empty()) {
     // anti part of each Nyquist plane on the Nyquist row / column (2n values per plane)
-    const std::vector<double> tab = radial_table(d->n, j0);
-    const Radial<double> R{tab.data(), (int)H1, j0};
+    const std::vector<double> tab = radial_all(d->n, j0, d->variant);
+    const Radial<double> R = host_radial(tab, d->n, j0, d->variant);
     const int Hh = d->n / 2;
     std::vector<double> anti(p->nyq.size() * 2 * N);
     for (size_t q = 0; q < p->nyq.size(); ++q) {

@@ -76,6 +76,7 @@ struct KParams {
   int* ctr;                     // [0] dispatch; [ctr_p1 + c]; [ctr_p2 + c]; [ctr_g + item]
   int ctr_p1, ctr_p2, ctr_g;
   int fetch_batch;              // warp path: consecutive items a CTA takes per global fetch
+  int variant;                  // 0 classic (meyerShearletSpect), 1 smooth (meyerNewShearletSpect)
   int compact;                  // f1 compact format: cube of reals + Nyquist vectors (G, H) in nyq_fwd
   int dbg;                      // measurement only (FFST_DBG): bit 0 skip FFTs, bit 1 skip output stores
   unsigned long long* trace;    // optional: per item {smid, t_start, t_ready, t_end} (globaltimer ns)

@@ -136,6 +136,14 @@ __device__ __forceinline__ void red_relaxed(int* ctr, int v) {
   asm volatile("red.relaxed.gpu.global.add.s32 [%0], %1;" ::"l"(ctr), "r"(v) : "memory");
 }
 
+// the plan's radial tables (classic rows; smooth rows after them when p.variant == 1)
+template <typename T, int N>
+__device__ __forceinline__ Radial<T> radial_of(const KParams& p) {
+  Radial<T> R{static_cast<const T*>(p.rtab), N / 2 + 1, p.j0};
+  if (p.variant == 1) R.smooth = static_cast<const T*>(p.rtab) + (size_t)(p.j0 + 1) * (N / 2 + 1);
+  return R;
+}
+
 template <typename T, int N>
 struct K {
   using G = Geo<T, N>;
@@ -195,7 +203,7 @@ struct K {
     const int tid = threadIdx.x, line = tid / G::THC, t = tid % G::THC;
     const C* tw = static_cast<const C*>(p.tw);
     const T delta = (T)p.delta;
-    const Radial<T> R{static_cast<const T*>(p.rtab), N / 2 + 1, p.j0};
+    const Radial<T> R = radial_of<T, N>(p);
     constexpr int ROUNDS = G::GC / G::LPC > 0 ? G::GC / G::LPC : 1;
 #pragma unroll 1
     for (int rd = 0; rd < ROUNDS; ++rd) {
@@ -259,7 +267,7 @@ struct K {
     T* wbuf = reinterpret_cast<T*>(tile + G::TILE_C);
     const int tid = threadIdx.x, line = tid / G::THC, t = tid % G::THC;
     const C* tw = static_cast<const C*>(p.tw);
-    const Radial<T> R{static_cast<const T*>(p.rtab), N / 2 + 1, p.j0};
+    const Radial<T> R = radial_of<T, N>(p);
     const int ci = line;
     const bool act = ci < cnt;
     const int cb = c0 + ci;
@@ -726,7 +734,7 @@ struct K {
     const int tid = threadIdx.x, line = tid / G::THC, t = tid % G::THC;
     const C* tw = static_cast<const C*>(p.tw);
     const T delta = (T)p.delta;
-    const Radial<T> R{static_cast<const T*>(p.rtab), N / 2 + 1, p.j0};
+    const Radial<T> R = radial_of<T, N>(p);
     const int g0 = I.group * G::LPC;
     const int g1 = g0 + G::LPC < H + 1 ? g0 + G::LPC : H + 1;
     const int cb = g0 + line;
@@ -1015,7 +1023,7 @@ __global__ void __launch_bounds__(256) nyq_fwd_kernel(KParams p) {
   if (act) P = p.planes[p.nyq_planes[nq]];
   const C* F = static_cast<const C*>(p.F) + (size_t)b * (H + 1) * N;
   const T delta = (T)p.delta;
-  const Radial<T> R{static_cast<const T*>(p.rtab), N / 2 + 1, p.j0};
+  const Radial<T> R = radial_of<T, N>(p);
   C r[G::EC];
 #pragma unroll 1
   for (int q = 0; q < G::EC; ++q) {
@@ -1060,7 +1068,7 @@ __global__ void __launch_bounds__(256) nyq_inv_kernel(KParams p) {
   C* scr = reinterpret_cast<C*>(smem_raw) + line * G::SMC;
   C* stage = reinterpret_cast<C*>(smem_raw) + G::SCR_C;          // [EC][NT] (also the reduction buffer)
   const T delta = (T)p.delta;
-  const Radial<T> R{static_cast<const T*>(p.rtab), N / 2 + 1, p.j0};
+  const Radial<T> R = radial_of<T, N>(p);
   C acc[G::EC];
 #pragma unroll
   for (int q = 0; q < G::EC; ++q) acc[q] = czero<T>();
@@ -1183,7 +1191,7 @@ template <typename T, int N>
 __global__ void spectra_kernel(KParams p, T* psi, int centred_layout) {
   const size_t total = (size_t)p.eta_l * N * N;
   const T delta = (T)p.delta;
-  const Radial<T> R{static_cast<const T*>(p.rtab), N / 2 + 1, p.j0};
+  const Radial<T> R = radial_of<T, N>(p);
   for (size_t e = blockIdx.x * (size_t)blockDim.x + threadIdx.x; e < total; e += (size_t)gridDim.x * blockDim.x) {
     const int i = (int)(e / ((size_t)N * N));
     const int rem = (int)(e - (size_t)i * N * N);

@@ -123,6 +123,18 @@ template <typename T> struct Radial {
   }
   FFST_HD T psi1(int j, int a) const { return ld(tab + j * stride + a); }
   FFST_HD T phi(int a) const { return ld(tab + j0 * stride + a); }
+  // smooth variant (Sec. smoothShearlets): rows of B_j(a) = varphi^2(4^-j Delta a),
+  // j = 0..j0+1, then of D_j(a) = B_(j+1)(a) - B_j(a), j = 0..j0 (computed stably by the planner);
+  // nullptr for the classic system.  Psi1(4^-j Delta u)^2 = B_(j+1)(a1) D_j(a2) + B_j(a2) D_j(a1):
+  // eq:newPsi1 with the tensor scaling function eq:Phi, a sum of non-negative terms (no cancellation).
+  const T* smooth = nullptr;
+  FFST_HD T corona(int j, int a1, int a2) const {
+    const T* B = smooth;
+    const T* D = smooth + (j0 + 2) * stride;
+    const T s = ld(B + (j + 1) * stride + a1) * ld(D + j * stride + a2) +
+                ld(B + j * stride + a2) * ld(D + j * stride + a1);
+    return s > T(0) ? sqrt(s) : T(0);
+  }
 };
 
 // psi1_hat(4^-j Delta |ua|) psi2_hat((k ua + 2^j ub)/ua) for |ub| <= |ua| (cone shearlet,
@@ -133,7 +145,8 @@ template <typename T> FFST_HD T cone_shearlet(int j, int k, int ua, int ub, cons
   const int num = k * ua + ub * (1 << j);                // exact (|num| < 2^24)
   const int anum = num < 0 ? -num : num;
   if (anum >= aa) return T(0);                           // |shear argument| >= 1 -> psi2 = 0
-  const T r = R.psi1(j, aa);
+  const int ab = ub < 0 ? -ub : ub;
+  const T r = R.smooth != nullptr ? R.corona(j, aa, ab) : R.psi1(j, aa);   // eq:Psi1 or eq:newPsi1
   if (r == T(0)) return T(0);
   const T t = T(aa - anum) / T(aa);                      // 1 - |argument|, one rounding
   return r * sqrt(meyer_v<T>(t));                        // psi2 = sqrt(v(1 - |x|))
@@ -142,7 +155,8 @@ template <typename T> FFST_HD T cone_shearlet(int j, int k, int ua, int ub, cons
 // psi_hat_i(Delta u1, Delta u2) for integer u (u may be +n/2: the mirrored point).
 template <typename T> FFST_HD T window(const PlaneDev& P, int u1, int u2, const Radial<T>& R) {
   const int a1 = u1 < 0 ? -u1 : u1, a2 = u2 < 0 ? -u2 : u2;
-  if (P.kind == 0) return R.phi(a2 <= a1 ? a1 : a2);     // eq:phi
+  if (P.kind == 0)                                        // eq:phi (classic) / eq:Phi (smooth)
+    return R.smooth != nullptr ? R.phi(a1) * R.phi(a2) : R.phi(a2 <= a1 ? a1 : a2);
   if (P.kind == 1) {                                     // horizontal cone |u2| < |u1|
     return a2 < a1 ? cone_shearlet<T>(P.j, P.k, u1, u2, R) : T(0);
   }

@@ -29,10 +29,12 @@ class ShardedTransform:
         self.world = dist.get_world_size(group)
 
     @classmethod
-    def create(cls, n: int, batch: int, dtype=torch.float32, device=None, group=None, root: int = 0):
+    def create(cls, n: int, batch: int, dtype=torch.float32, device=None, group=None, root: int = 0,
+               variant: str = "classic"):
         from .plan import Plan
         rank, world = dist.get_rank(group), dist.get_world_size(group)
-        return cls(Plan(n, batch, dtype, device=device, shard_rank=rank, shard_count=world), group, root)
+        return cls(Plan(n, batch, dtype, device=device, shard_rank=rank, shard_count=world,
+                        variant=variant), group, root)
 
     def forward(self, x):
         """x: images (valid on the root; overwritten by the broadcast elsewhere)."""

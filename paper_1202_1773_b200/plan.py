@@ -16,6 +16,7 @@ from ._lib import PlanDesc, check, lib
 KIND_NAMES = {0: "lowpass", 1: "h", 2: "v", 3: "x"}
 _DTYPES = {torch.float32: 0, torch.float64: 1}
 _CDTYPES = {torch.float32: torch.complex64, torch.float64: torch.complex128}
+_VARIANTS = {"classic": 0, "smooth": 1}
 
 
 def scales_for_size(n: int) -> int:
@@ -69,7 +70,7 @@ class Plan:
     i % shard_count == shard_rank (eta-sharding, DESIGN.md "Multi-GPU")."""
 
     def __init__(self, n: int, batch: int = 1, dtype=torch.float32, device=None, j0: int = 0,
-                 shard_rank: int = 0, shard_count: int = 1):
+                 shard_rank: int = 0, shard_count: int = 1, variant: str = "classic"):
         if not torch.cuda.is_available():
             raise RuntimeError("FFST Plan needs a CUDA device (no CPU fallback)")
         if dtype not in _DTYPES:
@@ -78,7 +79,10 @@ class Plan:
                                    torch.device(device).index or 0)
         self.dtype = dtype
         self.cdtype = _CDTYPES[dtype]
-        desc = PlanDesc(int(n), int(j0), int(batch), _DTYPES[dtype], 0, self.device.index,
+        if variant not in _VARIANTS:
+            raise ValueError("variant must be 'classic' (meyerShearletSpect) or 'smooth' (meyerNewShearletSpect)")
+        self.variant = variant
+        desc = PlanDesc(int(n), int(j0), int(batch), _DTYPES[dtype], _VARIANTS[variant], self.device.index,
                         int(shard_rank), int(shard_count))
         handle = C.c_void_p()
         with torch.cuda.device(self.device):

@@ -324,3 +324,104 @@ def test_compact_warp_path_unsupported(F, monkeypatch):
     x = torch.zeros(1, 64, 64, device="cuda")
     with pytest.raises(F.FFSTError):
         plan.forward_compact(x)
+
+
+# ------------------------------------------------------------------ smooth variant
+# The oracle writes eq:newPsi1 as printed, sqrt(Phi^2(w/4) - Phi^2(w)): where the difference is
+# O(eps) its square root is only good to ~sqrt(eps) ~ 1.5e-8 absolute, while the kernels use the
+# cancellation-free form (reading A19).  float64 comparisons against the oracle's
+# smooth spectra therefore use SMOOTH_F64 = 1e-7; squares agree to ~1e-15 and round trips (the
+# kernels' own frame) keep the classic 1e-10.
+SMOOTH_F64 = 1e-7
+TOL_SMOOTH = {torch.float32: 1e-4, torch.float64: SMOOTH_F64}
+
+
+@pytest.mark.parametrize("n,dtype", [(4, torch.float64), (16, torch.float64), (64, torch.float64),
+                                     (256, torch.float32), (512, torch.float32)])
+def test_smooth_spectra_match_oracle(F, n, dtype):
+    plan = F.Plan(n, 1, dtype, variant="smooth")
+    psi = plan.spectra(centred=True).cpu().double().numpy()
+    ref = O.shearlet_spectra(n, variant="smooth")
+    if dtype == torch.float64:
+        assert np.max(np.abs(psi**2 - ref**2)) < 1e-13
+        assert np.max(np.abs(psi - ref)) < SMOOTH_F64
+    else:
+        assert np.max(np.abs(psi - ref)) < 2e-6
+    assert np.max(np.abs(np.sum(psi**2, axis=0) - 1.0)) < (1e-13 if dtype == torch.float64 else 1e-5)
+    # the classic and smooth systems are different systems
+    assert np.max(np.abs(psi - O.shearlet_spectra(n))) > 1e-3 or n < 16
+
+
+@pytest.mark.parametrize("n", [4, 8, 16, 32, 64, 128, 256])
+@pytest.mark.parametrize("dtype", [torch.float64, torch.float32])
+def test_smooth_forward_inverse_small(F, n, dtype, monkeypatch):
+    monkeypatch.setenv("FFST_PATH", "warp")          # ignored for the smooth system (CTA kernels)
+    batch = 3
+    x, xo = images(2, batch, n, dtype)
+    plan = F.Plan(n, batch, dtype, variant="smooth")
+    c = plan.forward(x.cuda())
+    rec = plan.inverse(c)
+    torch.cuda.synchronize()
+    c = c.cpu().numpy()
+    rec = rec.cpu().numpy()
+    psi = O.shearlet_spectra(n, variant="smooth")
+    for b in range(batch):
+        ref = O.forward(xo[b], psi=psi)
+        assert plane_err(c[b], ref, np.max(np.abs(xo[b]))).max() <= TOL_SMOOTH[dtype], (n, b)
+        ref_inv = O.inverse(c[b].astype(np.complex128), psi=psi).real
+        assert plane_err(rec[b], ref_inv).max() <= TOL_SMOOTH[dtype]
+        assert plane_err(rec[b], xo[b]).max() <= TOL[dtype]
+
+
+def test_smooth_config2_full(F):
+    # configs[1] shape with the smooth system: every plane of every image, inverse, round trip
+    cfg = synth.config(2)
+    x, xo = images(2, cfg.batch, cfg.n, torch.float32)
+    plan = F.Plan(cfg.n, cfg.batch, torch.float32, variant="smooth")
+    c = plan.forward(x.cuda())
+    rec = plan.inverse(c).cpu().numpy()
+    c = c.cpu().numpy()
+    psi = O.shearlet_spectra(cfg.n, variant="smooth")
+    for b in range(cfg.batch):
+        ref = O.forward(xo[b], psi=psi)
+        assert plane_err(c[b], ref, np.max(np.abs(xo[b]))).max() <= 1e-4, b
+        ref_inv = O.inverse(c[b].astype(np.complex128), psi=psi).real
+        assert plane_err(rec[b], ref_inv).max() <= 1e-4
+        assert plane_err(rec[b], xo[b]).max() <= 1e-4
+
+
+def test_smooth_large_sampled(F):
+    # n = 2048 float32 (multi-slot planes in HBM): sampled planes, round trip, Parseval
+    n = 2048
+    x, _ = images(5, 1, n, torch.float32)
+    plan = F.Plan(n, 1, torch.float32, variant="smooth")
+    xd = x.cuda()
+    c = plan.forward(xd)
+    rec = plan.inverse(c)
+    assert float((rec - xd).abs().max() / xd.abs().max()) <= 1e-4
+    ec = float((c.abs() ** 2).double().sum())
+    ef = float((xd.double() ** 2).sum())
+    assert abs(ec - ef) / ef <= 1e-4
+    eta = plan.eta
+    nyq = plan.nyquist_planes()
+    planes = sorted({0, 1, eta // 2, eta - 1, nyq[0], nyq[len(nyq) // 2]})
+    x64 = x[0].double().numpy()
+    f_hat = O.dft2_centred(x64)
+    for i in planes:
+        ref = O.forward_plane(x64, i + 1, f_hat=f_hat, variant="smooth")
+        assert plane_err(c[0, i].cpu().numpy(), ref, np.max(np.abs(x64))) <= 1e-4, i
+
+
+@pytest.mark.parametrize("n,dtype,batch", [(64, torch.float64, 2), (256, torch.float32, 4)])
+def test_smooth_compact_format(F, n, dtype, batch):
+    x, xo = images(2, batch, n, dtype)
+    xd = x.cuda()
+    plan = F.Plan(n, batch, dtype, variant="smooth")
+    c = plan.forward(xd)
+    re, gh = plan.forward_compact(xd)
+    ce = plan.expand_compact(re, gh)
+    scale = c.abs().amax(dim=(2, 3), keepdim=True).clamp_min(1e-30)
+    tol = 1e-5 if dtype == torch.float32 else 1e-12
+    assert float(((ce - c).abs() / scale).max()) <= tol
+    r_compact = plan.inverse_compact(re, gh)
+    assert plane_err(r_compact.cpu().numpy(), xo).max() <= TOL[dtype]

@@ -389,3 +389,72 @@ def test_imaginary_part_rank_two(n):
         rec = sgn[:, None] * g[None, :] + sgn[None, :] * h[:, None]
         assert np.max(np.abs(rec - y)) <= 1e-12 * max(1.0, np.max(np.abs(c[i])))
         assert np.linalg.matrix_rank(y, tol=1e-10 * max(1.0, np.max(np.abs(y)))) <= 2
+
+
+# ---------------------------------------------------------------- smooth variant
+
+@pytest.mark.parametrize("n", [8, 9, 32, 33, 64, 65, 256])
+def test_smooth_frame_tightness(n):
+    # Sec. smoothShearlets: Phi^2(w) + sum_j Psi1^2(4^-j w) telescopes to
+    # Phi^2(4^-j0 w) = 1 on the grid, and the psi2 shears tile each cone as before, so the
+    # smooth system is again a Parseval frame: sum_i psi_i^2 = 1 at every grid point.
+    psi = O.shearlet_spectra(n, variant="smooth")
+    assert psi.shape[0] == O.num_shearlets(O.scales_for_size(n))
+    dev = np.max(np.abs(np.sum(psi**2, axis=0) - 1.0))
+    assert dev < 1e-13, dev
+
+
+def test_smooth_psi1_support_and_axis():
+    # Psi1 is supported in [-4,4]^2 minus [-1/2,1/2]^2.  On an axis Phi = varphi, so
+    # Psi1(w1, 0)^2 = varphi^2(w1/4) - varphi^2(w1), which the partition of unity
+    # varphi^2 + sum_j psi1^2(4^-j .) = 1 makes psi1_hat(w1)^2: the
+    # smooth corona function restricted to an axis is the classic radial function.
+    g = np.linspace(-5, 5, 401)
+    w1, w2 = np.meshgrid(g, g)
+    p = O.smooth_psi1(w1, w2)
+    m = np.maximum(np.abs(w1), np.abs(w2))
+    assert np.all(p[(m <= 0.5) | (m >= 4.0)] == 0.0)
+    assert np.all(p[(m > 0.55) & (m < 3.9)] > 0.0)
+    x = np.linspace(-5, 5, 2001)
+    assert np.max(np.abs(O.smooth_psi1(x, 0.0 * x) - O.psi1_hat(x))) < 1e-7   # sqrt of a difference
+    assert np.max(np.abs(O.smooth_psi1(x, 0.0 * x) ** 2 - O.psi1_hat(x) ** 2)) < 1e-14
+    # tensor scaling function: 1 on [-1/2,1/2]^2, 0 once a coordinate reaches 1, symmetric
+    assert np.all(O.tensor_scaling_Phi(w1, w2)[m <= 0.5] == 1.0)
+    assert np.all(O.tensor_scaling_Phi(w1, w2)[m >= 1.0] == 0.0)
+    assert np.array_equal(O.tensor_scaling_Phi(w1, w2), O.tensor_scaling_Phi(w2, w1))
+
+
+def test_smooth_equals_classic_near_the_axis():
+    # In the horizontal cone at scale j, where |4^-j w2| <= 1/2 the second factor of Phi is 1 at
+    # both dilations, so Psi1(4^-j w) = psi1_hat(4^-j w1) and the smooth cone shearlet equals the
+    # classic one (eq:newPsi1 vs eq:Psi1); the two systems differ only away from the axes.
+    n = 128
+    j0 = O.scales_for_size(n)
+    axis, *_ = O.frequency_grid(n, j0)
+    w1, w2 = np.meshgrid(axis[:n], axis[:n])
+    differs = 0
+    for i in range(2, O.num_shearlets(j0) + 1):
+        kind, j, k = O.index_to_params(j0, i)
+        if kind != O.KIND_H:
+            continue
+        a = O.shearlet_spectrum(n, i, j0)
+        b = O.shearlet_spectrum(n, i, j0, variant="smooth")
+        near = np.abs(w2) * 4.0 ** (-j) <= 0.5
+        assert np.max(np.abs(a[near] - b[near])) < 1e-7
+        differs += int(np.max(np.abs(a - b)) > 1e-3)
+    assert differs > 0
+
+
+@pytest.mark.parametrize("n", [16, 33])
+def test_smooth_round_trip_and_parseval(n):
+    # Parseval frame: ||SH f||^2 = ||f||^2 and the adjoint inverts the transform.
+    f = synth.make_batch(1, n=n)[0]
+    c = O.forward(f, variant="smooth")
+    assert abs(np.sum(np.abs(c) ** 2) - np.sum(f**2)) < 1e-10 * np.sum(f**2)
+    rec = O.inverse(c, variant="smooth")
+    assert np.max(np.abs(rec.real - f)) < 1e-11 * np.max(np.abs(f))
+
+
+def test_unknown_variant_rejected():
+    with pytest.raises(ValueError):
+        O.shearlet_spectrum(16, 2, variant="bogus")
