@@ -67,7 +67,7 @@ typedef enum { FFST_F32 = 0, FFST_F64 = 1 } ffst_dtype;
  * (P:L1766-1820): low-pass Phi(w) = varphi(w1) varphi(w2) (eq:Phi), cone shearlets
  * Psi1(4^-j w) psi2(2^j w_b/w_a + k) with Psi1 = sqrt(Phi^2(w/4) - Phi^2(w)) (eq:newPsi1,
  * eq:smoothPsi), same cones, seams and index order; isotropic dilation (reading A18). */
-typedef enum { FFST_CLASSIC = 0, FFST_SMOOTH = 1 } ffst_variant;
+typedef enum { FFST_CLASSIC = 0, FFST_SMOOTH = 1, FFST_USER = 2 } ffst_variant;   /* USER: see ffst_plan_create_user */
 
 /* Shearlet kinds of the flat index (Sec. 3.5.1): low-pass, horizontal cone,
  * vertical cone, glued seam ("h x v", |k| = 2^j). */
@@ -123,10 +123,35 @@ ffst_status ffst_plane_is_nyquist(int n, int j0, int index, int* is_nyquist);
  *   FFST_CHUNK_PLANES   planes per chunk (default 4; 32 for batch <= 4)
  *   FFST_SLOT_KB        chunk byte budget (default 4096)
  *   FFST_ACC_LANES      accumulator lanes of the inverse (default: up to 4 while <= 32 MB)
- *   FFST_VERBOSE        print the queue geometry
+ *   FFST_VERBOSE        print the queue geometry and the persistent grids
+ *   FFST_CTAS_PER_SM    cap on resident CTAs per SM of the persistent kernels (default: occupancy)
  * Measurement only (results are WRONG): FFST_QUEUE_ONLY=1|2 (one pass type), FFST_DBG bits. */
 ffst_status ffst_plan_create(ffst_plan** out, const ffst_plan_desc* desc);
 ffst_status ffst_plan_destroy(ffst_plan* plan);
+
+/* User-supplied spectra: "precomputed shearlet spectra which are then used for
+ * the computation of the transform" (the inverse with the same Psi,
+ * P:L2221-2224).  psi: DEVICE pointer (on desc->device) to eta real spectra [eta][n][n] of the
+ * plan's dtype, rows omega_2, columns omega_1; centred_layout != 0: omega = 0 at (n/2, n/2) (the
+ * paper's Psi), else natural FFT bin order.  Read during this call only (the plan
+ * keeps its own Hermitian-half copy of the symmetric parts, eta_local x (n/2+1) x n reals, and
+ * prunes each plane to its non-zero column range).  desc->variant and desc->j0 are ignored;
+ * eta may be any count >= 1 (the plan's eta).  Sharding as for ffst_plan_create (all eta
+ * planes are passed on every rank).  The spectra must be point-symmetric off the Nyquist lines,
+ * psi(u) = psi(-u) for u1, u2 != -n/2 (the spectra of real shearlets; every built-in system is),
+ * to within 1e-5 (float32) / 1e-12 (float64) absolute -- else INVALID_ARG; the Nyquist row and
+ * column may be asymmetric (handled exactly).  The Parseval admission check of
+ * P:L2219-2220 is computed but not enforced: ffst_plan_spectra_check.
+ * Errors: as ffst_plan_create, plus INVALID_ARG (null psi, eta < 1, asymmetric spectra). */
+ffst_status ffst_plan_create_user(ffst_plan** out, const ffst_plan_desc* desc, int eta, const void* psi,
+                                  int centred_layout);
+
+/* Admission numbers of the plan's system: *tightness = max over the grid of
+ * |sum_i psi_i^2 - 1| (0 for a Parseval frame, "close to zero" in the paper), *asymmetry = max
+ * |psi_i(u) - psi_i(-u)| off the Nyquist lines.  User plans: computed at creation.  Built-in
+ * plans: computed on the first call from the materialised spectra (needs shard_count == 1,
+ * else UNSUPPORTED; allocates eta n^2 reals temporarily). */
+ffst_status ffst_plan_spectra_check(ffst_plan* plan, double* tightness, double* asymmetry);
 
 /* Number of local planes and (if global_indices != NULL) their 0-based global indices. */
 ffst_status ffst_plan_local_planes(const ffst_plan* plan, int* count, int* global_indices);

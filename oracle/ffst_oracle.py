@@ -37,7 +37,7 @@ __all__ = [
     "scaling_varphi", "scales_for_size", "num_shearlets", "index_to_params",
     "params_to_index", "frequency_grid", "shearlet_spectrum", "shearlet_spectra",
     "dft2_centred", "idft2_centred", "dft2_direct", "idft2_direct",
-    "forward", "forward_plane", "inverse", "tensor_scaling_Phi", "smooth_psi1", "KIND_S", "KIND_H", "KIND_V", "KIND_X",
+    "forward", "forward_plane", "inverse", "tensor_scaling_Phi", "smooth_psi1", "frame_tightness", "KIND_S", "KIND_H", "KIND_V", "KIND_X",
 ]
 
 KIND_S, KIND_H, KIND_V, KIND_X = 0, 1, 2, 3   # low-pass, horizontal, vertical, seam ("h x v")
@@ -293,6 +293,13 @@ def idft2_direct(g):
     return (e @ g @ e.T) / (n * n)
 
 
+def frame_tightness(psi):
+    """The Parseval check of P:L2219-2220 for any spectra set (built-in or user-supplied,
+    P:L2209-2217): max over the grid of |sum_i psi_i^2 - 1| ("sum(abs(Psi).^2,3)-1")."""
+    psi = np.asarray(psi, dtype=np.float64)
+    return float(np.max(np.abs(np.sum(np.abs(psi) ** 2, axis=0) - 1.0)))
+
+
 # ---------------------------------------------------------------------------
 # 3.1 / 3.3  Forward and inverse transform
 # ---------------------------------------------------------------------------
@@ -332,8 +339,8 @@ def inverse(coeffs, psi=None, j0: int | None = None, direct: bool = False, plane
     n = coeffs.shape[-1]
     if j0 is None:
         j0 = scales_for_size(n)
-    if planes is None:
-        planes = range(1, num_shearlets(j0) + 1)
+    if planes is None:   # every plane of the system (a user Psi has len(psi) planes)
+        planes = range(1, (len(psi) if psi is not None else num_shearlets(j0)) + 1)
     dft, idft = (dft2_direct, idft2_direct) if direct else (dft2_centred, idft2_centred)
     acc = np.zeros((n, n), dtype=np.complex128)
     for slot, i in enumerate(planes):

@@ -16,6 +16,7 @@ SOURCES = ["ffst_api.cu", "ffst_kern_f32.cu", "ffst_kern_f64.cu"]
 NVCC = os.environ.get("NVCC", "/usr/local/cuda/bin/nvcc")
 FLAGS = ["-std=c++17", "-O3", "--expt-relaxed-constexpr", "-lineinfo", "-gencode", "arch=compute_100a,code=sm_100a",
          "-Xcompiler", "-fPIC", "-Xptxas", "-warn-spills", f"-I{ROOT / 'include'}", f"-I{CSRC}"]
+EXTRA = {}   # per-source extra flags (none)
 
 
 def _stale(obj: Path, deps) -> bool:
@@ -32,7 +33,7 @@ def build(verbose: bool = False, force: bool = False) -> Path:
     for src in SOURCES:
         obj = BUILD / (Path(src).stem + ".o")
         if force or _stale(obj, headers + [CSRC / src]):
-            jobs.append([NVCC, *FLAGS, "-c", str(CSRC / src), "-o", str(obj)])
+            jobs.append([NVCC, *FLAGS, *EXTRA.get(src, []), "-c", str(CSRC / src), "-o", str(obj)])
 
     def run(cmd):
         if verbose:

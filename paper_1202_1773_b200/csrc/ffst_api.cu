@@ -287,6 +287,9 @@ struct ffst_plan {
   cudaEvent_t fork[2] = {};
   int launches[2] = {0, 0};
   std::vector<void*> allocs;
+  // user spectra (f4, ffst_plan_create_user)
+  void* d_usym = nullptr;         // [eta_l][n/2+1][n] T symmetric parts
+  double tightness = -1, asymmetry = -1;   // admission check; -1: not computed yet
 };
 
 namespace {
@@ -609,7 +612,8 @@ KParams base_params(ffst_plan* p) {
   KParams k{};
   k.n = p->n; k.j0 = p->j0; k.batch = p->d.batch; k.eta_l = p->eta_l; k.n_nyq = (int)p->nyq.size();
   k.delta = p->delta;
-  k.variant = p->d.variant == FFST_SMOOTH ? 1 : 0;
+  k.variant = (int)p->d.variant;
+  k.usym = p->d_usym;
   k.planes = p->d_planes;
   k.nyq_planes = p->d_nyq;
   k.tw = p->d_tw;
@@ -776,6 +780,73 @@ ffst_status inverse_impl(ffst_plan* p, const void* coeff, void* img_out, int bat
   return FFST_OK;
 }
 
+// User spectra (f4): run the prepare kernels (ffst_user.cuh) on the caller's eta planes, keep the
+// admission numbers, and replace each local plane's provisional geometry by its column hull and
+// Nyquist flag.  `anti` receives the anti parts of every local plane ([eta_l][2][n], float64).
+struct UserSpectra {
+  int eta;
+  const void* psi;
+  int centred;
+};
+
+ffst_status user_prepare(ffst_plan* p, const UserSpectra& us, std::vector<double>& anti) {
+  const int n = p->n, H = n / 2, L = p->eta_l;
+  const size_t rsz = p->rsz;
+  void* ptr = nullptr;
+  TRY(dalloc(p, &ptr, (size_t)L * (H + 1) * n * rsz));
+  p->d_usym = ptr;
+  void *d_hull = nullptr, *d_anti = nullptr, *d_stats = nullptr;
+  cudaError_t e = cudaMalloc(&d_hull, (size_t)L * 2 * sizeof(int));
+  if (e == cudaSuccess) e = cudaMalloc(&d_anti, (size_t)L * 2 * n * rsz);
+  if (e == cudaSuccess) e = cudaMalloc(&d_stats, 2 * sizeof(unsigned long long));
+  std::vector<int> hull((size_t)L * 2);
+  for (int l = 0; l < L; ++l) { hull[2 * l] = H + 1; hull[2 * l + 1] = -1; }
+  if (e == cudaSuccess) e = cudaMemcpy(d_hull, hull.data(), hull.size() * sizeof(int), cudaMemcpyHostToDevice);
+  if (e == cudaSuccess) e = cudaMemset(d_stats, 0, 2 * sizeof(unsigned long long));
+  if (e == cudaSuccess) {
+    UserPrep u{};
+    u.psi = us.psi; u.n = n; u.eta = us.eta; u.centred = us.centred;
+    u.shard_rank = p->d.shard_rank; u.shard_count = p->d.shard_count; u.eta_l = L;
+    u.usym = p->d_usym; u.hull = static_cast<int*>(d_hull); u.anti = d_anti;
+    u.stats = static_cast<unsigned long long*>(d_stats);
+    const int grid = p->sm_count * 8;
+    e = p->d.dtype == FFST_F32 ? launch_user_prepare<float>(u, grid, 0) : launch_user_prepare<double>(u, grid, 0);
+  }
+  std::vector<unsigned char> an((size_t)L * 2 * n * rsz);
+  unsigned long long st[2] = {0, 0};
+  if (e == cudaSuccess) e = cudaDeviceSynchronize();
+  if (e == cudaSuccess) e = cudaMemcpy(hull.data(), d_hull, hull.size() * sizeof(int), cudaMemcpyDeviceToHost);
+  if (e == cudaSuccess) e = cudaMemcpy(an.data(), d_anti, an.size(), cudaMemcpyDeviceToHost);
+  if (e == cudaSuccess) e = cudaMemcpy(st, d_stats, sizeof(st), cudaMemcpyDeviceToHost);
+  cudaFree(d_hull); cudaFree(d_anti); cudaFree(d_stats);
+  if (e != cudaSuccess) return cuda_fail(e, "user spectra prepare");
+  std::memcpy(&p->tightness, &st[0], sizeof(double));
+  std::memcpy(&p->asymmetry, &st[1], sizeof(double));
+  // psi_i(u) = psi_i(-u) off the Nyquist lines is what the even-n decomposition relies on (real
+  // shearlets); an asymmetric part there would be dropped silently, so it is refused
+  const double tol = p->d.dtype == FFST_F32 ? 1e-5 : 1e-12;
+  if (!(p->asymmetry <= tol))
+    return fail(FFST_ERR_INVALID_ARG, "user spectra not point-symmetric off the Nyquist lines (max |psi(u) - psi(-u)| = " +
+                                          std::to_string(p->asymmetry) + ")");
+  anti.assign((size_t)L * 2 * n, 0.0);
+  for (size_t i = 0; i < anti.size(); ++i)
+    anti[i] = p->d.dtype == FFST_F32 ? (double)reinterpret_cast<const float*>(an.data())[i]
+                                      : reinterpret_cast<const double*>(an.data())[i];
+  p->nyq.clear();
+  for (int l = 0; l < L; ++l) {
+    PlaneDev& P = p->planes[l];
+    if (hull[2 * l] > hull[2 * l + 1]) { hull[2 * l] = 0; hull[2 * l + 1] = 0; }   // an all-zero plane
+    P.c_lo = hull[2 * l];
+    P.ncols = hull[2 * l + 1] - hull[2 * l] + 1;
+    P.ncols_pad = (P.ncols + p->geo.colpad - 1) / p->geo.colpad * p->geo.colpad;
+    bool nyq = false;
+    for (int m = 0; m < 2 * n && !nyq; ++m) nyq = anti[(size_t)l * 2 * n + m] != 0.0;
+    P.nyq = nyq ? (int)p->nyq.size() : -1;
+    if (nyq) p->nyq.push_back(l);
+  }
+  return FFST_OK;
+}
+
 }  // namespace
 
 // ============================================================================ C ABI
@@ -850,22 +921,41 @@ ffst_status ffst_plan_destroy(ffst_plan* p) {
   return FFST_OK;
 }
 
+static ffst_status plan_create_impl(ffst_plan** out, const ffst_plan_desc* d, const UserSpectra* us);
+
 ffst_status ffst_plan_create(ffst_plan** out, const ffst_plan_desc* d) {
   if (!out || !d) return fail(FFST_ERR_INVALID_ARG, "null argument");
+  if (d->variant == FFST_USER) return fail(FFST_ERR_INVALID_ARG, "FFST_USER plans come from ffst_plan_create_user");
+  return plan_create_impl(out, d, nullptr);
+}
+
+ffst_status ffst_plan_create_user(ffst_plan** out, const ffst_plan_desc* d, int eta, const void* psi,
+                                  int centred_layout) {
+  if (!out || !d || !psi) return fail(FFST_ERR_INVALID_ARG, "null argument");
+  if (eta < 1) return fail(FFST_ERR_INVALID_ARG, "eta < 1");
+  const UserSpectra us{eta, psi, centred_layout ? 1 : 0};
+  return plan_create_impl(out, d, &us);
+}
+
+static ffst_status plan_create_impl(ffst_plan** out, const ffst_plan_desc* d_in, const UserSpectra* us) {
   *out = nullptr;
+  ffst_plan_desc desc = *d_in;
+  if (us) { desc.variant = FFST_USER; desc.j0 = 0; }
+  const ffst_plan_desc* d = &desc;
   if (d->n < 4) return fail(FFST_ERR_INVALID_SIZE, "n < 4: no scale fits (P:L2163-2168)");
   if (d->dtype != FFST_F32 && d->dtype != FFST_F64) return fail(FFST_ERR_DTYPE, "dtype must be FFST_F32 or FFST_F64");
   const int maxn = d->dtype == FFST_F32 ? 4096 : 2048;
   if (d->n > maxn) return fail(FFST_ERR_INVALID_SIZE, "n above the largest built size (4096 f32, 2048 f64)");
   if (!is_pow2(d->n)) return fail(FFST_ERR_UNSUPPORTED, "n must be a power of two in this build");
-  if (d->variant != FFST_CLASSIC && d->variant != FFST_SMOOTH) return fail(FFST_ERR_INVALID_ARG, "unknown variant");
+  if (d->variant != FFST_CLASSIC && d->variant != FFST_SMOOTH && d->variant != FFST_USER)
+    return fail(FFST_ERR_INVALID_ARG, "unknown variant");
   if (d->batch < 1) return fail(FFST_ERR_INVALID_ARG, "batch < 1");
   if (d->shard_count < 1 || d->shard_rank < 0 || d->shard_rank >= d->shard_count)
     return fail(FFST_ERR_INVALID_ARG, "bad shard_rank / shard_count");
   const int j0 = d->j0 == 0 ? default_j0(d->n) : d->j0;
   if (j0 < 1 || (1 << (2 * j0)) > 4 * d->n || j0 > 12)
     return fail(FFST_ERR_INVALID_ARG, "j0 outside 1..(floor(log2 n)/2 + 1)");
-  const int eta = ffst_num_shearlets(j0);
+  const int eta = us ? us->eta : ffst_num_shearlets(j0);
   if (d->shard_count > eta) return fail(FFST_ERR_INVALID_ARG, "more shards than shearlets");
 
   ffst_plan* p = new ffst_plan();
@@ -886,16 +976,22 @@ ffst_status ffst_plan_create(ffst_plan** out, const ffst_plan_desc* d) {
   const auto table = index_table(j0);
   for (int i = d->shard_rank; i < eta; i += d->shard_count) {
     PlaneDev P{};
-    P.gi = i; P.kind = table[i].kind; P.j = table[i].j; P.k = table[i].k;
-    int lo, hi;
-    plane_columns(d->n, j0, table[i], &lo, &hi);
-    P.c_lo = lo; P.ncols = hi - lo + 1;
-    P.ncols_pad = (P.ncols + p->geo.colpad - 1) / p->geo.colpad * p->geo.colpad;
+    P.gi = i;
+    P.rec = (int)p->planes.size();   // (the warp path overwrites it with its column-record index)
     P.nyq = -1;
-    if (plane_nyquist(d->n, j0, table[i], d->variant)) {
-      P.nyq = (int)p->nyq.size();
-      p->nyq.push_back((int)p->planes.size());
+    if (us) {   // user spectra: the whole half plane until the prepare pass has found the hulls
+      P.c_lo = 0; P.ncols = d->n / 2 + 1;
+    } else {
+      P.kind = table[i].kind; P.j = table[i].j; P.k = table[i].k;
+      int lo, hi;
+      plane_columns(d->n, j0, table[i], &lo, &hi);
+      P.c_lo = lo; P.ncols = hi - lo + 1;
+      if (plane_nyquist(d->n, j0, table[i], d->variant)) {
+        P.nyq = (int)p->nyq.size();
+        p->nyq.push_back((int)p->planes.size());
+      }
     }
+    P.ncols_pad = (P.ncols + p->geo.colpad - 1) / p->geo.colpad * p->geo.colpad;
     p->planes.push_back(P);
   }
   p->eta_l = (int)p->planes.size();
@@ -919,11 +1015,22 @@ ffst_status ffst_plan_create(ffst_plan** out, const ffst_plan_desc* d) {
     if (af < 1 || ai < 1) return cleanup(fail(FFST_ERR_CUDA, "persistent kernels cannot be made resident"));
     p->grid_fwd = p->sm_count * af;
     p->grid_inv = p->sm_count * ai;
+    if (const char* cs = std::getenv("FFST_CTAS_PER_SM")) {   // measurement / debugging only
+      p->grid_fwd = p->sm_count * std::max(1, std::min(af, std::atoi(cs)));
+      p->grid_inv = p->sm_count * std::max(1, std::min(ai, std::atoi(cs)));
+    }
+    if (std::getenv("FFST_VERBOSE"))
+      std::fprintf(stderr, "[ffst] CTAs/SM fwd %d inv %d (grid %d / %d)\n", af, ai, p->grid_fwd, p->grid_inv);
     p->workers = std::max(p->grid_fwd, p->grid_inv);
   }
 
   const size_t B = (size_t)d->batch, N = (size_t)d->n, H1 = N / 2 + 1;
   const size_t csz = 2 * p->rsz;
+  std::vector<double> user_anti;      // user spectra: anti parts of every local plane [eta_l][2][n]
+  if (us) {
+    ffst_status st_u = user_prepare(p, *us, user_anti);
+    if (st_u != FFST_OK) return cleanup(st_u);
+  }
   const size_t ncpf = (size_t)p->geo.ncpf;          // row stride of the final column pass (aux kernels)
   // ring of intermediates: slot budget ~ L2 share, at least the largest plane
   long long maxplane = 0, image_total = 0;
@@ -1002,7 +1109,17 @@ ffst_status ffst_plan_create(ffst_plan** out, const ffst_plan_desc* d) {
     e = cudaMemcpy(p->d_colrec, d->dtype == FFST_F32 ? (const void*)rf.data() : (const void*)rd.data(), bytes,
                    cudaMemcpyHostToDevice);
   }
-  if (e == cudaSuccess && !p->nyq.empty()) {
+  if (e == cudaSuccess && !p->nyq.empty() && us) {
+    std::vector<double> anti(p->nyq.size() * 2 * N);
+    for (size_t q = 0; q < p->nyq.size(); ++q)
+      std::copy_n(user_anti.begin() + (size_t)p->nyq[q] * 2 * N, 2 * N, anti.begin() + q * 2 * N);
+    if (d->dtype == FFST_F32) {
+      std::vector<float> af(anti.begin(), anti.end());
+      e = cudaMemcpy(p->nyq_anti, af.data(), af.size() * sizeof(float), cudaMemcpyHostToDevice);
+    } else {
+      e = cudaMemcpy(p->nyq_anti, anti.data(), anti.size() * sizeof(double), cudaMemcpyHostToDevice);
+    }
+  } else if (e == cudaSuccess && !p->nyq.empty()) {
     // anti part of each Nyquist plane on the Nyquist row / column (2n values per plane)
     const std::vector<double> tab = radial_all(d->n, j0, d->variant);
     const Radial<double> R = host_radial(tab, d->n, j0, d->variant);
@@ -1066,6 +1183,41 @@ ffst_status ffst_plan_info(const ffst_plan* p, int* n, int* j0, int* eta, int* e
   if (eta) *eta = p->eta;
   if (eta_local) *eta_local = p->eta_l;
   if (batch) *batch = p->d.batch;
+  return FFST_OK;
+}
+
+ffst_status ffst_plan_spectra_check(ffst_plan* p, double* tightness, double* asymmetry) {
+  if (!p || !tightness || !asymmetry) return fail(FFST_ERR_INVALID_ARG, "null argument");
+  if (p->tightness < 0) {
+    // built-in systems: materialise the spectra once and reduce the same admission numbers
+    if (p->d.shard_count != 1) return fail(FFST_ERR_UNSUPPORTED, "spectra check of a sharded built-in plan");
+    TRY(set_device(p));
+    const size_t bytes = (size_t)p->eta * p->n * p->n * p->rsz;
+    void *psi = nullptr, *st = nullptr;
+    cudaError_t e = cudaMalloc(&psi, bytes);
+    if (e == cudaSuccess) e = cudaMalloc(&st, 2 * sizeof(unsigned long long));
+    if (e == cudaSuccess) e = cudaMemset(st, 0, 2 * sizeof(unsigned long long));
+    KParams k = base_params(p);
+    if (e == cudaSuccess)
+      e = p->d.dtype == FFST_F32 ? launch_spectra_export<float>(k, psi, 0, 0) : launch_spectra_export<double>(k, psi, 0, 0);
+    if (e == cudaSuccess) {
+      UserPrep u{};
+      u.psi = psi; u.n = p->n; u.eta = p->eta; u.centred = 0;
+      u.shard_rank = 0; u.shard_count = 1; u.eta_l = p->eta_l;
+      u.stats = static_cast<unsigned long long*>(st);
+      e = p->d.dtype == FFST_F32 ? launch_user_prepare<float>(u, p->sm_count * 8, 0)
+                                 : launch_user_prepare<double>(u, p->sm_count * 8, 0);
+    }
+    unsigned long long h[2] = {0, 0};
+    if (e == cudaSuccess) e = cudaMemcpy(h, st, sizeof(h), cudaMemcpyDeviceToHost);
+    cudaFree(psi);
+    cudaFree(st);
+    if (e != cudaSuccess) { cudaGetLastError(); return cuda_fail(e, "spectra check"); }
+    std::memcpy(&p->tightness, &h[0], sizeof(double));
+    std::memcpy(&p->asymmetry, &h[1], sizeof(double));
+  }
+  *tightness = p->tightness;
+  *asymmetry = p->asymmetry;
   return FFST_OK;
 }
 

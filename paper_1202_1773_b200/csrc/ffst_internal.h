@@ -76,10 +76,22 @@ struct KParams {
   int* ctr;                     // [0] dispatch; [ctr_p1 + c]; [ctr_p2 + c]; [ctr_g + item]
   int ctr_p1, ctr_p2, ctr_g;
   int fetch_batch;              // warp path: consecutive items a CTA takes per global fetch
-  int variant;                  // 0 classic (meyerShearletSpect), 1 smooth (meyerNewShearletSpect)
+  int variant;                  // 0 classic (meyerShearletSpect), 1 smooth (meyerNewShearletSpect), 2 user
+  const void* usym;             // user spectra: [eta_l][n/2+1][n] T symmetric parts (ffst_user.cuh), else nullptr
   int compact;                  // f1 compact format: cube of reals + Nyquist vectors (G, H) in nyq_fwd
   int dbg;                      // measurement only (FFST_DBG): bit 0 skip FFTs, bit 1 skip output stores
   unsigned long long* trace;    // optional: per item {smid, t_start, t_ready, t_end} (globaltimer ns)
+};
+
+// Plan-time preparation of user-supplied spectra (ffst_user.cuh).
+struct UserPrep {
+  const void* psi;          // [eta][n][n] T, device (the caller's; read only here)
+  int n, eta, centred;
+  int shard_rank, shard_count, eta_l;
+  void* usym;               // [eta_l][n/2+1][n] T (out)
+  int* hull;                // [eta_l][2] column lo / hi where sym != 0 (in: n/2+1 / -1)
+  void* anti;               // [eta_l][2][n] T (out): anti part on the Nyquist row (0) / column (1)
+  unsigned long long* stats;   // [2] bit patterns of two non-negative doubles (in: 0): tightness, asymmetry
 };
 
 // Launch geometry of one (T, N) instantiation (host + device visible).
@@ -108,6 +120,7 @@ template <typename T> cudaError_t launch_inv_main(const KParams& p, int grid, cu
 template <typename T> cudaError_t launch_nyq_inv(const KParams& p, int batch, cudaStream_t s);
 template <typename T> cudaError_t launch_nyq_compact_sums(const KParams& p, int batch, cudaStream_t s);
 template <typename T> cudaError_t launch_final(const KParams& p, int batch, int which, cudaStream_t s);
+template <typename T> cudaError_t launch_user_prepare(const UserPrep& u, int grid, cudaStream_t s);
 template <typename T> cudaError_t launch_spectra_export(const KParams& p, void* psi, int centred, cudaStream_t s);
 template <typename T> int max_active_main(int n, int device, int which);   // CTAs/SM of fwd (0) / inv (1)
 

@@ -136,12 +136,35 @@ __device__ __forceinline__ void red_relaxed(int* ctr, int v) {
   asm volatile("red.relaxed.gpu.global.add.s32 [%0], %1;" ::"l"(ctr), "r"(v) : "memory");
 }
 
+// Predicated cached loads (__ldg / __ldcg / __ldcs are non-volatile inline asm): the compiler may
+// hoist them above the guarding branch, so every such load's address is kept inside its buffer
+// even for idle lanes (clamped row / column indices).  Observed with cuda-gdb: a hoisted __ldg of
+// the user-spectra table through a null pointer (illegal address, n = 16, 32).
+//
+// Candidate-list entries live in the FFT scratch (complex-typed) of the warp's own lines; they
+// are stored and loaded with asm volatile + "memory" clobber so that no type-based alias analysis
+// can move the FFT's scratch accesses across them.
+__device__ __forceinline__ void sts_u16(unsigned short* a, unsigned short v) {
+  asm volatile("st.shared.u16 [%0], %1;" ::"r"((unsigned)__cvta_generic_to_shared(a)), "h"(v) : "memory");
+}
+__device__ __forceinline__ unsigned short lds_u16(const unsigned short* a) {
+  unsigned short v;
+  asm volatile("ld.shared.u16 %0, [%1];" : "=h"(v) : "r"((unsigned)__cvta_generic_to_shared(a)) : "memory");
+  return v;
+}
+
 // the plan's radial tables (classic rows; smooth rows after them when p.variant == 1)
 template <typename T, int N>
 __device__ __forceinline__ Radial<T> radial_of(const KParams& p) {
   Radial<T> R{static_cast<const T*>(p.rtab), N / 2 + 1, p.j0};
   if (p.variant == 1) R.smooth = static_cast<const T*>(p.rtab) + (size_t)(p.j0 + 1) * (N / 2 + 1);
   return R;
+}
+
+// user spectra (f4): the plane's [n/2+1][n] table of symmetric parts, else nullptr
+template <typename T, int N>
+__device__ __forceinline__ const T* user_plane(const KParams& p, const PlaneDev& P) {
+  return p.usym ? static_cast<const T*>(p.usym) + (size_t)P.rec * (N / 2 + 1) * N : nullptr;
 }
 
 template <typename T, int N>
@@ -160,9 +183,15 @@ struct K {
   // The lists live in the FFT scratch of the warp's own line(s) (used only by that warp's FFT,
   // after this call; lines longer than a warp are separated by a CTA barrier at the end).
   static __device__ __forceinline__ void window_lines(const PlaneDev& P, int cb0, bool act, T* wbuf, C* scr,
-                                                      const Radial<T>& R, T delta) {
+                                                      const Radial<T>& R, T delta, const T* us) {
     const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5, t = tid % G::THC;
     const int cb = cb0 + tid / G::THC;
+    if (us != nullptr) {   // user spectra (f4): the plane's symmetric part from its table, every row
+#pragma unroll
+      for (int q = 0; q < G::EC; ++q) wbuf[q * NT + tid] = act ? us[(size_t)cb * N + t + q * G::THC] : T(0);
+      SyncOf<G::THC>::sync();
+      return;
+    }
     const int u1 = cb == H ? -H : cb;
     const int w0 = warp * 32;    // first thread of the warp
     unsigned short* wl = reinterpret_cast<unsigned short*>(scr + (w0 / G::THC) * G::SMC) +
@@ -176,13 +205,13 @@ struct K {
       const bool cand = act && (cb == H || rb == H || col_candidate(bnd, centred(rb, N)));
       wbuf[q * NT + tid] = T(0);
       const unsigned m = __ballot_sync(0xffffffffu, cand);
-      if (cand) wl[count + __popc(m & ((1u << lane) - 1u))] = (unsigned short)((q << 5) | lane);
+      if (cand) sts_u16(wl + count + __popc(m & ((1u << lane) - 1u)), (unsigned short)((q << 5) | lane));
       count += __popc(m);
     }
     __syncwarp();
 #pragma unroll 1
     for (int k = lane; k < count; k += 32) {
-      const int e = wl[k];
+      const int e = lds_u16(wl + k);
       const int q = e >> 5, tid2 = warp * 32 + (e & 31);
       const int cb2 = cb0 + tid2 / G::THC, rb2 = tid2 % G::THC + q * G::THC;
       wbuf[q * NT + tid2] = window_sym<T>(P, cb2 == H ? -H : cb2, centred(rb2, N), H, R);
@@ -211,11 +240,11 @@ struct K {
       const bool act = ci < cnt;
       const int cb = c0 + ci;
       const int u1 = cb == H ? -H : cb;
-      const C* col = src + (size_t)cb * N;
+      const C* col = src + (size_t)(act ? cb : c0) * N;   // in range even for idle lines (hoisted loads)
       C r[G::EC];
       if constexpr (MODE == MODE_MAIN) {
         T* wbuf = reinterpret_cast<T*>(tile + G::TILE_C);
-        window_lines(P, c0 + rd * G::LPC, act, wbuf, scr, R, delta);
+        window_lines(P, c0 + rd * G::LPC, act, wbuf, scr, R, delta, user_plane<T, N>(p, P));
         if (rd == 0) FFST_PROBE(p, 0);
 #pragma unroll
         for (int q = 0; q < G::EC; ++q) {
@@ -271,12 +300,12 @@ struct K {
     const int ci = line;
     const bool act = ci < cnt;
     const int cb = c0 + ci;
-    window_lines(P, c0, act, wbuf, scr, R, (T)p.delta);
+    window_lines(P, c0, act, wbuf, scr, R, (T)p.delta, user_plane<T, N>(p, P));
     FFST_PROBE(p, 0);
     const int ncopy = cnt < G::GC ? cnt : G::GC;
 #pragma unroll 1
     for (int img = 0; img < 2; ++img) {
-      const C* col = (img == 0 ? src0 : src1) + (size_t)cb * N;
+      const C* col = (img == 0 ? src0 : src1) + (size_t)(act ? cb : c0) * N;
       C r[G::EC];
 #pragma unroll
       for (int q = 0; q < G::EC; ++q) {
@@ -327,15 +356,16 @@ struct K {
     for (int rd = 0; rd < rounds; ++rd) {
       const int ri = rd * G::LPR + line;
       const bool act = ri < cnt;
-      const int r = r0 + ri;
+      const int r = r0 + (act ? ri : 0);
       const C* row = src + (size_t)r * stride - c_lo;
       C z[G::ER], zm[G::ER];
       // phase 1: issue every load of the round (no use in between: all in flight together)
 #pragma unroll
       for (int q = 0; q < G::ER; ++q) {
         const int k = t + q * G::THR, km = H - k;
-        z[q] = (act && k >= c_lo && k < c_lo + ncols) ? __ldcg(row + k) : czero<T>();
-        zm[q] = (act && km >= c_lo && km < c_lo + ncols) ? __ldcg(row + km) : czero<T>();
+        const bool ik = act && k >= c_lo && k < c_lo + ncols, ikm = act && km >= c_lo && km < c_lo + ncols;
+        z[q] = ik ? __ldcg(row + (ik ? k : c_lo)) : czero<T>();
+        zm[q] = ikm ? __ldcg(row + (ikm ? km : c_lo)) : czero<T>();
       }
       // phase 2: Hermitian pre-processing of the half-length C2R
 #pragma unroll
@@ -417,7 +447,7 @@ struct K {
 #pragma unroll
           for (int q = 0; q < G::ER; ++q) {
             if (act) {
-              load_pair_cs<T>(src_c + (size_t)r * N + 2 * (t + q * G::THR), va[q], vb[q]);
+              load_pair_cs<T>(src_c + (size_t)(act ? r : r0) * N + 2 * (t + q * G::THR), va[q], vb[q]);
             } else {
               va[q] = czero<T>();
               vb[q] = czero<T>();
@@ -436,7 +466,7 @@ struct K {
         } else {
 #pragma unroll
           for (int q = 0; q < G::ER; ++q)
-            z[q] = act ? *reinterpret_cast<const cpx<T>*>(src_r + (size_t)r * N + 2 * (t + q * G::THR)) : czero<T>();
+            z[q] = act ? *reinterpret_cast<const cpx<T>*>(src_r + (size_t)(act ? r : r0) * N + 2 * (t + q * G::THR)) : czero<T>();
         }
         if (ti == 0 && rd == 0) FFST_PROBE(p, 0);
         LineFFT<T, H, false, N>::run(z, scr + line * G::SMR, t, tw);
@@ -535,7 +565,7 @@ struct K {
     for (int rd = 0; rd * RPR < cnt; ++rd) {
       const int ri = rd * RPR + 2 * line;
       const bool act = ri < cnt;
-      const int ra = r0 + ri;
+      const int ra = r0 + (act ? ri : 0);
       const C* wa = src + (size_t)ra * stride - c_lo;
       const C* wb = wa + stride;
       C z[G::EC];
@@ -546,8 +576,9 @@ struct K {
         const int k = up ? N - c : c;
         C a = czero<T>(), b = czero<T>();
         if (act && (unsigned)(k - c_lo) < nc) {
-          a = __ldcg(wa + k);
-          b = __ldcg(wb + k);
+          const int kk = (unsigned)(k - c_lo) < nc ? k : c_lo;   // in range even if hoisted
+          a = __ldcg(wa + kk);
+          b = __ldcg(wb + kk);
         }
         z[q] = up ? mk<T>(a.x + b.y, b.x - a.y) : mk<T>(a.x - b.y, a.y + b.x);
       }
@@ -609,7 +640,7 @@ struct K {
       for (int rd = 0; rd < ROUNDS; ++rd) {
         const int ri = rd * RPR + 2 * line;              // first row of the pair inside the tile
         const bool act = ri < G::GR && ti * G::GR + ri < cnt;
-        const int ra = rt0 + ri;
+        const int ra = act ? rt0 + ri : r0;
         const C* rowa = src_c + (size_t)ra * N;
         const C* rowb = rowa + N;
         C z[G::EC];
@@ -753,11 +784,11 @@ struct K {
       woff += N * P.ncols_pad;
       if (g1 <= P.c_lo || g0 >= P.c_lo + P.ncols) continue;          // CTA-uniform
       const bool in = act && cb >= P.c_lo && cb < P.c_lo + P.ncols;
-      const C* col = slot + cur + (size_t)(cb - P.c_lo) * N;
+      const C* col = slot + cur + (size_t)(in ? cb - P.c_lo : 0) * N;
       C r[G::EC];
 #pragma unroll
       for (int q = 0; q < G::EC; ++q) r[q] = in ? __ldcg(col + t + q * G::THC) : czero<T>();
-      window_lines(P, g0, in, wbuf, scr, R, delta);
+      window_lines(P, g0, in, wbuf, scr, R, delta, user_plane<T, N>(p, P));
       LineFFT<T, N, false, N>::run(r, scr + line * G::SMC, t, tw);
       if (in) {
 #pragma unroll
@@ -1204,7 +1235,23 @@ __global__ void spectra_kernel(KParams p, T* psi, int centred_layout) {
       u1 = centred(col, N);
       u2 = centred(row, N);
     }
-    psi[e] = window<T>(p.planes[i], u1, u2, R);
+    const PlaneDev& P = p.planes[i];
+    if (p.usym) {
+      // user spectra: sym(u) = sym(-u mod n) from the Hermitian-half table, plus the anti part
+      // on the Nyquist row / column
+      constexpr int H = N / 2;
+      int a1 = u1, a2 = u2;
+      if (u1 < 0 && u1 != -H) { a1 = -u1; a2 = u2 == -H ? -H : -u2; }
+      T v = user_plane<T, N>(p, P)[(size_t)(a1 == -H ? H : a1) * N + (a2 < 0 ? a2 + N : a2)];
+      if (P.nyq >= 0) {
+        const T* an = static_cast<const T*>(p.nyq_anti) + (size_t)P.nyq * 2 * N;
+        if (u2 == -H) v += an[u1 < 0 ? u1 + N : u1];
+        if (u1 == -H) v += an[N + (u2 < 0 ? u2 + N : u2)];
+      }
+      psi[e] = v;
+    } else {
+      psi[e] = window<T>(P, u1, u2, R);
+    }
   }
 }
 

@@ -1,6 +1,7 @@
 // ffst_launch.cuh — host launchers: runtime n -> compile-time N dispatch.
 #pragma once
 #include "ffst_warp.cuh"
+#include "ffst_user.cuh"
 
 namespace ffst {
 
@@ -173,6 +174,8 @@ template <typename T, int N> struct Launch {
     FFST_DISPATCH(T, p.n, final_(p, b, which, s), cudaErrorInvalidValue) }                                            \
   template <> cudaError_t launch_spectra_export<T>(const KParams& p, void* psi, int c, cudaStream_t s) {       \
     FFST_DISPATCH(T, p.n, spectra(p, psi, c, s), cudaErrorInvalidValue) }                                      \
+  template <> cudaError_t launch_user_prepare<T>(const UserPrep& u, int grid, cudaStream_t s) {              \
+    return user_prepare_<T>(u, grid, s); }                                                                     \
   template <> int max_active_main<T>(int n, int device, int which) {                                           \
     (void)device; FFST_DISPATCH(T, n, max_active(which), 0) }
 

@@ -93,7 +93,8 @@ struct PlaneDev {
   int c_lo, ncols;   // Hermitian-half column range [c_lo, c_lo + ncols), columns 0..n/2
   int ncols_pad;     // row stride of the forward intermediate
   int nyq;           // index among the plan's Nyquist planes, or -1
-  int rec;           // warp path: index of the plane's first column record (ColRec), column c_lo
+  int rec;           // warp path: index of the plane's first column record (ColRec), column c_lo;
+                     // user spectra (CTA path only): local plane index (block of the table)
 };
 
 // Per-column plan record (warp path): hull of the rows where sym_i can be non-zero in this column,

@@ -169,7 +169,9 @@ struct WK {
   };
   static __device__ __forceinline__ ColRec<T> col_rec(const KParams& p, const PlaneDev& P, int cb) {
     ColRec<T> r;
-    const ColRec<T>* src = static_cast<const ColRec<T>*>(p.colrec) + P.rec + (cb - P.c_lo);
+    // (clamped: callers may evaluate this for idle columns and the loads may be hoisted)
+    const int cc = cb < P.c_lo ? 0 : (cb >= P.c_lo + P.ncols ? P.ncols - 1 : cb - P.c_lo);
+    const ColRec<T>* src = static_cast<const ColRec<T>*>(p.colrec) + P.rec + cc;
 #pragma unroll
     for (int i = 0; i < 3; ++i) {
       r.lo[i] = __ldg(&src->lo[i]);

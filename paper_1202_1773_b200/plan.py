@@ -16,7 +16,7 @@ from ._lib import PlanDesc, check, lib
 KIND_NAMES = {0: "lowpass", 1: "h", 2: "v", 3: "x"}
 _DTYPES = {torch.float32: 0, torch.float64: 1}
 _CDTYPES = {torch.float32: torch.complex64, torch.float64: torch.complex128}
-_VARIANTS = {"classic": 0, "smooth": 1}
+_VARIANTS = {"classic": 0, "smooth": 1, "user": 2}
 
 
 def scales_for_size(n: int) -> int:
@@ -70,7 +70,8 @@ class Plan:
     i % shard_count == shard_rank (eta-sharding, DESIGN.md "Multi-GPU")."""
 
     def __init__(self, n: int, batch: int = 1, dtype=torch.float32, device=None, j0: int = 0,
-                 shard_rank: int = 0, shard_count: int = 1, variant: str = "classic"):
+                 shard_rank: int = 0, shard_count: int = 1, variant: str = "classic",
+                 spectra=None, centred: bool = True):
         if not torch.cuda.is_available():
             raise RuntimeError("FFST Plan needs a CUDA device (no CPU fallback)")
         if dtype not in _DTYPES:
@@ -79,7 +80,9 @@ class Plan:
                                    torch.device(device).index or 0)
         self.dtype = dtype
         self.cdtype = _CDTYPES[dtype]
-        if variant not in _VARIANTS:
+        if spectra is not None:
+            variant = "user"
+        elif variant not in _VARIANTS or variant == "user":
             raise ValueError("variant must be 'classic' (meyerShearletSpect) or 'smooth' (meyerNewShearletSpect)")
         self.variant = variant
         desc = PlanDesc(int(n), int(j0), int(batch), _DTYPES[dtype], _VARIANTS[variant], self.device.index,
@@ -87,7 +90,18 @@ class Plan:
         handle = C.c_void_p()
         with torch.cuda.device(self.device):
             torch.cuda.init()
-            check(lib.ffst_plan_create(C.byref(handle), C.byref(desc)), "ffst_plan_create")
+            if spectra is None:
+                check(lib.ffst_plan_create(C.byref(handle), C.byref(desc)), "ffst_plan_create")
+            else:
+                # user-supplied spectra: eta real n x n planes, copied by the plan
+                if (not torch.is_tensor(spectra) or spectra.dtype != dtype or spectra.device != self.device
+                        or spectra.dim() != 3 or tuple(spectra.shape[1:]) != (n, n)):
+                    raise ValueError(f"spectra must be a {dtype} tensor (eta, {n}, {n}) on {self.device}")
+                spectra = spectra.contiguous()
+                torch.cuda.current_stream(self.device).synchronize()
+                check(lib.ffst_plan_create_user(C.byref(handle), C.byref(desc), int(spectra.shape[0]),
+                                                C.c_void_p(spectra.data_ptr()), int(bool(centred))),
+                      "ffst_plan_create_user")
         self._h = handle
         vals = [C.c_int() for _ in range(5)]
         check(lib.ffst_plan_info(self._h, *[C.byref(v) for v in vals]), "ffst_plan_info")
@@ -164,6 +178,13 @@ class Plan:
         return out_host
 
     # -------------------------------------------------------------- compact format (f1)
+    def spectra_check(self):
+        """(tightness, asymmetry): max |sum_i psi_i^2 - 1| over the grid (the Parseval admission
+        check of P:L2219-2220) and max |psi_i(u) - psi_i(-u)| off the Nyquist lines."""
+        t, a = C.c_double(), C.c_double()
+        check(lib.ffst_plan_spectra_check(self._h, C.byref(t), C.byref(a)), "ffst_plan_spectra_check")
+        return t.value, a.value
+
     def nyquist_planes(self):
         """Local indices of the plan's Nyquist planes (the order of the compact format's G, H)."""
         cnt = C.c_int()

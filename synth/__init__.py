@@ -19,7 +19,7 @@ from dataclasses import dataclass
 import numpy as np
 
 __all__ = ["Config", "CONFIGS", "config", "make_image", "make_batch",
-           "uniform_image", "random_cube", "vertical_line_image"]
+           "uniform_image", "random_cube", "vertical_line_image", "random_spectra"]
 
 
 @dataclass(frozen=True)
@@ -182,3 +182,35 @@ def random_cube(shape, seed: int) -> np.ndarray:
     """Random complex array (real and imaginary parts N(0,1)) for adjoint tests."""
     rng = np.random.Generator(np.random.PCG64(seed))
     return rng.standard_normal(shape) + 1j * rng.standard_normal(shape)
+
+
+def random_spectra(n: int, eta: int, seed: int, parseval: bool = True) -> np.ndarray:
+    """A random user spectra set (eta, n, n), centred layout (omega = 0 at (n/2, n/2)), for the
+    user-spectra mode.  Input construction only, not the shearlet method:
+      * plane 0 is a random positive "low-pass" on every grid point (so every point is covered);
+      * planes 1.. are random non-negative bumps on a random band of columns |u1| in [lo, hi]
+        (exercises the per-plane column pruning), zero elsewhere;
+      * every plane is point-symmetric, g(u) = g(-u), off the Nyquist lines; on the row
+        u2 = -n/2 and the column u1 = -n/2 the values at u and -u are drawn independently
+        (asymmetric: the anti parts the even-n decomposition handles exactly);
+      * parseval=True divides all planes by sqrt(sum_i g_i^2) pointwise, so sum_i psi_i^2 = 1.
+    """
+    rng = np.random.Generator(np.random.PCG64(seed))
+    h = n // 2
+    u = np.arange(n) - h                                   # centred coordinates
+    u1, u2 = np.meshgrid(u, u)                             # columns omega_1, rows omega_2
+    neg = (n - np.arange(n)) % n                           # index of -u (with -(-n/2) = -n/2)
+    g = np.zeros((eta, n, n))
+    for i in range(eta):
+        r = rng.uniform(0.05, 1.0, (n, n))
+        if i > 0:
+            lo = int(rng.integers(0, h + 1))
+            hi = int(rng.integers(lo, h + 1))
+            r = r * ((np.abs(u1) >= lo) & (np.abs(u1) <= hi))
+            r = r * (rng.uniform(0, 1, (n, n)) < 0.7)
+        sym = 0.5 * (r + r[neg][:, neg])                   # point-symmetric copy
+        nyq = (u1 == -h) | (u2 == -h)
+        g[i] = np.where(nyq, r, sym)
+    if parseval:
+        g = g / np.sqrt(np.sum(g * g, axis=0))
+    return g

@@ -425,3 +425,100 @@ def test_smooth_compact_format(F, n, dtype, batch):
     assert float(((ce - c).abs() / scale).max()) <= tol
     r_compact = plan.inverse_compact(re, gh)
     assert plane_err(r_compact.cpu().numpy(), xo).max() <= TOL[dtype]
+
+
+# ------------------------------------------------------------------ user-supplied spectra
+
+def _user_plan(F, psi, batch, dtype, centred=True, **kw):
+    t = torch.from_numpy(psi).to(dtype).cuda()
+    if not centred:
+        t = torch.fft.ifftshift(t, dim=(-2, -1)).contiguous()
+    return F.Plan(psi.shape[-1], batch, dtype, spectra=t, centred=centred, **kw), t
+
+
+@pytest.mark.parametrize("n,dtype", [(16, torch.float64), (64, torch.float64), (256, torch.float32)])
+def test_user_spectra_builtin_system(F, n, dtype):
+    # the built-in spectra passed in as precomputed Psi reproduce the built-in plan
+    psi = O.shearlet_spectra(n)
+    batch = 3
+    x, xo = images(2, batch, n, dtype)
+    plan_u, _ = _user_plan(F, psi, batch, dtype)
+    plan_b = F.Plan(n, batch, dtype)
+    assert plan_u.eta == plan_b.eta and plan_u.variant == "user"
+    cu = plan_u.forward(x.cuda())
+    cb = plan_b.forward(x.cuda())
+    scale = cb.abs().amax(dim=(2, 3), keepdim=True).clamp_min(1e-30)
+    tol = 1e-5 if dtype == torch.float32 else 1e-12
+    assert float(((cu - cb).abs() / scale).max()) <= tol
+    ru = plan_u.inverse(cu)
+    assert plane_err(ru.cpu().numpy(), xo).max() <= TOL[dtype]
+    # export reproduces the input and the admission numbers are those of a Parseval frame
+    got = plan_u.spectra(centred=True).cpu().double().numpy()
+    # (exact off the Nyquist lines; sym + anti there re-rounds)
+    assert np.max(np.abs(got - psi.astype(np.float32 if dtype == torch.float32 else np.float64))) <= (
+        1e-7 if dtype == torch.float32 else 1e-15)
+    t, a = plan_u.spectra_check()
+    assert t < (1e-5 if dtype == torch.float32 else 1e-13) and a <= (1e-6 if dtype == torch.float32 else 1e-14)
+
+
+@pytest.mark.parametrize("n,eta,dtype,batch,centred", [(4, 3, torch.float64, 2, True), (16, 7, torch.float64, 3, True),
+                                                       (64, 13, torch.float64, 2, False), (256, 29, torch.float32, 4, True),
+                                                       (512, 9, torch.float32, 2, False)])
+def test_user_spectra_random_system(F, n, eta, dtype, batch, centred):
+    # a random Parseval system with pruned column bands and asymmetric Nyquist lines
+    psi = synth.random_spectra(n, eta, 100 + n)
+    x, xo = images(2, batch, n, dtype)
+    plan, t = _user_plan(F, psi, batch, dtype, centred=centred)
+    assert plan.eta == eta
+    psi_o = psi.astype(np.float32).astype(np.float64) if dtype == torch.float32 else psi
+    c = plan.forward(x.cuda())
+    rec = plan.inverse(c).cpu().numpy()
+    c = c.cpu().numpy()
+    for b in range(batch):
+        ref = O.forward(xo[b], psi=psi_o)
+        assert plane_err(c[b], ref, np.max(np.abs(xo[b]))).max() <= TOL[dtype], b
+        ref_inv = O.inverse(c[b].astype(np.complex128), psi=psi_o).real
+        assert plane_err(rec[b], ref_inv).max() <= TOL[dtype]
+        assert plane_err(rec[b], xo[b]).max() <= TOL[dtype]
+    got = plan.spectra(centred=True).cpu().double().numpy()
+    assert np.max(np.abs(got - psi_o)) <= (1e-7 if dtype == torch.float32 else 1e-15)
+    tight, asym = plan.spectra_check()
+    assert tight <= (1e-5 if dtype == torch.float32 else 1e-13) and asym == 0.0
+
+
+def test_user_spectra_non_parseval_and_sharded(F):
+    # a non-tight system runs (the check is reported, not enforced); shards sum to the full adjoint
+    n, eta = 64, 11
+    psi = synth.random_spectra(n, eta, 7, parseval=False)
+    x, xo = images(2, 2, n, torch.float64)
+    full, _ = _user_plan(F, psi, 2, torch.float64)
+    tight, _ = full.spectra_check()
+    assert abs(tight - O.frame_tightness(psi)) < 1e-12
+    c = full.forward(x.cuda())
+    ref = O.forward(xo[0], psi=psi)
+    assert plane_err(c[0].cpu().numpy(), ref, np.max(np.abs(xo[0]))).max() <= 1e-10
+    r_full = full.inverse(c)
+    acc = torch.zeros_like(r_full)
+    for rank in range(3):
+        sh, _ = _user_plan(F, psi, 2, torch.float64, shard_rank=rank, shard_count=3)
+        assert sh.local_planes == list(range(rank, eta, 3))
+        acc += sh.inverse(c[:, sh.local_planes].contiguous())
+    assert float((acc - r_full).abs().max() / r_full.abs().max()) <= 1e-12
+
+
+def test_user_spectra_rejections(F):
+    n = 32
+    psi = synth.random_spectra(n, 5, 3)
+    bad = psi.copy()
+    bad[1, 5, 7] += 0.1                      # interior asymmetry
+    with pytest.raises(F.FFSTError):
+        _user_plan(F, bad, 1, torch.float64)
+    with pytest.raises(ValueError):
+        F.Plan(n, 1, torch.float64, spectra=torch.zeros(5, n, n, dtype=torch.float32, device="cuda"))
+
+
+def test_builtin_spectra_check(F):
+    for variant in ("classic", "smooth"):
+        plan = F.Plan(128, 1, torch.float64, variant=variant)
+        tight, asym = plan.spectra_check()
+        assert tight < 1e-13 and asym < 1e-15

@@ -458,3 +458,39 @@ def test_smooth_round_trip_and_parseval(n):
 def test_unknown_variant_rejected():
     with pytest.raises(ValueError):
         O.shearlet_spectrum(16, 2, variant="bogus")
+
+
+# ---------------------------------------------------------------- user-supplied spectra
+
+def test_frame_tightness_check():
+    # sum(abs(Psi).^2,3) - 1 is ~0 for a Parseval system (the built-in one: the
+    # paper's Fig. frameTightness level) and exactly 3 when every spectrum is doubled.
+    psi = O.shearlet_spectra(32)
+    assert O.frame_tightness(psi) < 1e-13
+    assert abs(O.frame_tightness(2.0 * psi) - 3.0) < 1e-12
+    assert O.frame_tightness(synth.random_spectra(16, 5, 1)) < 1e-14
+    assert O.frame_tightness(synth.random_spectra(16, 5, 1, parseval=False)) > 1e-2
+
+
+@pytest.mark.parametrize("n,eta", [(8, 3), (16, 7)])
+def test_user_spectra_parseval_and_brute_force(n, eta):
+    # The transform with precomputed spectra: for any Parseval system the adjoint
+    # inverts it (P:L1730-1764 with sum_i psi_i^2 = 1) and energy is kept; and one coefficient of
+    # one plane against the double sum of its definition (eq:shearletTransform written out,
+    # brute force: c_i(x) = 1/N^2 sum_w psi_i(w) f_hat(w) e^{+2 pi i <w, x>/N}).
+    psi = synth.random_spectra(n, eta, 11)
+    f = synth.uniform_image(n, 5)
+    c = O.forward(f, psi=psi)
+    assert abs(np.sum(np.abs(c) ** 2) - np.sum(f**2)) < 1e-12 * np.sum(f**2)
+    rec = O.inverse(c, psi=psi)
+    assert np.max(np.abs(rec - f)) < 1e-12 * np.max(np.abs(f))
+    h = n // 2
+    u = np.arange(n) - h
+    x = np.arange(n) - h
+    fh = np.array([[sum(f[r, m] * np.exp(-2j * np.pi * (a1 * (m - h) + a2 * (r - h)) / n)
+                        for r in range(n) for m in range(n)) for a1 in u] for a2 in u])
+    for i in (0, eta - 1):
+        for (r, m) in ((0, 0), (3, n - 1), (h, 1)):
+            val = sum(psi[i, p, q] * fh[p, q] * np.exp(2j * np.pi * (u[q] * x[m] + u[p] * x[r]) / n)
+                      for p in range(n) for q in range(n)) / n**2
+            assert abs(val - c[i, r, m]) < 1e-12, (i, r, m)
