@@ -1041,17 +1041,22 @@ static ffst_status plan_create_impl(ffst_plan** out, const ffst_plan_desc* d_in,
   const char* env = std::getenv("FFST_SLOT_KB");
   const long long budget_bytes = (env ? std::atoll(env) : 4096) * 1024LL;
   p->slot_budget = std::max(maxplane, budget_bytes / (long long)csz);
-  const char* envc = std::getenv("FFST_CHUNK_PLANES");
-  // planes per chunk: 4 (pipelining granularity); small batches use long chunks so the inverse's
-  // per-image accumulation chain (one link per chunk) stays short (config 1: 0.24 -> 0.16 ms)
-  p->chunk_planes = std::max(1, envc ? std::atoi(envc) : (d->batch <= 4 ? 32 : 4));
   {
-    // accumulator lanes: up to 4 while the lanes of A stay L2-sized (<= 32 MB); above that the
+    // accumulator lanes: as many as keep the lanes of A L2-sized (<= 32 MB), at most 4 (16 for
+    // batch <= 4, where the inverse's pass 2 has few column groups to spread); above 32 MB the
     // final pass's extra reads would go to HBM (configs 3-5: one lane)
     const long long a_bytes = (long long)d->batch * (d->n / 2 + 1) * d->n * 2 * (long long)p->rsz;
-    p->acc_lanes = (int)std::max(1LL, std::min(4LL, (32LL << 20) / std::max(1LL, a_bytes)));
+    const long long cap = d->batch <= 4 ? 16 : 4;
+    p->acc_lanes = (int)std::max(1LL, std::min(cap, (32LL << 20) / std::max(1LL, a_bytes)));
     if (const char* el = std::getenv("FFST_ACC_LANES")) p->acc_lanes = std::max(1, std::min(16, std::atoi(el)));
   }
+  // planes per chunk: 4 (pipelining granularity).  Small batches: one chunk per accumulator lane
+  // (the lanes' pass-2 items then run side by side instead of one item walking every plane:
+  // config 1 inverse 0.166 -> 0.037 ms); with a single lane, long chunks keep the accumulation
+  // chain (one link per chunk) short.
+  const char* envc = std::getenv("FFST_CHUNK_PLANES");
+  const int small_chunk = p->acc_lanes >= 2 ? std::max(2, (p->eta_l + p->acc_lanes - 1) / p->acc_lanes) : 32;
+  p->chunk_planes = std::max(1, envc ? std::atoi(envc) : (d->batch <= 4 ? small_chunk : 4));
   const long long slot_max = std::min(image_total, std::max(maxplane, p->slot_budget)) + 64;
   const char* envr = std::getenv("FFST_RING_MB");
   const long long ring_bytes = (envr ? std::atoll(envr) : 80) * 1024LL * 1024LL;
