@@ -306,29 +306,78 @@ def run_gpu(args, cfg):
     else:
         rt_err = None
 
-    plan.set_timing(True)
+    # one GPU: the step (forward + inverse, every kernel of the path) is captured once in a CUDA
+    # graph and replayed -- the same launches without the per-launch CPU overhead, which is what
+    # bounds the small configurations.  --no-graph (or a failed capture) times eager launches.
+    graph, graph_note = None, "off"
+    if world == 1 and not args.no_graph:
+        try:
+            side = torch.cuda.Stream(dev)
+            side.wait_stream(stream)
+            with torch.cuda.stream(side):
+                step()
+            stream.wait_stream(side)
+            torch.cuda.synchronize(dev)
+            graph = torch.cuda.CUDAGraph()
+            with torch.cuda.graph(graph, capture_error_mode="thread_local"):
+                step()
+            torch.cuda.synchronize(dev)
+            graph.replay()
+            torch.cuda.synchronize(dev)
+            graph_note = "replayed CUDA graph of the whole step"
+        except Exception as exc:                           # capture unsupported: eager launches
+            graph, graph_note = None, f"eager (capture failed: {type(exc).__name__})"
+            torch.cuda.synchronize(dev)
+
     ev = [(torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)) for _ in range(args.steps)]
     fwd_main, inv_main, fwd_tot, inv_tot = [], [], [], []
     launches = (0, 0)
-    if world > 1:
-        dist.barrier()
-    torch.cuda.synchronize(dev)
-    with ClockSampler(local) as clk:
-        for k in range(args.steps):
-            flush.zero_()                                  # L2 flush between timed steps (untimed)
-            ev[k][0].record(stream)
+
+    def phase_pass():
+        # per-kernel durations from the library's own events (eager launches, same kernels)
+        plan.set_timing(True)
+        for _ in range(args.steps):
+            flush.zero_()
             step()
-            ev[k][1].record(stream)
             torch.cuda.synchronize(dev)
-            (tf, ti, tft, tit), launches = plan.phase_times()
+            (tf, ti, tft, tit), ln = plan.phase_times()
             fwd_main.append(tf)
             inv_main.append(ti)
             fwd_tot.append(tft)
             inv_tot.append(tit)
+        plan.set_timing(False)
+        return ln
+
+    if world > 1:
+        dist.barrier()
+    torch.cuda.synchronize(dev)
+    if graph is None:
+        plan.set_timing(True)
+    with ClockSampler(local) as clk:
+        for k in range(args.steps):
+            flush.zero_()                                  # L2 flush between timed steps (untimed)
+            ev[k][0].record(stream)
+            if graph is not None:
+                graph.replay()
+            else:
+                step()
+            ev[k][1].record(stream)
+            torch.cuda.synchronize(dev)
+            if graph is None:
+                (tf, ti, tft, tit), launches = plan.phase_times()
+                fwd_main.append(tf)
+                inv_main.append(ti)
+                fwd_tot.append(tft)
+                inv_tot.append(tit)
         if world > 1:
             dist.barrier()
         torch.cuda.synchronize(dev)
-    plan.set_timing(False)
+    # the timed steps' own result (graph replays included) against the input
+    rt_after = float((rec - x).abs().max() / x.abs().max()) if rank == 0 else None
+    if graph is None:
+        plan.set_timing(False)
+    else:
+        launches = phase_pass()
     total_ms = sum(a.elapsed_time(b) for a, b in ev)
     if world > 1:
         t = torch.tensor([total_ms], device=dev, dtype=torch.float64)
@@ -431,7 +480,8 @@ def run_gpu(args, cfg):
             "dtype": "f32" if dtype == torch.float32 else "f64", "data": "synthetic",
             "config": {"workload": f"config{cfg.cid}", "label": cfg.label, "n": N, "global_batch": B,
                        "j0": plan.j0, "eta": eta, "parallelism": f"eta-shard{world}" if world > 1 else "single",
-                       "l2": "flushed between timed steps (512 MiB write, untimed)"},
+                       "l2": "flushed between timed steps (512 MiB write, untimed)",
+                       "launch": graph_note},
             "coeff_gbs": coeff_gbs,
             "hbm_frac_step": hbm_frac_step,
             "algorithmic_bytes_per_step": algo_bytes,
@@ -448,6 +498,7 @@ def run_gpu(args, cfg):
             "e2e": e2e,
             "gpu_launches": (launches[0] + launches[1]) * args.steps,
             "roundtrip_max_rel_err": rt_err,
+            "roundtrip_after_timed_steps": rt_after,
         }
         print(json.dumps(line), flush=True)
     if world > 1:
@@ -457,6 +508,7 @@ def run_gpu(args, cfg):
 
 def main():
     ap = argparse.ArgumentParser()
+    ap.add_argument("--no-graph", action="store_true", help="time eager launches instead of a replayed CUDA graph")
     ap.add_argument("--gpus", type=int, default=1)
     ap.add_argument("--steps", type=int, default=10)
     ap.add_argument("--warmup", type=int, default=3)
