@@ -40,6 +40,11 @@ struct Geo {
   static constexpr int GC = LPC > (32 / ESZ) ? LPC : (32 / ESZ);
   static constexpr int GCP = GC + 1;
   static constexpr int TILE_C = N * GCP;
+  // n >= 2048: an N x GC transposition tile would fill the SM's shared memory (one CTA per SM,
+  // 12 % warps active at n = 4096); forward pass 1 then stores each column straight from
+  // registers (8-byte stores whose sectors the item's GC columns complete in L2)
+  static constexpr bool DIRECT = (long long)N * GCP * ESZ > 65536;
+  static constexpr int TILE_CE = DIRECT ? 0 : TILE_C;     // tile elements allocated
   // forward pass 2 / final rows: rows per item (~128 KB of output)
   static constexpr int RP2_ = (131072 / (N * ESZ)) > LPR ? (131072 / (N * ESZ)) : LPR;
   static constexpr int RP2 = RP2_ < N ? RP2_ : N;
@@ -57,7 +62,7 @@ struct Geo {
   // arithmetic is not unrolled into the FFT's register footprint
   static constexpr int WBUF = NT * EC * (int)sizeof(T) / ESZ;      // in complex elements
   static constexpr int NYQB = (N + RP2) * (int)sizeof(T) / ESZ + 1;   // staged Nyquist terms (complex units)
-  static constexpr size_t SMEM_FWD = (size_t)((SCR_C + TILE_C + WBUF) > (SCRX + NYQB) ? (SCR_C + TILE_C + WBUF) : (SCRX + NYQB)) * ESZ;
+  static constexpr size_t SMEM_FWD = (size_t)((SCR_C + TILE_CE + WBUF) > (SCRX + NYQB) ? (SCR_C + TILE_CE + WBUF) : (SCRX + NYQB)) * ESZ;
   static constexpr size_t SMEM_INV = (size_t)((SCRX + TILE_R) > (SCR_C + WBUF) ? (SCRX + TILE_R) : (SCR_C + WBUF)) * ESZ + 256;
   static constexpr size_t SMEM_AUX = SMEM_FWD > SMEM_INV ? SMEM_FWD : SMEM_INV;
   static constexpr size_t SMEM_NYQ = (size_t)(SCR_C + NT * EC) * ESZ;
@@ -243,7 +248,7 @@ struct K {
       const C* col = src + (size_t)(act ? cb : c0) * N;   // in range even for idle lines (hoisted loads)
       C r[G::EC];
       if constexpr (MODE == MODE_MAIN) {
-        T* wbuf = reinterpret_cast<T*>(tile + G::TILE_C);
+        T* wbuf = reinterpret_cast<T*>(tile + G::TILE_CE);
         window_lines(P, c0 + rd * G::LPC, act, wbuf, scr, R, delta, user_plane<T, N>(p, P));
         if (rd == 0) FFST_PROBE(p, 0);
 #pragma unroll
@@ -264,22 +269,33 @@ struct K {
       if (rd == 0) FFST_PROBE(p, 1);
       LineFFT<T, N, true, N>::run(r, scr + line * G::SMC, t, tw);
       if (rd == 0) FFST_PROBE(p, 2);
-      if (ci < G::GC) {
+      if constexpr (G::DIRECT) {
+        if (rd == 0 && dep != nullptr) {       // ring-slot reuse: wait only before writing dst
+          if (tid == 0) spin_wait(dep, dep_target);
+          __syncthreads();
+        }
+        if (act) {
+#pragma unroll
+          for (int q = 0; q < G::EC; ++q) dst[(size_t)(t + q * G::THC) * dst_stride + dst_col0 + ci] = r[q];
+        }
+      } else if (ci < G::GC) {
 #pragma unroll
         for (int q = 0; q < G::EC; ++q) tile[(t + q * G::THC) * G::GCP + ci] = r[q];
       }
       __syncthreads();
     }
-    if (dep != nullptr) {                      // ring-slot reuse: wait only before writing dst
-      if (tid == 0) spin_wait(dep, dep_target);
-      __syncthreads();
-    }
-    const int ncopy = cnt < G::GC ? cnt : G::GC;
-    FFST_PROBE(p, 3);
+    if constexpr (!G::DIRECT) {
+      if (dep != nullptr) {                    // ring-slot reuse: wait only before writing dst
+        if (tid == 0) spin_wait(dep, dep_target);
+        __syncthreads();
+      }
+      const int ncopy = cnt < G::GC ? cnt : G::GC;
+      FFST_PROBE(p, 3);
 #pragma unroll 1
-    for (int e = tid; e < N * G::GC; e += NT) {
-      const int rr = e / G::GC, ci = e - rr * G::GC;
-      if (ci < ncopy) dst[(size_t)rr * dst_stride + dst_col0 + ci] = tile[rr * G::GCP + ci];
+      for (int e = tid; e < N * G::GC; e += NT) {
+        const int rr = e / G::GC, ci = e - rr * G::GC;
+        if (ci < ncopy) dst[(size_t)rr * dst_stride + dst_col0 + ci] = tile[rr * G::GCP + ci];
+      }
     }
   }
 
@@ -293,7 +309,7 @@ struct K {
     static_assert(G::GC == G::LPC || true, "");
     C* scr = smem;
     C* tile = smem + G::SCR_C;
-    T* wbuf = reinterpret_cast<T*>(tile + G::TILE_C);
+    T* wbuf = reinterpret_cast<T*>(tile + G::TILE_CE);
     const int tid = threadIdx.x, line = tid / G::THC, t = tid % G::THC;
     const C* tw = static_cast<const C*>(p.tw);
     const Radial<T> R = radial_of<T, N>(p);
@@ -313,20 +329,29 @@ struct K {
         r[q] = w != T(0) ? cscale<T>(__ldg(col + t + q * G::THC), w) : czero<T>();
       }
       LineFFT<T, N, true, N>::run(r, scr + line * G::SMC, t, tw);
-      if (ci < G::GC) {
-#pragma unroll
-        for (int q = 0; q < G::EC; ++q) tile[(t + q * G::THC) * G::GCP + ci] = r[q];
-      }
       const int* dep = img == 0 ? dep0 : dep1;
-      if (tid == 0 && dep != nullptr) spin_wait(dep, img == 0 ? tgt0 : tgt1);   // ring-slot reuse
-      __syncthreads();
       C* dst = img == 0 ? dst0 : dst1;
+      if constexpr (G::DIRECT) {
+        if (tid == 0 && dep != nullptr) spin_wait(dep, img == 0 ? tgt0 : tgt1);   // ring-slot reuse
+        __syncthreads();
+        if (act) {
+#pragma unroll
+          for (int q = 0; q < G::EC; ++q) dst[(size_t)(t + q * G::THC) * dst_stride + dst_col0 + ci] = r[q];
+        }
+      } else {
+        if (ci < G::GC) {
+#pragma unroll
+          for (int q = 0; q < G::EC; ++q) tile[(t + q * G::THC) * G::GCP + ci] = r[q];
+        }
+        if (tid == 0 && dep != nullptr) spin_wait(dep, img == 0 ? tgt0 : tgt1);   // ring-slot reuse
+        __syncthreads();
 #pragma unroll 1
-      for (int e = tid; e < N * G::GC; e += NT) {
-        const int rr = e / G::GC, c = e - rr * G::GC;
-        if (c < ncopy) dst[(size_t)rr * dst_stride + dst_col0 + c] = tile[rr * G::GCP + c];
+        for (int e = tid; e < N * G::GC; e += NT) {
+          const int rr = e / G::GC, c = e - rr * G::GC;
+          if (c < ncopy) dst[(size_t)rr * dst_stride + dst_col0 + c] = tile[rr * G::GCP + c];
+        }
       }
-      __syncthreads();                          // tile reuse by the second image
+      __syncthreads();                          // scratch / tile reuse by the second image
     }
   }
 
