@@ -963,7 +963,7 @@ __device__ __forceinline__ void persistent_loop(const KParams& p) {
     const int it = s_item[cur];
     if (it >= p.n_items) break;
     if (threadIdx.x == 0) s_item[cur ^ 1] = atomicAdd(p.ctr, 1);
-    const ItemDev I = load_item(p.items, it);
+    const ItemDev I = load_item(p.items, it < p.n_items ? it : p.n_items - 1);   // (hoist-safe index)
     unsigned long long t_start = 0, t_ready = 0;
     if (p.trace != nullptr && threadIdx.x == 0) t_start = gtimer();
     if (I.type == 1) {

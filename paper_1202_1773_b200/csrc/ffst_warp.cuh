@@ -523,7 +523,8 @@ struct WK {
     }
     const int cb = I.group * G::LPC + line;
     if (cb <= H) {
-      C* a = static_cast<C*>(p.A) + (size_t)I.pad1 * p.a_lane_elems + ((size_t)I.b * (H + 1) + cb) * N;
+      const int cbc = cb <= H ? cb : H;          // in range even if the loads below are hoisted
+      C* a = static_cast<C*>(p.A) + (size_t)I.pad1 * p.a_lane_elems + ((size_t)I.b * (H + 1) + cbc) * N;
 #pragma unroll
       for (int q = 0; q < G::EC; ++q) {
         const int idx = t + q * G::THC;
@@ -627,7 +628,8 @@ struct WarpLoop {
   };
   __device__ void load_item_to(int slot, int it) const {
     if (lane < 4)
-      reinterpret_cast<int4*>(islot + slot)[lane] = __ldg(reinterpret_cast<const int4*>(p.items + it) + lane);
+      reinterpret_cast<int4*>(islot + slot)[lane] =
+          __ldg(reinterpret_cast<const int4*>(p.items + (it < p.n_items ? it : p.n_items - 1)) + lane);
     __syncwarp();
   }
   __device__ void fetch_next(Next& nx) const {
