@@ -121,7 +121,7 @@ ffst_status ffst_plane_is_nyquist(int n, int j0, int index, int* is_nyquist);
  *   FFST_PATH=warp      warp-worker kernels for 8 <= n <= 512 (default: CTA-item kernels)
  *   FFST_RING_MB        intermediate ring budget (default 80; at least 12 slots)
  *   FFST_CHUNK_PLANES   planes per chunk (default 4; batch <= 4: eta / lanes, or 32 with one lane)
- *   FFST_SLOT_KB        chunk byte budget (default 4096)
+ *   FFST_SLOT_KB        chunk byte budget (default 4096; 12288 for n >= 1024)
  *   FFST_ACC_LANES      accumulator lanes of the inverse (default: up to 4, 16 for batch <= 4, while <= 32 MB)
  *   FFST_VERBOSE        print the queue geometry and the persistent grids
  *   FFST_CTAS_PER_SM    cap on resident CTAs per SM of the persistent kernels (default: occupancy)
