@@ -28,10 +28,10 @@ def _load_dist_module():
 class OracleShard:
     """Per-rank stand-in: forward/inverse restricted to the owned planes (float64)."""
 
-    def __init__(self, n, planes):
+    def __init__(self, n, planes, variant="classic"):
         self.n = n
         self.local_planes = planes
-        self.psi = O.shearlet_spectra(n)
+        self.psi = O.shearlet_spectra(n, variant=variant)
 
     def forward(self, x):
         out = []
@@ -45,14 +45,14 @@ class OracleShard:
         return torch.from_numpy(np.stack(out))
 
 
-def _worker(rank, world, port, n, batch, result_q):
+def _worker(rank, world, port, n, batch, result_q, variant="classic"):
     os.environ["MASTER_ADDR"] = "127.0.0.1"
     os.environ["MASTER_PORT"] = str(port)
     dist.init_process_group("gloo", rank=rank, world_size=world)
     D = _load_dist_module()
     eta = O.num_shearlets(O.scales_for_size(n))
     planes = D.owned_planes(eta, rank, world)
-    st = D.ShardedTransform(OracleShard(n, planes))
+    st = D.ShardedTransform(OracleShard(n, planes, variant))
     if rank == 0:
         x = torch.from_numpy(synth.make_batch(2, batch=batch, n=n))
     else:
@@ -65,13 +65,13 @@ def _worker(rank, world, port, n, batch, result_q):
     dist.destroy_process_group()
 
 
-@pytest.mark.parametrize("world", [2, 3])
-def test_sharded_roundtrip_gloo(world):
+@pytest.mark.parametrize("world,variant", [(2, "classic"), (3, "classic"), (2, "smooth")])
+def test_sharded_roundtrip_gloo(world, variant):
     n, batch = 32, 2
     ctx = mp.get_context("spawn")
     q = ctx.Queue()
-    port = 29500 + (os.getpid() % 1000) + world
-    procs = [ctx.Process(target=_worker, args=(r, world, port, n, batch, q)) for r in range(world)]
+    port = 29500 + (os.getpid() % 1000) + world + (10 if variant == "smooth" else 0)
+    procs = [ctx.Process(target=_worker, args=(r, world, port, n, batch, q, variant)) for r in range(world)]
     for p in procs:
         p.start()
     results = [q.get(timeout=300) for _ in range(world + 1)]
@@ -84,6 +84,6 @@ def test_sharded_roundtrip_gloo(world):
     eta = O.num_shearlets(O.scales_for_size(n))
     owned = sorted(i for s in shards for i in s[2])
     assert owned == list(range(eta))                          # every plane on exactly one rank
-    full = np.stack([O.forward(img) for img in rec[2]])
+    full = np.stack([O.forward(img, variant=variant) for img in rec[2]])
     for _, rank, planes, c in shards:                         # each rank's cube = its planes of the full cube
         assert np.max(np.abs(c - full[:, planes])) < 1e-12
