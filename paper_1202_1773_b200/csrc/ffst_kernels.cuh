@@ -259,7 +259,8 @@ struct K {
       } else {   // final pass: the accumulator lanes of A summed in lane order
 #pragma unroll
         for (int q = 0; q < G::EC; ++q) r[q] = act ? __ldcg(col + t + q * G::THC) : czero<T>();
-        for (int l = 1; l < p.a_lanes; ++l) {
+#pragma unroll 2
+        for (int l = 1; l < p.a_lanes; ++l) {      // (two lanes' loads in flight)
           const C* cl = col + (size_t)l * p.a_lane_elems;
 #pragma unroll
           for (int q = 0; q < G::EC; ++q)
@@ -1029,12 +1030,13 @@ __global__ void __launch_bounds__(256) spec_cols_kernel(KParams p) {
 
 // final pass 1: columns of A[b] -> Fscr[b] row-major (stride NCPF); grid (ceil((H+1)/GC), B)
 template <typename T, int N>
-__global__ void __launch_bounds__(256) fin_cols_kernel(KParams p) {
+__global__ void __launch_bounds__(256) fin_cols_kernel(KParams p, int cpb) {
   extern __shared__ __align__(128) unsigned char smem_raw[];
   using G = Geo<T, N>;
   const int b = blockIdx.y;
-  const int c0 = blockIdx.x * G::GC;
-  const int rem = N / 2 + 1 - c0;
+  const int c0 = blockIdx.x * cpb;              // cpb <= GC columns per CTA (fewer for small problems)
+  const int rem0 = N / 2 + 1 - c0;
+  const int rem = rem0 < cpb ? rem0 : cpb;
   const cpx<T>* src = static_cast<const cpx<T>*>(p.A) + (size_t)b * (N / 2 + 1) * N;
   cpx<T>* dst = static_cast<cpx<T>*>(p.Fscr) + (size_t)b * N * G::NCPF;
   PlaneDev dummy{};

@@ -106,7 +106,11 @@ template <typename T, int N> struct Launch {
   static cudaError_t final_(const KParams& p, int batch, int which, cudaStream_t s) {
     if (which == 0) {
       FFST_CHECK(set_smem(fin_cols_kernel<T, N>, G::SMEM_FWD));
-      fin_cols_kernel<T, N><<<dim3((N / 2 + 1 + G::GC - 1) / G::GC, batch), G::NT, G::SMEM_FWD, s>>>(p);
+      // columns per CTA: GC, halved while the grid would not cover the SMs (config 1: one CTA
+      // walked all 33 columns x 16 accumulator lanes, 66 us)
+      int cpb = G::GC;
+      while (cpb > 1 && ((N / 2 + cpb) / cpb) * batch < 148) cpb = (cpb + 1) / 2;
+      fin_cols_kernel<T, N><<<dim3((N / 2 + cpb) / cpb, batch), G::NT, G::SMEM_FWD, s>>>(p, cpb);
       return cudaGetLastError();
     }
     FFST_CHECK(set_smem(fin_rows_kernel<T, N>, G::SMEM_FWD));
