@@ -103,11 +103,64 @@ def tensor_scaling_Phi(omega1, omega2):
     return scaling_varphi(omega1) * scaling_varphi(omega2)
 
 
-def smooth_psi1(omega1, omega2):
+def smooth_psi1(omega1, omega2, precise: bool = True):
     """eq:newPsi1: Psi1(w) = sqrt(Phi^2(w/4) - Phi^2(w)), written out as printed
-    (clipped at 0 against rounding).  Supported in [-4,4]^2 minus [-1/2,1/2]^2."""
-    d = tensor_scaling_Phi(omega1 / 4.0, omega2 / 4.0) ** 2 - tensor_scaling_Phi(omega1, omega2) ** 2
-    return np.sqrt(np.maximum(d, 0.0))
+    (clipped at 0 against rounding).  Supported in [-4,4]^2 minus [-1/2,1/2]^2.
+
+    In float64 the printed difference of two squares cancels where both are close to 1 (just
+    outside |w_i| = 1/2, where varphi = 1 - O(v^2)): the square root of an O(eps) difference is
+    then good to only ~sqrt(eps) absolute.  ``precise`` re-evaluates the same printed formula --
+    v, varphi, Phi, the difference and the root -- in 40-digit arithmetic (mpmath) wherever the
+    float64 difference is a cancellation below 1e-4 (Phi(w) > 0 and not both |w_i| <= 1/2, where
+    the exact value is 0), so the result is correct to ~1e-14 absolute everywhere [reading A19]."""
+    omega1 = np.asarray(omega1, dtype=np.float64)
+    omega2 = np.asarray(omega2, dtype=np.float64)
+    phi_w = tensor_scaling_Phi(omega1, omega2)
+    d = tensor_scaling_Phi(omega1 / 4.0, omega2 / 4.0) ** 2 - phi_w ** 2
+    out = np.sqrt(np.maximum(d, 0.0))
+    if not precise:
+        return out
+    w1b, w2b = np.broadcast_arrays(omega1, omega2)
+    out = np.array(np.broadcast_to(out, w1b.shape), dtype=np.float64)
+    small = np.broadcast_to((d < 1e-4) & (phi_w > 0.0) & (np.maximum(np.abs(omega1), np.abs(omega2)) > 0.5),
+                            w1b.shape)
+    if np.any(small):
+        # Psi1 depends on (|w1|, |w2|) only: evaluate each distinct pair once
+        a1 = np.abs(w1b[small])
+        a2 = np.abs(w2b[small])
+        pairs = np.stack([a1, a2], axis=1)
+        uniq, inv = np.unique(pairs, axis=0, return_inverse=True)
+        vals = np.array([_smooth_psi1_mp(float(x), float(y)) for x, y in uniq], dtype=np.float64)
+        out[small] = vals[np.asarray(inv).reshape(-1)]
+    return out
+
+
+def _smooth_psi1_mp(a1: float, a2: float) -> float:
+    """eq:newPsi1 at one point, every step of the printed formula in 40-digit arithmetic:
+    v (eq:v, P:L77-85), varphi (P:L696-703), Phi = varphi(w1) varphi(w2) (eq:Phi),
+    sqrt(Phi^2(w/4) - Phi^2(w)).  The inputs are the exact float64 grid values."""
+    import mpmath as mp
+    with mp.workdps(40):
+        def v(x):
+            if x < 0:
+                return mp.mpf(0)
+            if x > 1:
+                return mp.mpf(1)
+            return 35 * x**4 - 84 * x**5 + 70 * x**6 - 20 * x**7
+
+        def varphi(w):
+            a = abs(w)
+            if a <= mp.mpf(1) / 2:
+                return mp.mpf(1)
+            if a < 1:
+                return mp.cos(mp.pi / 2 * v(2 * a - 1))
+            return mp.mpf(0)
+
+        x1, x2 = mp.mpf(a1), mp.mpf(a2)
+        big = (varphi(x1 / 4) * varphi(x2 / 4)) ** 2
+        small = (varphi(x1) * varphi(x2)) ** 2
+        d = big - small
+        return float(mp.sqrt(d)) if d > 0 else 0.0
 
 
 # ---------------------------------------------------------------------------

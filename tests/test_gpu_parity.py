@@ -327,13 +327,10 @@ def test_compact_warp_path_unsupported(F, monkeypatch):
 
 
 # ------------------------------------------------------------------ smooth variant
-# The oracle writes eq:newPsi1 as printed, sqrt(Phi^2(w/4) - Phi^2(w)): where the difference is
-# O(eps) its square root is only good to ~sqrt(eps) ~ 1.5e-8 absolute, while the kernels use the
-# cancellation-free form (reading A19).  float64 comparisons against the oracle's
-# smooth spectra therefore use SMOOTH_F64 = 1e-7; squares agree to ~1e-15 and round trips (the
-# kernels' own frame) keep the classic 1e-10.
-SMOOTH_F64 = 1e-7
-TOL_SMOOTH = {torch.float32: 1e-4, torch.float64: SMOOTH_F64}
+# The oracle evaluates eq:newPsi1 as printed, sqrt(Phi^2(w/4) - Phi^2(w)), re-done in 40-digit
+# arithmetic where float64 would cancel (reading A19); the kernels use the
+# cancellation-free form.  Both are exact to rounding: the classic tolerances apply.
+TOL_SMOOTH = TOL
 
 
 @pytest.mark.parametrize("n,dtype", [(4, torch.float64), (16, torch.float64), (64, torch.float64),
@@ -344,7 +341,7 @@ def test_smooth_spectra_match_oracle(F, n, dtype):
     ref = O.shearlet_spectra(n, variant="smooth")
     if dtype == torch.float64:
         assert np.max(np.abs(psi**2 - ref**2)) < 1e-13
-        assert np.max(np.abs(psi - ref)) < SMOOTH_F64
+        assert np.max(np.abs(psi - ref)) < 1e-13
     else:
         assert np.max(np.abs(psi - ref)) < 2e-6
     assert np.max(np.abs(np.sum(psi**2, axis=0) - 1.0)) < (1e-13 if dtype == torch.float64 else 1e-5)

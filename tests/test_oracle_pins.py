@@ -416,12 +416,47 @@ def test_smooth_psi1_support_and_axis():
     assert np.all(p[(m <= 0.5) | (m >= 4.0)] == 0.0)
     assert np.all(p[(m > 0.55) & (m < 3.9)] > 0.0)
     x = np.linspace(-5, 5, 2001)
-    assert np.max(np.abs(O.smooth_psi1(x, 0.0 * x) - O.psi1_hat(x))) < 1e-7   # sqrt of a difference
+    # the printed difference evaluated in float64 alone is only sqrt(eps)-accurate next to
+    # |w| = 1/2; the oracle's 40-digit re-evaluation of the same formula is exact to rounding
+    assert np.max(np.abs(O.smooth_psi1(x, 0.0 * x, precise=False) - O.psi1_hat(x))) > 1e-12
+    assert np.max(np.abs(O.smooth_psi1(x, 0.0 * x) - O.psi1_hat(x))) < 1e-13
     assert np.max(np.abs(O.smooth_psi1(x, 0.0 * x) ** 2 - O.psi1_hat(x) ** 2)) < 1e-14
     # tensor scaling function: 1 on [-1/2,1/2]^2, 0 once a coordinate reaches 1, symmetric
     assert np.all(O.tensor_scaling_Phi(w1, w2)[m <= 0.5] == 1.0)
     assert np.all(O.tensor_scaling_Phi(w1, w2)[m >= 1.0] == 0.0)
     assert np.array_equal(O.tensor_scaling_Phi(w1, w2), O.tensor_scaling_Phi(w2, w1))
+
+
+def test_smooth_psi1_off_axis_closed_form():
+    # Off the axes, with both |w_i| < 1: Phi(w/4) = 1 there (|w_i|/4 < 1/4), so eq:newPsi1 is
+    # sqrt(1 - varphi^2(w1) varphi^2(w2)).  With varphi^2 = 1 - s_i, s_i = sin^2(pi/2 v(2|w_i|-1))
+    # on 1/2 < |w_i| < 1, 1 - varphi1^2 varphi2^2 = s1 + s2 - s1 s2: a sum that does
+    # not cancel, evaluated here independently of the printed difference.
+    g = np.concatenate([np.linspace(0.5, 0.52, 401), np.linspace(0.52, 0.999, 300)])
+    w1, w2 = np.meshgrid(g, g[::7])
+    s = lambda w: np.where(np.abs(w) > 0.5, np.sin(np.pi / 2 * O.meyer_aux(2 * np.abs(w) - 1)) ** 2, 0.0)
+    s1, s2 = s(w1), s(w2)
+    ref = np.sqrt(s1 + s2 - s1 * s2)
+    assert np.max(np.abs(O.smooth_psi1(w1, w2) - ref)) < 1e-13
+    assert np.max(np.abs(O.smooth_psi1(-w1, w2) - ref)) < 1e-13
+
+
+@pytest.mark.parametrize("variant", ["classic", "smooth"])
+@pytest.mark.parametrize("n", [16, 32, 33, 64])
+def test_forward_plane_is_a_plane_of_forward(n, variant):
+    # forward_plane (the per-plane form the large-n parity tests use) is plane i of the whole
+    # transform eq:shearletTransform, for every flat index i, both systems, even
+    # and odd n; forward itself is pinned by the direct DFT, Parseval and the round trip above.
+    f = synth.make_batch(1, n=n)[0]
+    full = O.forward(f, variant=variant)
+    f_hat = O.dft2_centred(f)
+    for i in range(1, full.shape[0] + 1):
+        a = O.forward_plane(f, i, variant=variant)
+        b = O.forward_plane(f, i, f_hat=f_hat, variant=variant)
+        assert np.max(np.abs(a - full[i - 1])) <= 1e-15 * max(1.0, np.max(np.abs(full))), i
+        assert np.array_equal(a, b)
+    with pytest.raises(IndexError):
+        O.forward_plane(f, full.shape[0] + 1, variant=variant)
 
 
 def test_smooth_equals_classic_near_the_axis():
