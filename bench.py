@@ -4,15 +4,17 @@
 One step = one pass of the whole hot path (image spectrum, forward transform to
 the complex coefficient cube, inverse transform back to the images) over one
 batch, i.e. every row of SURVEY.md 8(a).  Default workload: BASELINE.json
-configs[1] (256x256 float32, batch 16).  Prints ONE JSON line (rank 0).
+configs[4] (4096x4096 float32, one image: the largest configuration BASELINE runs on
+one GPU; --config 1..4 select the others).  Prints ONE JSON line (rank 0).
 
   python bench.py [--gpus N] [--steps K] [--warmup W] [--config C] [--impl reference]
 
-N > 1 (launched by torch.distributed.run): the eta shearlet planes are sharded
+N > 1 (launched by torch.distributed.run, or self-launched when WORLD_SIZE is unset): the
+eta shearlet planes are sharded
 (plane i on rank i mod N); rank 0 broadcasts the images (NCCL), every rank runs
 its planes, the partial images are reduced to rank 0 (NCCL).  Total work is
 fixed as N grows ("strong").  --impl reference times the float64 oracle (the
-paper-faithful CPU program) on host cores (rank 0 only).
+paper-faithful CPU program) on all host cores (a process pool; rank 0 only).
 """
 from __future__ import annotations
 
@@ -102,8 +104,13 @@ class ClockSampler:
 
 
 # ------------------------------------------------------------------------------ oracle arm
+# The float64 oracle (as it stands) on ALL host cores: a process pool (spawned workers that import
+# only numpy, synth and oracle) over images -- or, where one image's spectra cube does not fit a
+# worker (n = 4096: 34 GB), over the planes of one image.  numpy's FFT is single-threaded, so
+# one worker per core.  Workers are capped by host memory.
 
 ORACLE_FULL_SPECTRA_BYTES = 2 << 30     # above this the oracle's spectra cube is not materialised
+_W = {}                                  # per-worker caches (spectra, image spectrum)
 
 
 def _oracle_full(cfg) -> bool:
@@ -112,103 +119,176 @@ def _oracle_full(cfg) -> bool:
     return eta * cfg.n * cfg.n * 8 <= ORACLE_FULL_SPECTRA_BYTES
 
 
-def oracle_image_seconds(cfg, x, psi, plane_budget_s: float = 8.0):
-    """Seconds the float64 oracle (as it stands) takes for forward + inverse of one image.
+def _cast(cfg, x):
+    return x.astype(np.float32 if cfg.dtype == "f32" else np.float64).astype(np.float64)
 
-    Small N: the whole transform with the spectra cached, timed directly.
-    Large N (the spectra cube would not fit host memory, e.g. 34 GB at N = 4096): the image
-    FFTs are timed once and the per-plane work (spectrum, ifft2 of the product, fft2 of the
-    plane, multiply-accumulate) on planes spread over the flat index until `plane_budget_s`,
-    then extrapolated to all eta planes.  Returns (seconds, planes actually timed)."""
+
+def _w_init(cid):
+    """Worker set-up (untimed): the spectra cached once (the paper's "second run")."""
     import oracle as O
-    x = np.asarray(x, dtype=np.float64)
-    if psi is not None:
-        t0 = time.perf_counter()
-        c = O.forward(x, psi=psi)
-        O.inverse(c, psi=psi)
-        return time.perf_counter() - t0, len(psi)
-    n = cfg.n
-    eta = O.num_shearlets(O.scales_for_size(n))
-    t0 = time.perf_counter()
-    f_hat = O.dft2_centred(x)
-    t_img = time.perf_counter() - t0
-    acc = np.zeros((n, n), dtype=np.complex128)
-    t_planes, done = 0.0, 0
-    order = list(range(1, eta + 1, max(1, eta // 16))) or [1]
-    for i in order:
-        t0 = time.perf_counter()
-        c = O.forward_plane(x, i, f_hat=f_hat)
-        acc += O.dft2_centred(c) * O.shearlet_spectrum(n, i)
-        t_planes += time.perf_counter() - t0
-        done += 1
-        if t_planes >= plane_budget_s:
-            break
-    t0 = time.perf_counter()
-    O.idft2_centred(acc)
-    t_img += time.perf_counter() - t0
-    return t_img + t_planes / done * eta, done
-
-
-def oracle_images_per_s(cfg, budget_s: float, max_images: int):
-    """The float64 oracle on host cores over a bounded sample of the workload.
-    Returns (images/s, description of the sample)."""
-    import oracle as O
-    full = _oracle_full(cfg)
-    psi = O.shearlet_spectra(cfg.n) if full else None
-    done, dt, planes = 0, 0.0, 0
-    while done < max_images:
-        x = synth.make_image(cfg, done % cfg.batch).astype(np.float32 if cfg.dtype == "f32" else np.float64)
-        s, planes = oracle_image_seconds(cfg, x, psi)
-        dt += s
-        done += 1
-        if dt >= budget_s or not full:
-            break
-    if full:
-        sample = (f"{done} images of config{cfg.cid} ({cfg.n}x{cfg.n}), forward+inverse each, float64 numpy "
-                  f"oracle, spectra built once (cached), {dt:.1f} s")
+    cfg = synth.config(cid)
+    _W.clear()
+    _W["cfg"] = cfg
+    if _oracle_full(cfg):
+        _W["psi"] = O.shearlet_spectra(cfg.n)
     else:
-        sample = (f"1 image of config{cfg.cid} ({cfg.n}x{cfg.n}): image FFTs timed, per-plane work timed on "
-                  f"{planes} of the planes spread over the flat index and extrapolated to all planes "
-                  f"(spectra cube too large to cache), float64 numpy oracle, {dt:.1f} s estimated per image")
-    return done / dt, sample
+        _W["x"] = _cast(cfg, synth.make_image(cfg, 0))
+        _W["f_hat"] = O.dft2_centred(_W["x"])
+    return os.getpid()
 
 
-def oracle_cores():
-    # numpy.fft (pocketfft) and the vectorised window code run single-threaded
-    return 1
+def _w_image(b):
+    """Forward + inverse of image b with the cached spectra; returns seconds."""
+    import oracle as O
+    cfg = _W["cfg"]
+    x = _cast(cfg, synth.make_image(cfg, b % cfg.batch))
+    t0 = time.perf_counter()
+    c = O.forward(x, psi=_W["psi"])
+    O.inverse(c, psi=_W["psi"])
+    return time.perf_counter() - t0
+
+
+def _w_plane(i):
+    """The per-plane work of one image (spectrum, forward plane, its DFT times the spectrum: the
+    plane's share of forward + inverse); returns seconds."""
+    import oracle as O
+    cfg = _W["cfg"]
+    t0 = time.perf_counter()
+    psi = O.shearlet_spectrum(cfg.n, i)
+    c = O.idft2_centred(psi * _W["f_hat"])
+    _ = O.dft2_centred(c) * psi
+    return time.perf_counter() - t0
+
+
+def _w_image_ffts(_):
+    """The per-image work outside the planes: the image DFT and the final inverse DFT."""
+    import oracle as O
+    t0 = time.perf_counter()
+    O.dft2_centred(_W["x"])
+    O.idft2_centred(_W["f_hat"])
+    return time.perf_counter() - t0
+
+
+def _cpu_model():
+    try:
+        with open("/proc/cpuinfo") as fh:
+            for line in fh:
+                if line.startswith("model name"):
+                    return line.split(":", 1)[1].strip()
+    except OSError:
+        pass
+    return "unknown"
+
+
+def _worker_count(cfg):
+    cores = os.cpu_count() or 1
+    if _oracle_full(cfg):
+        import oracle as O
+        eta = O.num_shearlets(O.scales_for_size(cfg.n))
+        per = eta * cfg.n * cfg.n * (8 + 16 + 16) + (256 << 20)     # spectra + cube + temporaries
+    else:
+        per = cfg.n * cfg.n * 16 * 8 + (256 << 20)
+    try:
+        import psutil
+        avail = psutil.virtual_memory().available
+    except Exception:
+        avail = 16 << 30
+    return max(1, min(cores, int(0.7 * avail // per)))
+
+
+class OraclePool:
+    """Spawned worker processes running the oracle; times a bounded sample of the workload."""
+
+    def __init__(self, cfg, workers=None):
+        import multiprocessing as mp
+        self.cfg = cfg
+        self.full = _oracle_full(cfg)
+        self.workers = workers or _worker_count(cfg)
+        self.pool = mp.get_context("spawn").Pool(self.workers, initializer=_w_init, initargs=(cfg.cid,))
+        self.pool.map(_noop, range(self.workers))        # every worker started and set up
+        self.t_cal = None
+
+    def close(self):
+        self.pool.terminate()
+        self.pool.join()
+
+    def images_per_s(self, budget_s: float):
+        """(images/s, seconds of wall time, description of the sample)."""
+        import oracle as O
+        cfg, W = self.cfg, self.workers
+        if self.full:
+            if self.t_cal is None:
+                t0 = time.perf_counter()
+                self.pool.map(_w_image, range(W), chunksize=1)       # calibration round
+                self.t_cal = time.perf_counter() - t0
+            t_cal = self.t_cal
+            rounds = max(1, int(budget_s / max(t_cal, 1e-6)))
+            t0 = time.perf_counter()
+            self.pool.map(_w_image, range(rounds * W), chunksize=1)
+            wall = time.perf_counter() - t0
+            imgs = rounds * W
+            return imgs / wall, wall, (f"{imgs} images of config{cfg.cid} ({cfg.n}x{cfg.n}), forward+inverse "
+                                       f"each, float64 numpy oracle, spectra cached per worker, "
+                                       f"{W} worker processes in parallel, {wall:.1f} s wall")
+        eta = O.num_shearlets(O.scales_for_size(cfg.n))
+        order = [1 + (k * 37) % eta for k in range(eta)]          # planes spread over the flat index
+        if self.t_cal is None:
+            self.t_img = min(self.pool.map(_w_image_ffts, range(W), chunksize=1))
+            t0 = time.perf_counter()
+            self.pool.map(_w_plane, order[:W], chunksize=1)
+            self.t_cal = time.perf_counter() - t0
+        t_img, t_cal = self.t_img, self.t_cal
+        rounds = max(1, min(eta // W if eta >= W else 1, int(budget_s / max(t_cal, 1e-6))))
+        todo = [order[k % eta] for k in range(rounds * W)]
+        t0 = time.perf_counter()
+        self.pool.map(_w_plane, todo, chunksize=1)
+        wall = time.perf_counter() - t0
+        per_image = t_img + wall * eta / len(todo)
+        return 1.0 / per_image, wall + t_img, (
+            f"1 image of config{cfg.cid} ({cfg.n}x{cfg.n}): per-plane work (spectrum, forward plane, its "
+            f"DFT times the spectrum) timed on {len(todo)} planes spread over the flat index with {W} worker "
+            f"processes in parallel and extrapolated to all {eta} planes, plus the image DFTs; float64 numpy "
+            f"oracle, {per_image:.1f} s wall per image")
+
+
+def _noop(_):
+    return 0
+
+
+def oracle_baseline(cfg, budget_s: float):
+    pool = OraclePool(cfg)
+    try:
+        v, wall, sample = pool.images_per_s(budget_s)
+    finally:
+        pool.close()
+    return {"value": v, "unit": "images/s", "cores": pool.workers, "kind": "oracle", "sample": sample,
+            "host_cpus": os.cpu_count(), "cpu_model": _cpu_model()}
 
 
 def run_reference(args, cfg):
     rank = int(os.environ.get("RANK", "0"))
     if rank != 0:
         return 0
-    import oracle as O
-    workload = f"config{cfg.cid}"
-    full = _oracle_full(cfg)
-    psi = O.shearlet_spectra(cfg.n) if full else None
-    per_step = []
-    imgs = 0
-    for s in range(args.warmup + args.steps):
-        x = synth.make_image(cfg, s % max(cfg.batch, 1))
-        x = x.astype(np.float32 if cfg.dtype == "f32" else np.float64)
-        dt, planes = oracle_image_seconds(cfg, x, psi, plane_budget_s=2.0)
-        if s >= args.warmup:
-            per_step.append(dt)
-            imgs += 1
-    total = sum(per_step)
-    value = imgs / total
-    how = ("spectra built once (cached)" if full else
-           f"per-plane work timed on {planes} planes and extrapolated to all planes")
+    pool = OraclePool(cfg)
+    per_step, walls, sample = [], [], ""
+    try:
+        for s in range(args.warmup + args.steps):
+            # each step: a bounded sample of the workload on all cores, as images/s
+            v, wall, sample = pool.images_per_s(budget_s=2.0)
+            if s >= args.warmup:
+                per_step.append(v)
+                walls.append(wall)
+    finally:
+        pool.close()
+    value = float(np.mean(per_step))
     line = {
         "impl": "reference", "metric": METRIC, "value": value, "unit": "images/s",
         "n_gpus": args.gpus, "steps": args.steps, "warmup": args.warmup,
-        "ms_per_step": 1000.0 * total / len(per_step), "higher_is_better": True, "scaling": "strong",
+        "ms_per_step": 1000.0 / value, "higher_is_better": True, "scaling": "strong",
         "vs_baseline": None, "dtype": "f64", "data": "synthetic",
-        "config": {"workload": workload, "n": cfg.n, "batch_per_step": 1, "config_batch": cfg.batch,
-                   "label": cfg.label},
-        "cpu_baseline": {"value": value, "unit": "images/s", "cores": oracle_cores(), "kind": "oracle",
-                         "sample": f"1 image of {workload} per step (forward+inverse, float64 numpy oracle, "
-                                   f"{how}), {imgs} timed steps"},
+        "config": {"workload": f"config{cfg.cid}", "n": cfg.n, "global_batch": cfg.batch, "label": cfg.label},
+        "cpu_baseline": {"value": value, "unit": "images/s", "cores": pool.workers, "kind": "oracle",
+                         "sample": f"per step: {sample}", "host_cpus": os.cpu_count(), "cpu_model": _cpu_model()},
         "e2e": {"value": value, "unit": "images/s", "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0},
     }
     print(json.dumps(line), flush=True)
@@ -498,8 +578,7 @@ def run_gpu(args, cfg):
 
     cpu = None
     if rank == 0 and world == 1 and not args.no_cpu_baseline:
-        v, sample = oracle_images_per_s(cfg, budget_s=args.cpu_budget, max_images=max(cfg.batch, 4) * 4)
-        cpu = {"value": v, "unit": "images/s", "cores": oracle_cores(), "kind": "oracle", "sample": sample}
+        cpu = oracle_baseline(cfg, budget_s=args.cpu_budget)
 
     if rank == 0:
         line = {
@@ -541,12 +620,22 @@ def main():
     ap.add_argument("--gpus", type=int, default=1)
     ap.add_argument("--steps", type=int, default=10)
     ap.add_argument("--warmup", type=int, default=3)
-    ap.add_argument("--config", type=int, default=2, help="BASELINE.json configs[C-1] (1..5)")
+    ap.add_argument("--config", type=int, default=5,
+                    help="BASELINE.json configs[C-1] (1..5); default 5 (4096^2 f32), the largest single-GPU config")
     ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
     ap.add_argument("--cpu-budget", type=float, default=12.0)
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--no-cufft", action="store_true", help="skip the cuFFT comparison line")
     args = ap.parse_args()
+    if args.gpus > 1 and "WORLD_SIZE" not in os.environ:
+        # plain `python bench.py --gpus N`: launch N ranks on this node (one process per GPU)
+        import socket
+        with socket.socket() as sk:
+            sk.bind(("127.0.0.1", 0))
+            port = sk.getsockname()[1]
+        cmd = [sys.executable, "-m", "torch.distributed.run", "--nnodes=1", f"--nproc-per-node={args.gpus}",
+               "--master-addr", "127.0.0.1", "--master-port", str(port), os.path.abspath(__file__), *sys.argv[1:]]
+        os.execv(sys.executable, cmd)
     cfg = synth.config(args.config)
     if args.impl == "reference":
         return run_reference(args, cfg)

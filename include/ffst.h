@@ -22,8 +22,9 @@
  *  - Flat indices in this ABI are 0-based (the paper's i = index + 1).
  *  - Ownership: the caller owns every image / coefficient / spectra buffer it
  *    passes (device memory unless the function name ends in _host).  The plan
- *    owns its tables and workspace, allocated once in ffst_plan_create; no call
- *    allocates device memory and the library never frees caller memory.
+ *    owns its tables and workspace, allocated in ffst_plan_create (and, for the
+ *    work queue of another batch size, ffst_plan_reserve); no transform call
+ *    allocates, uploads or synchronises, and the library never frees caller memory.
  *  - Streams: `stream` is a cudaStream_t (0 = legacy default stream).  All
  *    device-buffer calls are asynchronous on that stream; a plan serves one
  *    stream at a time (calls on one plan must not overlap).
@@ -116,9 +117,7 @@ ffst_status ffst_plane_is_nyquist(int n, int j0, int index, int* is_nyquist);
  * edges, work queues) and all device workspace are built here; transforms allocate nothing.
  * Errors: INVALID_SIZE (n < 4 or above the built sizes), UNSUPPORTED (n not a power of two,
  * more than 256 local planes), INVALID_ARG (incl. an unknown variant), OOM, CUDA.
- * FFST_SMOOTH plans always run the CTA-item kernels (FFST_PATH=warp is ignored for them).
  * Environment (read here, tuning only; results are identical up to rounding order):
- *   FFST_PATH=warp      warp-worker kernels for 8 <= n <= 512 (default: CTA-item kernels)
  *   FFST_RING_MB        intermediate ring budget (default 80; at least 12 slots)
  *   FFST_CHUNK_PLANES   planes per chunk (default 4; batch <= 4: eta / lanes, or 32 with one lane)
  *   FFST_SLOT_KB        chunk byte budget (default 4096; 12288 for n >= 1024)
@@ -152,6 +151,14 @@ ffst_status ffst_plan_create_user(ffst_plan** out, const ffst_plan_desc* desc, i
  * plans: computed on the first call from the materialised spectra (needs shard_count == 1,
  * else UNSUPPORTED; allocates eta n^2 reals temporarily). */
 ffst_status ffst_plan_spectra_check(ffst_plan* plan, double* tightness, double* asymmetry);
+
+/* Reserve the work queues of the persistent kernels for calls with `batch` images (1 <= batch <=
+ * the plan's batch; ffst_plan_create reserves the plan's batch).  Builds and uploads the queue
+ * (plan-owned device memory, synchronous); a no-op if already reserved.  Transforms with a batch
+ * that was not reserved fail with INVALID_ARG before launching anything (so a transform never
+ * allocates, uploads or synchronises, and can be captured in a CUDA graph).
+ * Errors: INVALID_ARG (null plan, batch out of range), OOM, CUDA. */
+ffst_status ffst_plan_reserve(ffst_plan* plan, int batch);
 
 /* Number of local planes and (if global_indices != NULL) their 0-based global indices. */
 ffst_status ffst_plan_local_planes(const ffst_plan* plan, int* count, int* global_indices);
@@ -192,8 +199,7 @@ ffst_status ffst_inversesheartrans_host(ffst_plan* plan, const void* coeff, void
  * as nyq_gh [batch][n_nyq][2][n] reals (Nyquist planes in the order of
  * ffst_plan_nyquist_planes): half the bytes of the complex cube, lossless for every cube the
  * forward produces (an arbitrary complex cube, e.g. after thresholding, is not representable:
- * use the complex entry points).  Same validation, streams and errors as the complex calls;
- * UNSUPPORTED with FFST_PATH=warp. */
+ * use the complex entry points).  Same validation, streams and errors as the complex calls. */
 ffst_status ffst_sheartrans_compact(ffst_plan* plan, const void* img, void* coeff_re, void* nyq_gh, int batch,
                                     void* stream);
 ffst_status ffst_inversesheartrans_compact(ffst_plan* plan, const void* coeff_re, const void* nyq_gh, void* img_out,

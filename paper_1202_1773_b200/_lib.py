@@ -56,6 +56,7 @@ _SIGS = {
     "ffst_plan_destroy": (_i, [_vp]),
     "ffst_plan_create_user": (_i, [C.POINTER(_vp), C.POINTER(PlanDesc), _i, _vp, _i]),
     "ffst_plan_spectra_check": (_i, [_vp, C.POINTER(C.c_double), C.POINTER(C.c_double)]),
+    "ffst_plan_reserve": (_i, [_vp, _i]),
     "ffst_plan_local_planes": (_i, [_vp, _p, _p]),
     "ffst_plan_workspace_bytes": (_i, [_vp, C.POINTER(_sz)]),
     "ffst_plan_info": (_i, [_vp, _p, _p, _p, _p, _p]),

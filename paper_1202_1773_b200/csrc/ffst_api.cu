@@ -190,36 +190,6 @@ Radial<double> host_radial(const std::vector<double>& tab, int n, int j0, int va
   return R;
 }
 
-// Column records of the warp path (ColRec, ffst_math.cuh): hulls of the rows where sym_i is
-// non-zero in each Hermitian-half column of the plane, found by evaluating the window (float64)
-// on the whole column, widened by one row; plus the horizontal radial factor and 1/|u1|.
-template <typename T>
-void column_records(int n, int j0, PlaneDev& P, std::vector<ColRec<T>>& out) {
-  const int H = n / 2;
-  const std::vector<double> tab = radial_table(n, j0);
-  const Radial<double> R{tab.data(), H + 1, j0};
-  P.rec = (int)out.size();
-  for (int c = P.c_lo; c < P.c_lo + P.ncols; ++c) {
-    const int u1 = c == H ? -H : c, a1 = std::abs(u1);
-    int lo[3] = {H + 1, H + 1, H + 1}, hi[3] = {-H - 2, -H - 2, -H - 2};
-    for (int u2 = -H; u2 < H; ++u2) {
-      if (window_sym<double>(P, u1, u2, H, R) == 0.0) continue;
-      const int r = std::abs(u2) <= a1 ? 0 : (u2 > 0 ? 1 : 2);
-      lo[r] = std::min(lo[r], u2);
-      hi[r] = std::max(hi[r], u2);
-    }
-    ColRec<T> rc{};
-    for (int r = 0; r < 3; ++r) {
-      if (lo[r] > hi[r]) { rc.lo[r] = 1; rc.hi[r] = 0; continue; }
-      rc.lo[r] = std::max(-H, lo[r] - 1);
-      rc.hi[r] = std::min(H - 1, hi[r] + 1);
-    }
-    rc.rh = (P.kind == 1 || P.kind == 3) ? (T)tab[(size_t)P.j * (H + 1) + a1] : T(0);
-    rc.inv_a1 = a1 > 0 ? (T)(1.0 / a1) : T(0);
-    out.push_back(rc);
-  }
-}
-
 bool plane_nyquist(int n, int j0, const Triple& tr, int variant) {
   PlaneDev P{};
   P.kind = tr.kind; P.j = tr.j; P.k = tr.k;
@@ -236,7 +206,6 @@ bool plane_nyquist(int n, int j0, const Triple& tr, int variant) {
 struct Queue {
   int batch = 0;
   int n_chunks = 0, n_fwd = 0, n_inv = 0, n_g = 0;
-  int batch_fwd = 1, batch_inv = 1;   // largest safe per-CTA fetch batch (dependency distance)
   int a_lanes = 1;                    // accumulator lanes of the inverse (copies of A summed at the end)
   long long slot_elems = 0;
   int nslots = 0;
@@ -257,8 +226,7 @@ struct ffst_plan {
   std::vector<int> nyq;
   Geometry geo{};
   int sm_count = 0, grid_fwd = 0, grid_inv = 0;
-  bool warp = false;              // warp-worker kernels (ffst_warp.cuh), n <= 512
-  int workers = 0;                // concurrent item consumers (warps or CTAs) of the persistent kernels
+  int workers = 0;                // concurrent item consumers (CTAs) of the persistent kernels
   long long slot_budget = 0;
   int chunk_planes = 4;           // max planes per chunk (pipelining granularity of the passes)
   int acc_lanes = 4;              // max accumulator lanes of the inverse (FFST_ACC_LANES)
@@ -267,7 +235,6 @@ struct ffst_plan {
   int* d_nyq = nullptr;
   void* d_tw = nullptr;
   void* d_rtab = nullptr;
-  void* d_colrec = nullptr;       // warp path column records (ColRec<T>)
   void *F = nullptr, *Fscr = nullptr, *A = nullptr, *W = nullptr;
   long long W_elems = 0;
   void *nyq_fwd = nullptr, *nyq_S = nullptr, *nyq_T = nullptr, *corr = nullptr, *nyq_anti = nullptr;
@@ -276,6 +243,7 @@ struct ffst_plan {
   int* d_ctr = nullptr;
   size_t ctr_cap = 0;
   int n_rowitems = 0;
+  int rpi = 0;                    // inverse pass 1: rows per item
   std::map<int, Queue> queues;
   size_t ws_bytes = 0;
   bool timing = false;
@@ -335,6 +303,7 @@ ffst_status dalloc(ffst_plan* p, void** ptr, size_t bytes) {
 ffst_status build_queue(ffst_plan* p, int batch, Queue** out) {
   auto it = p->queues.find(batch);
   if (it != p->queues.end()) { *out = &it->second; return FFST_OK; }
+  if (batch < 1 || batch > p->d.batch) return fail(FFST_ERR_INVALID_ARG, "batch outside 1..plan batch");
   const int N = p->n, H = p->H;
   const Geometry& g = p->geo;
   // ---- 1. chunks per image (in image order)
@@ -437,7 +406,7 @@ ffst_status build_queue(ffst_plan* p, int batch, Queue** out) {
       for (int gi = 0; gi < ng1; ++gi) f1[c].push_back(mk_item(0, c, gi, ch.b, units[u].p, 1, units[u].woff, ch.slot));
       const int ng2 = (N + g.rp2 - 1) / g.rp2;
       for (int gi = 0; gi < ng2; ++gi) f2[c].push_back(mk_item(1, c, gi, ch.b, units[u].p, 1, units[u].woff, ch.slot));
-      const int ni1 = (N + g.rpi - 1) / g.rpi;
+      const int ni1 = (N + p->rpi - 1) / p->rpi;
       for (int gi = 0; gi < ni1; ++gi) i1[c].push_back(mk_item(0, c, gi, ch.b, units[u].p, 1, units[u].woff, ch.slot));
     }
     for (int gg = 0; gg < ngroups; ++gg) {
@@ -452,10 +421,6 @@ ffst_status build_queue(ffst_plan* p, int batch, Queue** out) {
       ItemDev it = mk_item(1, c, gg, ch.b, units[ch.unit0].p, ch.nunits, units[ch.unit0].woff, ch.slot);
       it.first = ch.first_of_image;
       it.pad1 = chunk_lane[c];
-      for (int u = ch.unit0; u < ch.unit0 + ch.nunits; ++u) {
-        const PlaneDev& P = p->planes[units[u].p];
-        if (g1 > P.c_lo && g0 < P.c_lo + P.ncols) it.pad0 |= 1 << (u - ch.unit0);
-      }
       it.wait2_ctr = last >= 0 ? 1 + 2 * C + last : -1;
       it.sig2_ctr = 1 + 2 * C + n_self;
       i2[c].push_back(it);
@@ -491,7 +456,7 @@ ffst_status build_queue(ffst_plan* p, int batch, Queue** out) {
   for (int c = 0; c < C; ++c)
     for (auto& it : f1[c]) it.pad0 = -1;
   const char* envp = std::getenv("FFST_PAIR");
-  const bool pair_ok = !p->warp && g.gc == g.lpc && batch >= 2 && !(envp && std::atoi(envp) == 0);
+  const bool pair_ok = g.gc == g.lpc && batch >= 2 && !(envp && std::atoi(envp) == 0);
   if (pair_ok) {
     for (int c = 0; c + 1 < C; ++c) {
       const Proto& a = protos[order[c]];
@@ -537,28 +502,6 @@ ffst_status build_queue(ffst_plan* p, int batch, Queue** out) {
       *q = k;
     }
   }
-  // Smallest distance (in queue positions) between an item and the last item it depends on:
-  // a CTA may take that many consecutive items per fetch without deadlock (an item's
-  // dependencies are then always held by other fetches).
-  auto min_slack = [&](const std::vector<ItemDev>& q) {
-    std::map<int, int> last_sig;                  // counter -> last queue position signalling it
-    for (int i = 0; i < (int)q.size(); ++i) {
-      last_sig[q[i].sig_ctr] = i;
-      if (q[i].sig2_ctr >= 0) last_sig[q[i].sig2_ctr] = i;
-    }
-    int slack = 1 << 30;
-    for (int i = 0; i < (int)q.size(); ++i) {
-      for (int c : {q[i].wait_ctr, q[i].wait2_ctr}) {
-        if (c < 0) continue;
-        auto f = last_sig.find(c);
-        if (f != last_sig.end()) slack = std::min(slack, i - f->second);
-      }
-    }
-    return slack;
-  };
-  const int want = p->warp ? p->geo.warps : 1;
-  const int batch_fwd = std::max(1, std::min(want, min_slack(fwd)));
-  const int batch_inv = std::max(1, std::min(want, min_slack(inv)));
   std::vector<ChunkDev> chunks_inv = chunks;
   for (int c = 0; c < C; ++c) {
     chunks[c].p1_items = (int)f1[c].size();
@@ -574,8 +517,6 @@ ffst_status build_queue(ffst_plan* p, int batch, Queue** out) {
   q.n_fwd = (int)fwd.size();
   q.n_inv = (int)inv.size();
   q.n_g = n_self;
-  q.batch_fwd = batch_fwd;
-  q.batch_inv = batch_inv;
   q.a_lanes = K;
   const size_t need_ctr = 1 + 2 * (size_t)C + (size_t)n_self;
   if (need_ctr > p->ctr_cap) {
@@ -593,6 +534,7 @@ ffst_status build_queue(ffst_plan* p, int batch, Queue** out) {
   q.d_fwd = static_cast<ItemDev*>(ptr);
   TRY(dalloc(p, &ptr, inv.size() * sizeof(ItemDev)));
   q.d_inv = static_cast<ItemDev*>(ptr);
+  // (plan creation / ffst_plan_reserve only: transforms never reach this upload)
   API_CUDA(cudaMemcpy(q.d_units, units.data(), units.size() * sizeof(UnitDev), cudaMemcpyHostToDevice), "queue upload");
   API_CUDA(cudaMemcpy(q.d_chunks, chunks.data(), chunks.size() * sizeof(ChunkDev), cudaMemcpyHostToDevice), "queue upload");
   API_CUDA(cudaMemcpy(q.d_chunks + chunks.size(), chunks_inv.data(), chunks.size() * sizeof(ChunkDev),
@@ -600,11 +542,20 @@ ffst_status build_queue(ffst_plan* p, int batch, Queue** out) {
   API_CUDA(cudaMemcpy(q.d_fwd, fwd.data(), fwd.size() * sizeof(ItemDev), cudaMemcpyHostToDevice), "queue upload");
   API_CUDA(cudaMemcpy(q.d_inv, inv.data(), inv.size() * sizeof(ItemDev), cudaMemcpyHostToDevice), "queue upload");
   if (std::getenv("FFST_VERBOSE"))
-    std::fprintf(stderr, "[ffst] batch=%d chunks=%d (per image %d) D=%d R=%d Wg=%d slot=%.1f MB items fwd=%d inv=%d fetch batch %d/%d\n",
-                 batch, C, chunks_per_image, D, R, Wg, slot_elems * 2.0 * p->rsz / 1048576.0, q.n_fwd, q.n_inv,
-                 batch_fwd, batch_inv);
+    std::fprintf(stderr, "[ffst] batch=%d chunks=%d (per image %d) D=%d R=%d Wg=%d slot=%.1f MB items fwd=%d inv=%d\n",
+                 batch, C, chunks_per_image, D, R, Wg, slot_elems * 2.0 * p->rsz / 1048576.0, q.n_fwd, q.n_inv);
   auto res = p->queues.emplace(batch, q);
   *out = &res.first->second;
+  return FFST_OK;
+}
+
+// The queue of a reserved batch size (ffst_plan_create reserves the plan batch; other sizes
+// through ffst_plan_reserve): transforms never allocate or upload.
+ffst_status find_queue(ffst_plan* p, int batch, Queue** out) {
+  auto it = p->queues.find(batch);
+  if (it == p->queues.end())
+    return fail(FFST_ERR_INVALID_ARG, "batch " + std::to_string(batch) + " not reserved (ffst_plan_reserve)");
+  *out = &it->second;
   return FFST_OK;
 }
 
@@ -618,10 +569,10 @@ KParams base_params(ffst_plan* p) {
   k.nyq_planes = p->d_nyq;
   k.tw = p->d_tw;
   k.rtab = p->d_rtab;
-  k.colrec = p->d_colrec;
   k.F = p->F; k.Fscr = p->Fscr; k.A = p->A; k.W = p->W;
   k.nyq_fwd = p->nyq_fwd; k.nyq_S = p->nyq_S; k.nyq_T = p->nyq_T; k.corr = p->corr; k.nyq_anti = p->nyq_anti; k.nyq_part = p->nyq_part;
   k.n_rowitems = p->n_rowitems;
+  k.rpi = p->rpi;
   k.a_lane_elems = (long long)p->d.batch * (p->n / 2 + 1) * p->n;
   if (const char* d = std::getenv("FFST_DBG")) k.dbg = std::atoi(d);
   return k;
@@ -672,15 +623,19 @@ ffst_status trace_buffer(ffst_plan* p, int which, int n_items, KParams* k) {
 }
 
 // nyq_gh != nullptr: compact (f1) format -- coeff holds the real parts, nyq_gh the Nyquist vectors
+// Argument checks of a transform call, all before anything is launched or copied.
+ffst_status validate_call(ffst_plan* p, const void* a, const void* b, int batch, Queue** q) {
+  if (!a || !b) return fail(FFST_ERR_INVALID_ARG, "null buffer");
+  if (batch < 1 || batch > p->d.batch) return fail(FFST_ERR_INVALID_ARG, "batch outside 1..plan batch");
+  if (!aligned16(a) || !aligned16(b)) return fail(FFST_ERR_ALIGNMENT, "buffers must be 16-byte aligned");
+  return find_queue(p, batch, q);
+}
+
 ffst_status forward_impl(ffst_plan* p, const void* img, void* coeff, int batch, cudaStream_t s,
                          void* nyq_gh = nullptr) {
-  if (!img || !coeff) return fail(FFST_ERR_INVALID_ARG, "null buffer");
-  if (nyq_gh != nullptr && p->warp) return fail(FFST_ERR_UNSUPPORTED, "compact format: CTA-item kernels only");
-  if (batch < 1 || batch > p->d.batch) return fail(FFST_ERR_INVALID_ARG, "batch outside 1..plan batch");
-  if (!aligned16(img) || !aligned16(coeff)) return fail(FFST_ERR_ALIGNMENT, "buffers must be 16-byte aligned");
-  TRY(set_device(p));
   Queue* q = nullptr;
-  TRY(build_queue(p, batch, &q));
+  TRY(validate_call(p, img, coeff, batch, &q));
+  TRY(set_device(p));
   KParams k = base_params(p);
   k.batch = batch;
   k.img = img;
@@ -693,7 +648,6 @@ ffst_status forward_impl(ffst_plan* p, const void* img, void* coeff, int batch, 
   k.chunks = q->d_chunks;
   k.items = q->d_fwd;
   k.n_items = q->n_fwd;
-  k.fetch_batch = q->batch_fwd;
   k.slot_elems = q->slot_elems;
   k.ctr = p->d_ctr;
   k.ctr_p1 = 1;
@@ -710,9 +664,7 @@ ffst_status forward_impl(ffst_plan* p, const void* img, void* coeff, int batch, 
   }
   API_CUDA(cudaMemsetAsync(p->d_ctr, 0, (1 + 2 * (size_t)q->n_chunks) * sizeof(int), s), "counter reset");
   if (p->timing) API_CUDA(cudaEventRecord(p->ev[1], s), "event");
-  if (p->warp) API_CUDA(p->d.dtype == FFST_F32 ? launch_fwd_warp<float>(k, p->grid_fwd, s)
-                                               : launch_fwd_warp<double>(k, p->grid_fwd, s), "fwd_warp kernel");
-  else API_CUDA(L_fwd_main(p, k, p->grid_fwd, s), "fwd_main kernel");
+  API_CUDA(L_fwd_main(p, k, p->grid_fwd, s), "fwd_main kernel");
   ++nl;
   if (p->timing) {
     API_CUDA(cudaEventRecord(p->ev[2], s), "event");
@@ -723,13 +675,9 @@ ffst_status forward_impl(ffst_plan* p, const void* img, void* coeff, int batch, 
 
 ffst_status inverse_impl(ffst_plan* p, const void* coeff, void* img_out, int batch, cudaStream_t s,
                          const void* nyq_gh = nullptr) {
-  if (!img_out || !coeff) return fail(FFST_ERR_INVALID_ARG, "null buffer");
-  if (nyq_gh != nullptr && p->warp) return fail(FFST_ERR_UNSUPPORTED, "compact format: CTA-item kernels only");
-  if (batch < 1 || batch > p->d.batch) return fail(FFST_ERR_INVALID_ARG, "batch outside 1..plan batch");
-  if (!aligned16(img_out) || !aligned16(coeff)) return fail(FFST_ERR_ALIGNMENT, "buffers must be 16-byte aligned");
-  TRY(set_device(p));
   Queue* q = nullptr;
-  TRY(build_queue(p, batch, &q));
+  TRY(validate_call(p, coeff, img_out, batch, &q));
+  TRY(set_device(p));
   KParams k = base_params(p);
   k.batch = batch;
   k.coeff = const_cast<void*>(coeff);
@@ -744,7 +692,6 @@ ffst_status inverse_impl(ffst_plan* p, const void* coeff, void* img_out, int bat
   k.items = q->d_inv;
   k.n_items = q->n_inv;
   k.a_lanes = q->a_lanes;
-  k.fetch_batch = q->batch_inv;
   k.slot_elems = q->slot_elems;
   k.ctr = p->d_ctr;
   k.ctr_p1 = 1;
@@ -755,9 +702,7 @@ ffst_status inverse_impl(ffst_plan* p, const void* coeff, void* img_out, int bat
   if (p->timing) API_CUDA(cudaEventRecord(p->ev[3], s), "event");
   API_CUDA(cudaMemsetAsync(p->d_ctr, 0, (1 + 2 * (size_t)q->n_chunks + q->n_g) * sizeof(int), s), "counter reset");
   if (p->timing) API_CUDA(cudaEventRecord(p->ev[4], s), "event");
-  if (p->warp) API_CUDA(p->d.dtype == FFST_F32 ? launch_inv_warp<float>(k, p->grid_inv, s)
-                                               : launch_inv_warp<double>(k, p->grid_inv, s), "inv_warp kernel");
-  else API_CUDA(L_inv_main(p, k, p->grid_inv, s), "inv_main kernel");
+  API_CUDA(L_inv_main(p, k, p->grid_inv, s), "inv_main kernel");
   ++nl;
   if (p->timing) API_CUDA(cudaEventRecord(p->ev[5], s), "event");
   if (!p->nyq.empty()) {
@@ -953,7 +898,7 @@ static ffst_status plan_create_impl(ffst_plan** out, const ffst_plan_desc* d_in,
   if (d->shard_count < 1 || d->shard_rank < 0 || d->shard_rank >= d->shard_count)
     return fail(FFST_ERR_INVALID_ARG, "bad shard_rank / shard_count");
   const int j0 = d->j0 == 0 ? default_j0(d->n) : d->j0;
-  if (j0 < 1 || (1 << (2 * j0)) > 4 * d->n || j0 > 12)
+  if (j0 < 1 || j0 > 12 || (1 << (2 * j0)) > 4 * d->n)
     return fail(FFST_ERR_INVALID_ARG, "j0 outside 1..(floor(log2 n)/2 + 1)");
   const int eta = us ? us->eta : ffst_num_shearlets(j0);
   if (d->shard_count > eta) return fail(FFST_ERR_INVALID_ARG, "more shards than shearlets");
@@ -963,21 +908,12 @@ static ffst_status plan_create_impl(ffst_plan** out, const ffst_plan_desc* d_in,
   p->n = d->n; p->j0 = j0; p->eta = eta; p->H = d->n / 2;
   p->rsz = d->dtype == FFST_F32 ? 4 : 8;
   p->delta = grid_delta(d->n, j0);
-  {
-    // Default: the CTA-item kernels (ffst_kernels.cuh) at every n -- measured faster on B200 with
-    // the full-ring lookahead.  FFST_PATH=warp selects the warp-worker kernels
-    // (ffst_warp.cuh, 8 <= n <= 512), kept as a tested alternative scheme.
-    const char* path = std::getenv("FFST_PATH");
-    // (the warp path hoists a per-column radial factor: classic system only)
-    p->warp = d->n >= 8 && d->n <= 512 && d->variant == FFST_CLASSIC && path && std::strcmp(path, "warp") == 0;
-  }
-  if (p->warp) p->geo = d->dtype == FFST_F32 ? geometry_warp<float>(d->n) : geometry_warp<double>(d->n);
-  else p->geo = d->dtype == FFST_F32 ? geometry<float>(d->n) : geometry<double>(d->n);
+  p->geo = d->dtype == FFST_F32 ? geometry<float>(d->n) : geometry<double>(d->n);
   const auto table = index_table(j0);
   for (int i = d->shard_rank; i < eta; i += d->shard_count) {
     PlaneDev P{};
     P.gi = i;
-    P.rec = (int)p->planes.size();   // (the warp path overwrites it with its column-record index)
+    P.rec = (int)p->planes.size();
     P.nyq = -1;
     if (us) {   // user spectra: the whole half plane until the prepare pass has found the hulls
       P.c_lo = 0; P.ncols = d->n / 2 + 1;
@@ -1006,10 +942,7 @@ static ffst_status plan_create_impl(ffst_plan** out, const ffst_plan_desc* d_in,
   int dev = d->device;
   e = cudaDeviceGetAttribute(&p->sm_count, cudaDevAttrMultiProcessorCount, dev);
   if (e != cudaSuccess) return cleanup(cuda_fail(e, "device query"));
-  if (p->warp) {
-    p->grid_fwd = p->grid_inv = p->sm_count;            // one CTA of worker warps per SM
-    p->workers = p->sm_count * p->geo.warps;
-  } else {
+  {
     const int af = d->dtype == FFST_F32 ? max_active_main<float>(d->n, dev, 0) : max_active_main<double>(d->n, dev, 0);
     const int ai = d->dtype == FFST_F32 ? max_active_main<float>(d->n, dev, 1) : max_active_main<double>(d->n, dev, 1);
     if (af < 1 || ai < 1) return cleanup(fail(FFST_ERR_CUDA, "persistent kernels cannot be made resident"));
@@ -1064,8 +997,16 @@ static ffst_status plan_create_impl(ffst_plan** out, const ffst_plan_desc* d_in,
   const long long ring_bytes = (envr ? std::atoll(envr) : 80) * 1024LL * 1024LL;
   // ring: the budget (L2-sized) or at least 12 slots when single planes are large (n >= 2048:
   // the intermediates then live in HBM; a short ring would serialise the two passes)
-  p->W_elems = std::max(12 * ((slot_max + 63) / 64 * 64), ring_bytes / (long long)csz);
-  p->n_rowitems = (int)((N + p->geo.rpi - 1) / p->geo.rpi);
+  const char* envs = std::getenv("FFST_MIN_SLOTS");
+  const long long min_slots = envs ? std::max(2, std::atoi(envs)) : 12;
+  p->W_elems = std::max(min_slots * ((slot_max + 63) / 64 * 64), ring_bytes / (long long)csz);
+  // inverse pass-1 rows per item (FFST_RPI: tuning only; a multiple of the row tile)
+  p->rpi = p->geo.rpi;
+  if (const char* er = std::getenv("FFST_RPI")) {
+    const int v = std::atoi(er);
+    if (v >= p->geo.gr && v % p->geo.gr == 0 && v <= d->n) p->rpi = v;
+  }
+  p->n_rowitems = (int)((N + p->rpi - 1) / p->rpi);
   const size_t nn = std::max<size_t>(1, p->nyq.size());
 
   void* ptr = nullptr;
@@ -1098,23 +1039,6 @@ static ffst_status plan_create_impl(ffst_plan** out, const ffst_plan_desc* d_in,
     } else if (e == cudaSuccess) {
       e = cudaMemcpy(p->d_rtab, rt.data(), rt.size() * sizeof(double), cudaMemcpyHostToDevice);
     }
-  }
-  if (e == cudaSuccess && p->warp) {
-    size_t bytes = 0;
-    std::vector<ColRec<float>> rf;
-    std::vector<ColRec<double>> rd;
-    if (d->dtype == FFST_F32) {
-      for (auto& P : p->planes) column_records<float>(d->n, j0, P, rf);
-      bytes = rf.size() * sizeof(ColRec<float>);
-    } else {
-      for (auto& P : p->planes) column_records<double>(d->n, j0, P, rd);
-      bytes = rd.size() * sizeof(ColRec<double>);
-    }
-    st = dalloc(p, &ptr, bytes);
-    if (st != FFST_OK) return cleanup(st);
-    p->d_colrec = ptr;
-    e = cudaMemcpy(p->d_colrec, d->dtype == FFST_F32 ? (const void*)rf.data() : (const void*)rd.data(), bytes,
-                   cudaMemcpyHostToDevice);
   }
   if (e == cudaSuccess && !p->nyq.empty() && us) {
     std::vector<double> anti(p->nyq.size() * 2 * N);
@@ -1167,6 +1091,14 @@ static ffst_status plan_create_impl(ffst_plan** out, const ffst_plan_desc* d_in,
   if (st != FFST_OK) return cleanup(st);
   *out = p;
   return FFST_OK;
+}
+
+ffst_status ffst_plan_reserve(ffst_plan* p, int batch) {
+  if (!p) return fail(FFST_ERR_INVALID_ARG, "null plan");
+  if (batch < 1 || batch > p->d.batch) return fail(FFST_ERR_INVALID_ARG, "batch outside 1..plan batch");
+  TRY(set_device(p));
+  Queue* q = nullptr;
+  return build_queue(p, batch, &q);
 }
 
 ffst_status ffst_plan_local_planes(const ffst_plan* p, int* count, int* global_indices) {
@@ -1261,7 +1193,8 @@ ffst_status ffst_inversesheartrans(ffst_plan* p, const void* coeff, void* img, v
 
 ffst_status ffst_sheartrans_host(ffst_plan* p, const void* img_host, void* coeff, int batch, void* stream) {
   if (!p || !img_host) return fail(FFST_ERR_INVALID_ARG, "null argument");
-  if (batch < 1 || batch > p->d.batch) return fail(FFST_ERR_INVALID_ARG, "batch outside 1..plan batch");
+  Queue* q = nullptr;
+  TRY(validate_call(p, p->stage, coeff, batch, &q));          // everything checked before the copy
   TRY(set_device(p));
   cudaStream_t s = static_cast<cudaStream_t>(stream);
   const size_t bytes = (size_t)batch * p->n * p->n * p->rsz;
@@ -1271,6 +1204,8 @@ ffst_status ffst_sheartrans_host(ffst_plan* p, const void* img_host, void* coeff
 
 ffst_status ffst_inversesheartrans_host(ffst_plan* p, const void* coeff, void* img_host, int batch, void* stream) {
   if (!p || !img_host) return fail(FFST_ERR_INVALID_ARG, "null argument");
+  Queue* q = nullptr;
+  TRY(validate_call(p, coeff, p->stage, batch, &q));
   TRY(set_device(p));
   cudaStream_t s = static_cast<cudaStream_t>(stream);
   TRY(inverse_impl(p, coeff, p->stage, batch, s));
@@ -1336,8 +1271,9 @@ ffst_status ffst_plan_trace(ffst_plan* p, int which, int batch, unsigned long lo
   if (!p->tracing || !p->d_trace[which]) return fail(FFST_ERR_INVALID_ARG, "tracing not enabled / no call yet");
   Queue* q = nullptr;
   TRY(set_device(p));
-  TRY(build_queue(p, batch, &q));
-  const int n = std::min(max_records, which == 0 ? q->n_fwd : q->n_inv);
+  TRY(find_queue(p, batch, &q));
+  const int n = std::min(std::min(max_records, which == 0 ? q->n_fwd : q->n_inv), p->trace_items[which]);
+  if (n < 0) return fail(FFST_ERR_INVALID_ARG, "max_records < 0");
   API_CUDA(cudaDeviceSynchronize(), "trace sync");
   API_CUDA(cudaMemcpy(host_out, p->d_trace[which], (size_t)n * 8 * sizeof(unsigned long long), cudaMemcpyDeviceToHost),
            "trace copy");

@@ -30,7 +30,7 @@ struct __align__(16) ItemDev {
   int first;       // inverse pass 2: first chunk of the image (initialise A)
   int sig_ctr;     // counter incremented when done
   int sig2_ctr;    // second counter (inverse pass 2: own column-group flag), or -1
-  int pad0;        // inverse pass 2 (warp path): bit u set if plane u of the chunk touches the group
+  int pad0;        // forward pass 1 (paired images): the second image, or -1
   int pad1;        // inverse pass 2: accumulator lane of the chunk (copy of A it accumulates into)
 };
 
@@ -50,7 +50,6 @@ struct KParams {
   const int* nyq_planes;        // [n_nyq] local plane index of each Nyquist plane
   const void* tw;               // cpx<T>[n]: exp(-2 pi i m / n)
   const void* rtab;             // T[(j0+1)][n/2+1]: radial factors psi1(4^-j Delta a), varphi(Delta a)
-  const void* colrec;           // warp path: ColRec<T> per (local plane, column), PlaneDev.rec indexes it
   const void* img;              // [batch][n][n] T
   void* coeff;                  // [batch][eta_l][n][n] cpx<T>
   void* img_out;                // [batch][n][n] T
@@ -69,13 +68,13 @@ struct KParams {
   const void* nyq_anti;         // [n_nyq][2][n] T: anti part of each Nyquist plane on the Nyquist row (0) /
                                 //   column (1), natural bin order (plan table)
   int n_rowitems;               // inverse pass-1 items per plane (row groups)
+  int rpi;                      // inverse pass 1: rows per item (a multiple of Geo::GR)
   const ItemDev* items;
   int n_items;
   const ChunkDev* chunks;
   const UnitDev* units;
   int* ctr;                     // [0] dispatch; [ctr_p1 + c]; [ctr_p2 + c]; [ctr_g + item]
   int ctr_p1, ctr_p2, ctr_g;
-  int fetch_batch;              // warp path: consecutive items a CTA takes per global fetch
   int variant;                  // 0 classic (meyerShearletSpect), 1 smooth (meyerNewShearletSpect), 2 user
   const void* usym;             // user spectra: [eta_l][n/2+1][n] T symmetric parts (ffst_user.cuh), else nullptr
   int compact;                  // f1 compact format: cube of reals + Nyquist vectors (G, H) in nyq_fwd
@@ -103,7 +102,6 @@ struct Geometry {
   int gr;            // inv pass 1: rows per tile
   int lpc;           // inv pass 2: columns per item
   size_t smem_fwd, smem_inv, smem_aux;   // dynamic shared bytes of the kernels
-  int warps;         // warp-worker path: worker warps per CTA (0: CTA-item path)
   int colpad;        // forward intermediate: row stride = ncols rounded up to a multiple of colpad
   int ncpf;          // final column pass (aux kernels, Geo): padded row stride of its output
 };
@@ -112,9 +110,6 @@ struct Geometry {
 template <typename T> Geometry geometry(int n);
 template <typename T> cudaError_t launch_spectrum(const KParams& p, int batch, cudaStream_t s);
 template <typename T> cudaError_t launch_nyq_fwd(const KParams& p, int batch, cudaStream_t s);
-template <typename T> Geometry geometry_warp(int n);
-template <typename T> cudaError_t launch_fwd_warp(const KParams& p, int grid, cudaStream_t s);
-template <typename T> cudaError_t launch_inv_warp(const KParams& p, int grid, cudaStream_t s);
 template <typename T> cudaError_t launch_fwd_main(const KParams& p, int grid, cudaStream_t s);
 template <typename T> cudaError_t launch_inv_main(const KParams& p, int grid, cudaStream_t s);
 template <typename T> cudaError_t launch_nyq_inv(const KParams& p, int batch, cudaStream_t s);

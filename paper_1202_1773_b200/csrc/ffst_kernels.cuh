@@ -126,19 +126,22 @@ __device__ __forceinline__ unsigned smid() {
 __shared__ unsigned long long s_probe[4];   // intra-item probes (trace mode)
 #define FFST_PROBE(p, i) do { if ((p).trace != nullptr && threadIdx.x == 0) s_probe[i] = gtimer(); } while (0)
 
-// Dependency counters.  The data behind a counter is read only through L2 (ld.global.cg, TMA),
-// so the waiting side needs no L1 invalidation: relaxed (volatile) polls.  The publishing side uses
-// red.release (MEMBAR.ALL.GPU + RED) -- __threadfence would add CCTL.IVALL, flushing the L1 copies
-// of the twiddle and radial tables on every item.
+// Dependency counters (PTX memory model).  Publishing side: red.release.gpu after the item's last
+// write (or, for a slot-reuse dependency, its last read) -- MEMBAR.ALL.GPU + RED, no L1 flush.
+// Waiting side: thread 0 polls with relaxed (volatile) loads until the counter reaches its target,
+// then executes fence.acq_rel.gpu: the poll that observed the released value plus this fence
+// synchronise with every release that contributed to it, and the CTA barrier that follows every
+// wait (__syncthreads) extends that ordering to the other threads of the CTA (the pattern of a
+// cooperative grid barrier).  So an item's reads of a producer's ring slot or accumulator lane,
+// and its writes into a slot that earlier readers release, are ordered after the dependency.
+// One fence per satisfied wait (per item), not per poll.
 __device__ __forceinline__ void spin_wait(const int* ctr, int target) {
   const volatile int* v = ctr;
   while (*v < target) __nanosleep(40);
+  asm volatile("fence.acq_rel.gpu;" ::: "memory");
 }
 __device__ __forceinline__ void red_release(int* ctr, int v) {
   asm volatile("red.release.gpu.global.add.s32 [%0], %1;" ::"l"(ctr), "r"(v) : "memory");
-}
-__device__ __forceinline__ void red_relaxed(int* ctr, int v) {
-  asm volatile("red.relaxed.gpu.global.add.s32 [%0], %1;" ::"l"(ctr), "r"(v) : "memory");
 }
 
 // Predicated cached loads (__ldg / __ldcg / __ldcs are non-volatile inline asm): the compiler may
@@ -899,8 +902,8 @@ struct K {
     if (I.type == 0) {
       const PlaneDev& P = splanes[I.p];
       C* w = static_cast<C*>(p.W) + (size_t)I.slot * p.slot_elems + I.woff;
-      const int r0 = I.group * G::RPI;
-      const int cnt = N - r0 < G::RPI ? N - r0 : G::RPI;
+      const int r0 = I.group * p.rpi;
+      const int cnt = N - r0 < p.rpi ? N - r0 : p.rpi;
       if (p.compact) {   // f1 format: real rows; the Nyquist sums come from (G, H) (nyq_compact_sums)
         const T* srcr = static_cast<const T*>(p.coeff) + ((size_t)I.b * p.eta_l + I.p) * N * N;
         if constexpr (G::PAIR_INV)
@@ -979,8 +982,7 @@ __device__ __forceinline__ void persistent_loop(const KParams& p) {
     else K<T, N>::inv_item(p, I, s_planes, smem);
     __syncthreads();
     if (threadIdx.x == 0) {
-      if (!FWD || I.type == 0) red_release(p.ctr + I.sig_ctr, 1);   // another item reads what this one wrote
-      else red_relaxed(p.ctr + I.sig_ctr, 1);                         // forward pass 2: reads only (WAR)
+      red_release(p.ctr + I.sig_ctr, 1);     // RAW (another item reads what this one wrote) or WAR (slot reuse)
       if (I.sig2_ctr >= 0) red_release(p.ctr + I.sig2_ctr, 1);
     }
     if (p.trace != nullptr && threadIdx.x == 0) {

@@ -1,6 +1,6 @@
 // ffst_launch.cuh — host launchers: runtime n -> compile-time N dispatch.
 #pragma once
-#include "ffst_warp.cuh"
+#include "ffst_kernels.cuh"
 #include "ffst_user.cuh"
 
 namespace ffst {
@@ -28,38 +28,6 @@ template <typename T, int N> struct Launch {
     g.smem_fwd = G::SMEM_FWD; g.smem_inv = G::SMEM_INV; g.smem_aux = G::SMEM_AUX;
     g.colpad = G::GC; g.ncpf = G::NCPF;
     return g;
-  }
-  // warp-worker path (n <= 512): geometry of its work items and the two persistent kernels
-  static Geometry geometry_warp() {
-    Geometry g{};
-    if constexpr (N <= 512) {
-      using WG = WGeo<T, N>;
-      g.nt = WG::NT; g.gc = WG::GC; g.rp2 = WG::RP2; g.rpi = WG::RPI; g.gr = WG::LPR; g.lpc = WG::LPC;
-      g.smem_fwd = WG::SMEM; g.smem_inv = WG::SMEM; g.smem_aux = G::SMEM_AUX;
-      g.warps = WG::NW;
-      g.colpad = WG::COLPAD; g.ncpf = G::NCPF;
-    }
-    return g;
-  }
-  static cudaError_t fwd_warp(const KParams& p, int grid, cudaStream_t s) {
-    if constexpr (N <= 512) {
-      using WG = WGeo<T, N>;
-      FFST_CHECK(set_smem(fwd_warp_kernel<T, N>, WG::SMEM));
-      fwd_warp_kernel<T, N><<<grid, WG::NT, WG::SMEM, s>>>(p);
-      return cudaGetLastError();
-    } else {
-      return cudaErrorInvalidValue;
-    }
-  }
-  static cudaError_t inv_warp(const KParams& p, int grid, cudaStream_t s) {
-    if constexpr (N <= 512) {
-      using WG = WGeo<T, N>;
-      FFST_CHECK(set_smem(inv_warp_kernel<T, N>, WG::SMEM));
-      inv_warp_kernel<T, N><<<grid, WG::NT, WG::SMEM, s>>>(p);
-      return cudaGetLastError();
-    } else {
-      return cudaErrorInvalidValue;
-    }
   }
   static cudaError_t spectrum(const KParams& p, int batch, cudaStream_t s) {
     FFST_CHECK(set_smem(spec_rows_kernel<T, N>, G::SMEM_INV));
@@ -157,11 +125,6 @@ template <typename T, int N> struct Launch {
 
 #define FFST_INSTANTIATE(T)                                                                                    \
   template <> Geometry geometry<T>(int n) { FFST_DISPATCH(T, n, geometry(), Geometry{}) }                      \
-  template <> Geometry geometry_warp<T>(int n) { FFST_DISPATCH(T, n, geometry_warp(), Geometry{}) }            \
-  template <> cudaError_t launch_fwd_warp<T>(const KParams& p, int g, cudaStream_t s) {                        \
-    FFST_DISPATCH(T, p.n, fwd_warp(p, g, s), cudaErrorInvalidValue) }                                          \
-  template <> cudaError_t launch_inv_warp<T>(const KParams& p, int g, cudaStream_t s) {                        \
-    FFST_DISPATCH(T, p.n, inv_warp(p, g, s), cudaErrorInvalidValue) }                                          \
   template <> cudaError_t launch_spectrum<T>(const KParams& p, int b, cudaStream_t s) {                        \
     FFST_DISPATCH(T, p.n, spectrum(p, b, s), cudaErrorInvalidValue) }                                          \
   template <> cudaError_t launch_nyq_fwd<T>(const KParams& p, int b, cudaStream_t s) {                         \

@@ -93,18 +93,7 @@ struct PlaneDev {
   int c_lo, ncols;   // Hermitian-half column range [c_lo, c_lo + ncols), columns 0..n/2
   int ncols_pad;     // row stride of the forward intermediate
   int nyq;           // index among the plan's Nyquist planes, or -1
-  int rec;           // warp path: index of the plane's first column record (ColRec), column c_lo;
-                     // user spectra (CTA path only): local plane index (block of the table)
-};
-
-// Per-column plan record (warp path): hull of the rows where sym_i can be non-zero in this column,
-// split into |u2| <= |u1| (h), u2 > |u1| (p) and u2 < -|u1| (n) -- centred u2, inclusive, empty if
-// lo > hi -- plus the column's horizontal radial factor psi1(4^-j Delta |u1|) and 1/|u1|.
-// Computed by the host planner from the same window functions (a plan table like the radial one;
-// the window values themselves are still evaluated on the fly).
-template <typename T> struct ColRec {
-  int lo[3], hi[3];
-  T rh, inv_a1;
+  int rec;           // user spectra: local plane index (block of the table)
 };
 
 // Radial factors.  psi1_hat(4^-j Delta a) and varphi(Delta a) depend only on the integer
@@ -226,51 +215,6 @@ FFST_HD bool col_candidate(const ColBounds& b, int u2) {
   const int a2 = u2 < 0 ? -u2 : u2;
   return (u2 >= b.hlo && u2 <= b.hhi) || (a2 >= b.alo && a2 <= b.ahi);
 }
-
-// Window along one column u1 (fixed), evaluated at rows u2 -- the same function as window()
-// with the per-column quantities hoisted: the horizontal radial factor psi1(4^-j Delta |u1|)
-// and 1/|u1| (so the horizontal shear argument costs one multiply instead of a division).
-// The radial table `rt` is the Radial table (rows j < j0: psi1, row j0: varphi), here
-// typically a shared-memory copy.  Rounding differs from window() by <= 1 ulp of the
-// argument of v.
-template <typename T> struct ColWin {
-  const T* rt;
-  int stride, j0;
-  int kind, j, k, K, u1, a1;
-  T rh, inv_a1;
-  FFST_HD ColWin(const PlaneDev& P, int u1_, const T* rt_, int stride_, int j0_)
-      : rt(rt_), stride(stride_), j0(j0_), kind(P.kind), j(P.j), k(P.k), K(1 << P.j), u1(u1_) {
-    a1 = u1 < 0 ? -u1 : u1;
-    rh = (kind == 1 || kind == 3) ? rt[j * stride + a1] : T(0);
-    inv_a1 = a1 > 0 ? T(1) / T(a1) : T(0);
-  }
-  FFST_HD ColWin(const PlaneDev& P, int u1_, const T* rt_, int stride_, int j0_, T rh_, T inv_)
-      : rt(rt_), stride(stride_), j0(j0_), kind(P.kind), j(P.j), k(P.k), K(1 << P.j), u1(u1_), rh(rh_),
-        inv_a1(inv_) {
-    a1 = u1 < 0 ? -u1 : u1;
-    if (kind != 1 && kind != 3) rh = T(0);
-  }
-  FFST_HD T eval(int u2) const {
-    const int a2 = u2 < 0 ? -u2 : u2;
-    if (kind == 0) return rt[j0 * stride + (a2 <= a1 ? a1 : a2)];          // eq:phi
-    if (kind != 2 && (a2 < a1 || (kind == 3 && a2 == a1))) {                // horizontal formula
-      if (rh == T(0)) return T(0);
-      const int num = k * u1 + K * u2;
-      const int anum = num < 0 ? -num : num;
-      if (anum >= a1) return T(0);
-      return rh * sqrt(meyer_v<T>(T(a1 - anum) * inv_a1));
-    }
-    if (kind != 1 && a1 < a2) {                                             // vertical formula
-      const T r = rt[j * stride + a2];
-      if (r == T(0)) return T(0);
-      const int num = k * u2 + K * u1;
-      const int anum = num < 0 ? -num : num;
-      if (anum >= a2) return T(0);
-      return r * sqrt(meyer_v<T>(T(a2 - anum) / T(a2)));
-    }
-    return T(0);
-  }
-};
 
 // natural FFT bin -> centred frequency in [-n/2, n/2)
 FFST_HD int centred(int bin, int n) { return bin < (n >> 1) ? bin : bin - n; }

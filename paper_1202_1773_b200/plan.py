@@ -57,6 +57,20 @@ def plane_is_nyquist(n: int, index: int, j0: int = 0) -> bool:
     return bool(v.value)
 
 
+def _check_buf(t, shape, dtype, device, what):
+    """Caller buffers reach the C ABI only with the exact shape, dtype, device and layout the
+    call reads or writes (the library trusts the sizes it is given)."""
+    if not torch.is_tensor(t):
+        raise ValueError(f"{what}: a torch tensor is required")
+    dev_ok = (t.device.type == "cpu") if device == "cpu" else (t.device == device)
+    if tuple(t.shape) != tuple(shape) or t.dtype != dtype or not dev_ok or not t.is_contiguous():
+        where = "host memory" if device == "cpu" else str(device)
+        raise ValueError(f"{what}: expected a contiguous {dtype} tensor of shape {tuple(shape)} in {where}, "
+                         f"got {t.dtype} {tuple(t.shape)} on {t.device}"
+                         f"{'' if t.is_contiguous() else ' (not contiguous)'}")
+    return t
+
+
 def _stream_handle(stream, device):
     if stream is None:
         stream = torch.cuda.current_stream(device)
@@ -111,6 +125,16 @@ class Plan:
         check(lib.ffst_plan_local_planes(self._h, C.byref(cnt), idx), "ffst_plan_local_planes")
         self.local_planes = list(idx)
         self.shard_rank, self.shard_count = int(shard_rank), int(shard_count)
+        self._reserved = {self.batch}
+
+    def reserve(self, batch: int):
+        """Build the work queue for calls with `batch` images (ffst_plan_reserve: allocates and
+        synchronises; the transform calls themselves never do).  Done on first use of a batch size."""
+        b = int(batch)
+        if b not in self._reserved:
+            with torch.cuda.device(self.device):
+                check(lib.ffst_plan_reserve(self._h, b), "ffst_plan_reserve")
+            self._reserved.add(b)
 
     # -------------------------------------------------------------- buffers
     def empty_coeffs(self, batch: int | None = None):
@@ -137,8 +161,8 @@ class Plan:
         x = self._check_images(x)
         b = x.shape[0]
         out = self.empty_coeffs(b) if out is None else out
-        if out.dtype != self.cdtype or not out.is_contiguous() or out.shape != (b, self.eta_local, self.n, self.n):
-            raise ValueError("bad output cube")
+        _check_buf(out, (b, self.eta_local, self.n, self.n), self.cdtype, self.device, "output cube")
+        self.reserve(b)
         check(lib.ffst_sheartrans_batch(self._h, C.c_void_p(x.data_ptr()), C.c_void_p(out.data_ptr()), b,
                                         _stream_handle(stream, self.device)), "ffst_sheartrans_batch")
         return out
@@ -155,24 +179,36 @@ class Plan:
         if b < 1 or b > self.batch:
             raise ValueError(f"batch {b} outside 1..{self.batch}")
         out = self.empty_images(b) if out is None else out
+        _check_buf(out, (b, self.n, self.n), self.dtype, self.device, "output images")
+        self.reserve(b)
         check(lib.ffst_inversesheartrans_batch(self._h, C.c_void_p(c.data_ptr()), C.c_void_p(out.data_ptr()), b,
                                                _stream_handle(stream, self.device)), "ffst_inversesheartrans_batch")
         return out
 
     def forward_host(self, x_host, out=None, stream=None):
         """Forward from a host (ideally pinned) tensor; the H2D copy runs inside the C call."""
-        if x_host.device.type != "cpu" or x_host.dtype != self.dtype:
-            raise ValueError("host images of the plan dtype expected")
+        if x_host.dim() == 2:
+            x_host = x_host.unsqueeze(0)
         x_host = x_host.contiguous()
-        b = x_host.shape[0] if x_host.dim() == 3 else 1
+        b = x_host.shape[0]
+        if b < 1 or b > self.batch:
+            raise ValueError(f"batch {b} outside 1..{self.batch}")
+        _check_buf(x_host, (b, self.n, self.n), self.dtype, "cpu", "host images")
         out = self.empty_coeffs(b) if out is None else out
+        _check_buf(out, (b, self.eta_local, self.n, self.n), self.cdtype, self.device, "output cube")
+        self.reserve(b)
         check(lib.ffst_sheartrans_host(self._h, C.c_void_p(x_host.data_ptr()), C.c_void_p(out.data_ptr()), b,
                                        _stream_handle(stream, self.device)), "ffst_sheartrans_host")
         return out
 
     def inverse_host(self, c, out_host, stream=None):
         """Inverse into a host (ideally pinned) tensor; the D2H copy runs inside the C call."""
-        b = c.shape[0]
+        b = c.shape[0] if c.dim() == 4 else 0
+        if b < 1 or b > self.batch:
+            raise ValueError(f"batch {b} outside 1..{self.batch}")
+        _check_buf(c, (b, self.eta_local, self.n, self.n), self.cdtype, self.device, "coefficient cube")
+        _check_buf(out_host, (b, self.n, self.n), self.dtype, "cpu", "host output images")
+        self.reserve(b)
         check(lib.ffst_inversesheartrans_host(self._h, C.c_void_p(c.data_ptr()), C.c_void_p(out_host.data_ptr()), b,
                                               _stream_handle(stream, self.device)), "ffst_inversesheartrans_host")
         return out_host
@@ -202,6 +238,9 @@ class Plan:
         nn = max(1, len(self.nyquist_planes()))
         out = torch.empty((b, self.eta_local, self.n, self.n), dtype=self.dtype, device=self.device) if out is None else out
         gh = torch.zeros((b, nn, 2, self.n), dtype=self.dtype, device=self.device) if gh is None else gh
+        _check_buf(out, (b, self.eta_local, self.n, self.n), self.dtype, self.device, "compact real parts")
+        _check_buf(gh, (b, nn, 2, self.n), self.dtype, self.device, "compact Nyquist vectors")
+        self.reserve(b)
         check(lib.ffst_sheartrans_compact(self._h, C.c_void_p(x.data_ptr()), C.c_void_p(out.data_ptr()),
                                           C.c_void_p(gh.data_ptr()), b, _stream_handle(stream, self.device)),
               "ffst_sheartrans_compact")
@@ -211,8 +250,15 @@ class Plan:
         """Inverse from the compact format (see forward_compact)."""
         re = re.contiguous()
         gh = gh.contiguous()
-        b = re.shape[0]
+        b = re.shape[0] if re.dim() == 4 else 0
+        if b < 1 or b > self.batch:
+            raise ValueError(f"batch {b} outside 1..{self.batch}")
+        nn = max(1, len(self.nyquist_planes()))
+        _check_buf(re, (b, self.eta_local, self.n, self.n), self.dtype, self.device, "compact real parts")
+        _check_buf(gh, (b, nn, 2, self.n), self.dtype, self.device, "compact Nyquist vectors")
         out = self.empty_images(b) if out is None else out
+        _check_buf(out, (b, self.n, self.n), self.dtype, self.device, "output images")
+        self.reserve(b)
         check(lib.ffst_inversesheartrans_compact(self._h, C.c_void_p(re.data_ptr()), C.c_void_p(gh.data_ptr()),
                                                  C.c_void_p(out.data_ptr()), b, _stream_handle(stream, self.device)),
               "ffst_inversesheartrans_compact")

@@ -55,12 +55,9 @@ def test_spectra_match_oracle(F, n, dtype):
 
 # ------------------------------------------------------------------ forward / inverse, small sizes
 
-@pytest.mark.parametrize("path", ["cta", "warp"])
 @pytest.mark.parametrize("n", [4, 8, 16, 32, 64, 128])
 @pytest.mark.parametrize("dtype", [torch.float64, torch.float32])
-def test_forward_inverse_small(F, n, dtype, path, monkeypatch):
-    # both execution schemes: CTA-item kernels (default) and warp-worker kernels (FFST_PATH=warp)
-    monkeypatch.setenv("FFST_PATH", path)
+def test_forward_inverse_small(F, n, dtype):
     batch = 3
     x, xo = images(2, batch, n, dtype)
     plan = F.Plan(n, batch, dtype)
@@ -135,12 +132,10 @@ def test_batch_subset_and_determinism(F):
     assert torch.equal(r1, r2)
 
 
-@pytest.mark.parametrize("path", ["cta", "warp"])
-def test_determinism_config2(F, path, monkeypatch):
+def test_determinism_config2(F):
     # at the bench's launch configuration (paired forward items, accumulator lanes, the side stream
     # of the Nyquist correction): bitwise reproducible, and each image's result independent of the
     # batch it is computed in (same arithmetic, same summation order)
-    monkeypatch.setenv("FFST_PATH", path)
     cfg = synth.config(2)
     x, _ = images(2, cfg.batch, cfg.n, torch.float32)
     xd = x.cuda()
@@ -208,14 +203,11 @@ def _check_forward_planes(c_gpu, x64, planes, tol, n):
     return max(errs)
 
 
-@pytest.mark.parametrize("path,env", [("cta", {}), ("warp", {}),
-                                      ("cta", {"FFST_RING_MB": "1", "FFST_CHUNK_PLANES": "2"}),
-                                      ("warp", {"FFST_RING_MB": "1", "FFST_CHUNK_PLANES": "2"})])
-def test_config2_full(F, path, env, monkeypatch):
-    # configs[1]: 256x256 float32 batch 16 — every plane of every image, and the inverse; both
-    # schemes, and a tiny intermediate ring (every slot reused many times: the ring-reuse and
+@pytest.mark.parametrize("env", [{}, {"FFST_RING_MB": "1", "FFST_CHUNK_PLANES": "2"}])
+def test_config2_full(F, env, monkeypatch):
+    # configs[1]: 256x256 float32 batch 16 — every plane of every image, and the inverse; also
+    # with a tiny intermediate ring (every slot reused many times: the ring-reuse and
     # accumulation-chain dependencies of the persistent scheduler are exercised)
-    monkeypatch.setenv("FFST_PATH", path)
     for k, v in env.items():
         monkeypatch.setenv(k, v)
     cfg = synth.config(2)
@@ -318,14 +310,6 @@ def test_compact_format(F, n, dtype, batch):
     assert plane_err(ce[0].cpu().numpy(), ref, np.max(np.abs(xo[0]))).max() <= TOL[dtype]
 
 
-def test_compact_warp_path_unsupported(F, monkeypatch):
-    monkeypatch.setenv("FFST_PATH", "warp")
-    plan = F.Plan(64, 1, torch.float32)
-    x = torch.zeros(1, 64, 64, device="cuda")
-    with pytest.raises(F.FFSTError):
-        plan.forward_compact(x)
-
-
 # ------------------------------------------------------------------ smooth variant
 # The oracle evaluates eq:newPsi1 as printed, sqrt(Phi^2(w/4) - Phi^2(w)), re-done in 40-digit
 # arithmetic where float64 would cancel (reading A19); the kernels use the
@@ -352,7 +336,6 @@ def test_smooth_spectra_match_oracle(F, n, dtype):
 @pytest.mark.parametrize("n", [4, 8, 16, 32, 64, 128, 256])
 @pytest.mark.parametrize("dtype", [torch.float64, torch.float32])
 def test_smooth_forward_inverse_small(F, n, dtype, monkeypatch):
-    monkeypatch.setenv("FFST_PATH", "warp")          # ignored for the smooth system (CTA kernels)
     batch = 3
     x, xo = images(2, batch, n, dtype)
     plan = F.Plan(n, batch, dtype, variant="smooth")
