@@ -355,23 +355,27 @@ def run_gpu(args, cfg):
     rsz = 4 if dtype == torch.float32 else 8
     B, N = cfg.batch, cfg.n
 
-    plan = F.Plan(N, B, dtype, device=dev, shard_rank=rank, shard_count=world)
+    comm = None
+    if world > 1:
+        from paper_1202_1773_b200.dist import create_comm
+        comm = create_comm(device=dev)              # the library's own NCCL communicator (C ABI)
+    plan = F.Plan(N, B, dtype, device=dev, shard_rank=rank, shard_count=world, nccl_comm=comm)
     eta, eta_l = plan.eta, plan.eta_local
     x_host = torch.from_numpy(synth.make_batch(cfg.cid)).to(dtype)
-    x = x_host.to(dev) if rank == 0 else torch.empty(B, N, N, dtype=dtype, device=dev)
+    x = x_host.to(dev) if rank == 0 else None
+    if x is None:
+        x = torch.empty(B, N, N, dtype=dtype, device=dev)
     cube = plan.empty_coeffs()
     rec = plan.empty_images()
     flush = torch.empty(L2_FLUSH_BYTES // 4, dtype=torch.float32, device=dev)
     stream = torch.cuda.current_stream(dev)
 
     if world > 1:
-        from paper_1202_1773_b200.dist import ShardedTransform
-        sharded = ShardedTransform(plan)
-
+        # eta-sharded: the library broadcasts the images from rank 0 and sums the partial adjoint
+        # spectra onto rank 0 (NCCL, chunked by image groups on a plan-owned stream)
         def step():
-            dist.broadcast(x, src=0)                       # images in (NCCL)
-            plan.forward(x, out=cube)                      # local planes
-            sharded.inverse(cube, out=rec)                 # partial image, NCCL reduce to rank 0
+            plan.forward(x if rank == 0 else None, out=cube, batch=B)
+            plan.inverse(cube, out=rec, root=0)
     else:
         def step():
             plan.forward(x, out=cube)

@@ -33,11 +33,17 @@
  *    FFST_ERR_CUDA with a detail string (ffst_last_error_detail, thread-local);
  *    asynchronous kernel faults surface at a later call or synchronisation.
  *  - Buffers must be 16-byte aligned and contiguous.
- *  - Multi-GPU (eta-sharding): a plan created with shard_count = G > 1 owns the
- *    planes i with (i mod G) == shard_rank; its cube holds only those planes and
- *    its inverse returns the partial image of those planes (the caller reduces the
- *    partials across ranks, e.g. with an NCCL reduce: the inverse is linear in the
- *    planes, eq:inverseShearletTransform).
+ *  - Multi-GPU (eta-sharding): a plan created with shard_count = G > 1
+ *    owns a subset of the planes (ffst_shard_planes: a cost-balanced LPT map by
+ *    default, or round robin i mod G); its cube holds only those planes.  With an
+ *    NCCL communicator in the descriptor (nccl_comm, the G ranks, rank = shard_rank)
+ *    the library runs the two exchange steps itself on a plan-owned stream, chunked
+ *    by image groups so that they overlap the kernels: the forward broadcasts the
+ *    images from rank 0, the inverse sums the ranks' partial adjoint spectra onto
+ *    `root` (the inverse is linear in the planes, eq:inverseShearletTransform,
+ *    P:L1730-1764) and only the root runs the final synthesis.  Without a
+ *    communicator the inverse returns the partial image of the local planes (the
+ *    caller reduces).
  */
 #ifndef FFST_H
 #define FFST_H
@@ -57,7 +63,7 @@ typedef enum {
   FFST_ERR_ALIGNMENT = 5,      /* buffer not 16-byte aligned */
   FFST_ERR_OOM = 6,            /* workspace allocation failed at plan creation */
   FFST_ERR_CUDA = 7,           /* CUDA runtime error (see ffst_last_error_detail) */
-  FFST_ERR_NCCL = 8,           /* reserved */
+  FFST_ERR_NCCL = 8,           /* NCCL failure (see ffst_last_error_detail) */
   FFST_ERR_UNSUPPORTED = 9     /* n not a power of two, or more local planes than built */
 } ffst_status;
 
@@ -76,6 +82,11 @@ typedef enum { FFST_KIND_LOWPASS = 0, FFST_KIND_H = 1, FFST_KIND_V = 2, FFST_KIN
 
 typedef struct ffst_plan ffst_plan;   /* opaque */
 
+/* Plane-to-rank map of a sharded plan.  LPT: planes sorted by their cost
+ * n/2 + (pruned column count) (the row pass plus the pruned column pass of each direction, in
+ * line FFTs) and dealt greedily to the least-loaded rank; ROUND_ROBIN: plane i on rank i mod G. */
+typedef enum { FFST_SHARD_LPT = 0, FFST_SHARD_ROUND_ROBIN = 1 } ffst_shard_policy;
+
 typedef struct {
   int n;              /* image side, power of two, 4 <= n <= 4096 */
   int j0;             /* number of scales; 0 = default floor(log2(n)/2) */
@@ -84,7 +95,11 @@ typedef struct {
   ffst_variant variant;
   int device;         /* CUDA device ordinal */
   int shard_rank;     /* 0 <= shard_rank < shard_count */
-  int shard_count;    /* >= 1; planes i (0-based) with i % shard_count == shard_rank are local */
+  int shard_count;    /* >= 1: the planes of ffst_shard_planes(n, j0, shard_count, shard_rank, policy) are local */
+  ffst_shard_policy shard_policy;   /* FFST_SHARD_LPT (0, default) or FFST_SHARD_ROUND_ROBIN; user-spectra
+                                       plans always use round robin */
+  void* nccl_comm;    /* ncclComm_t over the shard_count ranks (NCCL rank = shard_rank) from
+                         ffst_nccl_comm_create, or NULL (no library collectives); not owned by the plan */
 } ffst_plan_desc;
 
 /* ---- host-only queries (no device needed) ------------------------------ */
@@ -110,6 +125,23 @@ ffst_status ffst_plane_support(int n, int j0, int index, int* col_lo, int* col_h
  * anti-symmetric part on the Nyquist row/column), else 0.  A plan's own list, for either
  * variant: ffst_plan_nyquist_planes. */
 ffst_status ffst_plane_is_nyquist(int n, int j0, int index, int* is_nyquist);
+
+/* Global 0-based indices of the planes rank `shard_rank` of `shard_count` owns (ascending), for the
+ * built-in systems; j0 = 0: default.  global_indices may be NULL (count only).
+ * Errors: INVALID_SIZE, INVALID_ARG (bad shard / policy), UNSUPPORTED (n not supported). */
+ffst_status ffst_shard_planes(int n, int j0, int shard_count, int shard_rank, ffst_shard_policy policy, int* count,
+                              int* global_indices);
+
+/* ---- NCCL communicators for sharded plans -------------------------------- */
+
+/* 128 opaque bytes (an ncclUniqueId): created on one rank, shared with the others out of band
+ * (e.g. a torch.distributed broadcast), then passed to ffst_nccl_comm_create on every rank. */
+typedef struct { char bytes[128]; } ffst_nccl_id;
+ffst_status ffst_nccl_unique_id(ffst_nccl_id* id);
+/* Collective over the nranks ranks (each calls it with its rank and device).  *comm receives an
+ * ncclComm_t for ffst_plan_desc.nccl_comm.  Errors: INVALID_ARG, CUDA, NCCL. */
+ffst_status ffst_nccl_comm_create(void** comm, int nranks, int rank, const ffst_nccl_id* id, int device);
+ffst_status ffst_nccl_comm_destroy(void* comm);
 
 /* ---- plans ------------------------------------------------------------- */
 
@@ -173,20 +205,27 @@ ffst_status ffst_plan_info(const ffst_plan* plan, int* n, int* j0, int* eta, int
  * FFT bin order. */
 ffst_status ffst_shearlet_spectra(ffst_plan* plan, void* psi, int centred, void* stream);
 
-/* Forward: img [batch][n][n] real -> coeff [batch][eta_local][n][n] complex. */
+/* Forward: img [batch][n][n] real -> coeff [batch][eta_local][n][n] complex.
+ * With an NCCL communicator: img is read on rank 0 only (it may be NULL elsewhere) and broadcast
+ * to the other ranks inside the call (into the plan's staging buffer). */
 ffst_status ffst_sheartrans(ffst_plan* plan, const void* img, void* coeff, void* stream);
 ffst_status ffst_sheartrans_batch(ffst_plan* plan, const void* img, void* coeff, int batch, void* stream);
 
 /* Inverse / adjoint: coeff [batch][eta_local][n][n] complex -> img_out [batch][n][n] real
- * = Re ifft2(sum_{local i} psi_hat_i fft2(c_i)) (the full image when shard_count == 1). */
-ffst_status ffst_inversesheartrans(ffst_plan* plan, const void* coeff, void* img_out, void* stream);
-ffst_status ffst_inversesheartrans_batch(ffst_plan* plan, const void* coeff, void* img_out, int batch, void* stream);
+ * = Re ifft2(sum_i psi_hat_i fft2(c_i)).  shard_count == 1: the full image (root ignored).
+ * Sharded with an NCCL communicator: the ranks' partial adjoint spectra are summed onto rank
+ * `root`, which alone writes img_out (the full image; img_out may be NULL on other ranks).
+ * Sharded without one: img_out is the partial image of the local planes (root ignored). */
+ffst_status ffst_inversesheartrans(ffst_plan* plan, const void* coeff, void* img_out, int root, void* stream);
+ffst_status ffst_inversesheartrans_batch(ffst_plan* plan, const void* coeff, void* img_out, int batch, int root,
+                                         void* stream);
 
 /* ---- host-buffer variants (end-to-end path) ----------------------------- */
 
 /* Same as the _batch calls, with the image in HOST memory (pinned for full speed):
  * the host<->device copy of the image is issued on `stream` inside the call
- * (through a plan-owned device staging buffer).  The cube stays on the device. */
+ * (through a plan-owned device staging buffer).  The cube stays on the device.
+ * Sharded plans with a communicator: root 0 (the images are read / written on rank 0). */
 ffst_status ffst_sheartrans_host(ffst_plan* plan, const void* img_host, void* coeff, int batch, void* stream);
 ffst_status ffst_inversesheartrans_host(ffst_plan* plan, const void* coeff, void* img_host, int batch, void* stream);
 
@@ -199,11 +238,17 @@ ffst_status ffst_inversesheartrans_host(ffst_plan* plan, const void* coeff, void
  * as nyq_gh [batch][n_nyq][2][n] reals (Nyquist planes in the order of
  * ffst_plan_nyquist_planes): half the bytes of the complex cube, lossless for every cube the
  * forward produces (an arbitrary complex cube, e.g. after thresholding, is not representable:
- * use the complex entry points).  Same validation, streams and errors as the complex calls. */
+ * use the complex entry points).  Same validation, streams, errors and sharding (root 0) as the
+ * complex calls. */
 ffst_status ffst_sheartrans_compact(ffst_plan* plan, const void* img, void* coeff_re, void* nyq_gh, int batch,
                                     void* stream);
 ffst_status ffst_inversesheartrans_compact(ffst_plan* plan, const void* coeff_re, const void* nyq_gh, void* img_out,
                                            int batch, void* stream);
+/* The complex cube of a compact one (format conversion, one kernel): coeff [batch][eta_local][n][n]
+ * complex = coeff_re + i (-1)^r G_i(m1) + i (-1)^m1 H_i(r) on the Nyquist planes, coeff_re + 0 i
+ * elsewhere.  Errors: INVALID_ARG, ALIGNMENT, CUDA. */
+ffst_status ffst_expand_compact(ffst_plan* plan, const void* coeff_re, const void* nyq_gh, void* coeff, int batch,
+                                void* stream);
 /* The local Nyquist planes: count and (if local_indices != NULL) their local plane indices. */
 ffst_status ffst_plan_nyquist_planes(const ffst_plan* plan, int* count, int* local_indices);
 

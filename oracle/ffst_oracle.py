@@ -51,7 +51,11 @@ def meyer_aux(x):
     """Meyer's auxiliary function v, eq:v (Sec. 2.1):
     0 for x<0;  35x^4 - 84x^5 + 70x^6 - 20x^7 for 0<=x<=1;  1 for x>1."""
     x = np.asarray(x, dtype=np.float64)
-    poly = 35.0 * x**4 - 84.0 * x**5 + 70.0 * x**6 - 20.0 * x**7
+    x2 = x * x                      # the monomials as products (numpy's generic pow is ~10x slower)
+    x4 = x2 * x2
+    x5, x6 = x4 * x, x4 * x2
+    x7 = x6 * x
+    poly = 35.0 * x4 - 84.0 * x5 + 70.0 * x6 - 20.0 * x7
     return np.where(x < 0.0, 0.0, np.where(x > 1.0, 1.0, poly))
 
 

@@ -2,8 +2,8 @@
 transform and its adjoint as sm_100a CUDA kernels behind the C ABI of
 include/ffst.h.  See DESIGN.md."""
 from ._lib import EXPORTED, FFSTError, LIB_PATH, lib  # noqa: F401
-from .plan import (KIND_NAMES, Plan, index_to_params, num_shearlets, params_to_index,  # noqa: F401
-                   plane_is_nyquist, plane_support, scales_for_size)
+from .plan import (KIND_NAMES, NcclComm, Plan, index_to_params, num_shearlets, params_to_index,  # noqa: F401
+                   plane_is_nyquist, plane_support, scales_for_size, shard_planes)
 
-__all__ = ["Plan", "FFSTError", "scales_for_size", "num_shearlets", "index_to_params",
-           "params_to_index", "plane_support", "plane_is_nyquist", "KIND_NAMES"]
+__all__ = ["Plan", "NcclComm", "FFSTError", "scales_for_size", "num_shearlets", "index_to_params",
+           "params_to_index", "plane_support", "plane_is_nyquist", "shard_planes", "KIND_NAMES"]

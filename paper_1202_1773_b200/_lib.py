@@ -41,7 +41,11 @@ def check(status: int, where: str) -> None:
 class PlanDesc(C.Structure):
     _fields_ = [("n", C.c_int), ("j0", C.c_int), ("batch", C.c_int), ("dtype", C.c_int),
                 ("variant", C.c_int), ("device", C.c_int), ("shard_rank", C.c_int),
-                ("shard_count", C.c_int)]
+                ("shard_count", C.c_int), ("shard_policy", C.c_int), ("nccl_comm", C.c_void_p)]
+
+
+class NcclId(C.Structure):
+    _fields_ = [("bytes", C.c_char * 128)]
 
 
 _i, _p, _vp, _sz = C.c_int, C.POINTER(C.c_int), C.c_void_p, C.c_size_t
@@ -63,13 +67,18 @@ _SIGS = {
     "ffst_shearlet_spectra": (_i, [_vp, _vp, _i, _vp]),
     "ffst_sheartrans": (_i, [_vp, _vp, _vp, _vp]),
     "ffst_sheartrans_batch": (_i, [_vp, _vp, _vp, _i, _vp]),
-    "ffst_inversesheartrans": (_i, [_vp, _vp, _vp, _vp]),
-    "ffst_inversesheartrans_batch": (_i, [_vp, _vp, _vp, _i, _vp]),
+    "ffst_inversesheartrans": (_i, [_vp, _vp, _vp, _i, _vp]),
+    "ffst_inversesheartrans_batch": (_i, [_vp, _vp, _vp, _i, _i, _vp]),
+    "ffst_shard_planes": (_i, [_i, _i, _i, _i, _i, _p, _p]),
+    "ffst_nccl_unique_id": (_i, [C.POINTER(NcclId)]),
+    "ffst_nccl_comm_create": (_i, [C.POINTER(_vp), _i, _i, C.POINTER(NcclId), _i]),
+    "ffst_nccl_comm_destroy": (_i, [_vp]),
     "ffst_sheartrans_host": (_i, [_vp, _vp, _vp, _i, _vp]),
     "ffst_inversesheartrans_host": (_i, [_vp, _vp, _vp, _i, _vp]),
     "ffst_sheartrans_compact": (_i, [_vp, _vp, _vp, _vp, _i, _vp]),
     "ffst_inversesheartrans_compact": (_i, [_vp, _vp, _vp, _vp, _i, _vp]),
     "ffst_plan_nyquist_planes": (_i, [_vp, _p, _p]),
+    "ffst_expand_compact": (_i, [_vp, _vp, _vp, _vp, _i, _vp]),
     "ffst_plan_set_timing": (_i, [_vp, _i]),
     "ffst_plan_phase_times": (_i, [_vp, C.POINTER(C.c_float), _p]),
     "ffst_plan_set_trace": (_i, [_vp, _i]),

@@ -14,8 +14,24 @@ BUILD = PKG / "_build"
 LIB = PKG / "libffst.so"
 SOURCES = ["ffst_api.cu", "ffst_kern_f32.cu", "ffst_kern_f64.cu"]
 NVCC = os.environ.get("NVCC", "/usr/local/cuda/bin/nvcc")
+
+
+def _nccl_dir() -> Path:
+    """The NCCL that torch.distributed loads (nvidia-nccl wheel): headers and libnccl.so.2.  Found
+    without importing torch; the library binds to the same SONAME torch has loaded."""
+    import importlib.util
+    spec = importlib.util.find_spec("nvidia")
+    for base in (spec.submodule_search_locations if spec else []):
+        d = Path(base) / "nccl"
+        if (d / "include" / "nccl.h").exists() and (d / "lib" / "libnccl.so.2").exists():
+            return d
+    raise RuntimeError("NCCL (nvidia-nccl wheel: include/nccl.h, lib/libnccl.so.2) not found")
+
+
+NCCL = _nccl_dir()
 FLAGS = ["-std=c++17", "-O3", "--expt-relaxed-constexpr", "-lineinfo", "-gencode", "arch=compute_100a,code=sm_100a",
-         "-Xcompiler", "-fPIC", "-Xptxas", "-warn-spills", f"-I{ROOT / 'include'}", f"-I{CSRC}"]
+         "-Xcompiler", "-fPIC", "-Xptxas", "-warn-spills", f"-I{ROOT / 'include'}", f"-I{CSRC}",
+         f"-I{NCCL / 'include'}"]
 EXTRA = {}   # per-source extra flags (none)
 
 
@@ -49,7 +65,8 @@ def build(verbose: bool = False, force: bool = False) -> Path:
         list(ex.map(run, jobs))
     objs = [str(BUILD / (Path(s).stem + ".o")) for s in SOURCES]
     if force or jobs or not LIB.exists():
-        run([NVCC, "-shared", "-gencode", "arch=compute_100a,code=sm_100a", *objs, "-o", str(LIB)])
+        run([NVCC, "-shared", "-gencode", "arch=compute_100a,code=sm_100a", *objs, "-o", str(LIB),
+             f"-L{NCCL / 'lib'}", "-l:libnccl.so.2", "-Xlinker", f"-rpath={NCCL / 'lib'}"])
     return LIB
 
 

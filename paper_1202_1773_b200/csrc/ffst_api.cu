@@ -9,6 +9,7 @@
 //    item is an earlier item (deadlock-free dynamic scheduling);
 //  * all device workspace, allocated once here (no allocation per call).
 #include <cuda_runtime.h>
+#include <nccl.h>
 
 #include <algorithm>
 #include <cmath>
@@ -37,6 +38,15 @@ ffst_status cuda_fail(cudaError_t e, const char* where) {
   g_detail = std::string(where) + ": " + cudaGetErrorString(e);
   return FFST_ERR_CUDA;
 }
+
+#define API_NCCL(x, where)                                                        \
+  do {                                                                            \
+    ncclResult_t r_ = (x);                                                        \
+    if (r_ != ncclSuccess) {                                                      \
+      g_detail = std::string(where) + ": " + ncclGetErrorString(r_);              \
+      return FFST_ERR_NCCL;                                                       \
+    }                                                                             \
+  } while (0)
 
 #define API_CUDA(x, where)                       \
   do {                                           \
@@ -99,6 +109,34 @@ void plane_columns(int n, int j0, const Triple& tr, int* lo, int* hi) {
   }
   *lo = std::min(hlo, vlo);
   *hi = std::max(hhi, vhi);
+}
+
+// Plane-to-rank map.  LPT: planes by decreasing cost n/2 + (pruned column count)
+// -- the row pass plus the pruned column pass of a direction, in line FFTs -- each dealt to the
+// least-loaded rank (lowest rank on ties); round robin: plane i on rank i mod G.
+std::vector<int> shard_owner(int n, int j0, int eta, int count, int policy) {
+  std::vector<int> owner(eta);
+  if (policy == FFST_SHARD_ROUND_ROBIN || count <= 1) {
+    for (int i = 0; i < eta; ++i) owner[i] = i % std::max(1, count);
+    return owner;
+  }
+  const auto table = index_table(j0);
+  std::vector<std::pair<long, int>> order;
+  for (int i = 0; i < eta; ++i) {
+    int lo, hi;
+    plane_columns(n, j0, table[i], &lo, &hi);
+    order.push_back({-(long)(n / 2 + (hi - lo + 1)), i});
+  }
+  std::sort(order.begin(), order.end());
+  std::vector<long> load(count, 0);
+  for (auto& o : order) {
+    int r = 0;
+    for (int q = 1; q < count; ++q)
+      if (load[q] < load[r]) r = q;
+    owner[o.second] = r;
+    load[r] += -o.first;
+  }
+  return owner;
 }
 
 // Radial factor table (float64): rows j < j0: psi1_hat(4^-j Delta a) by the closed form of
@@ -252,6 +290,9 @@ struct ffst_plan {
   bool tracing = false;
   cudaEvent_t ev[8] = {};
   cudaStream_t aux = nullptr;     // side stream of the inverse (Nyquist correction beside the final column pass)
+  ncclComm_t comm = nullptr;      // desc.nccl_comm (not owned): the library's exchange steps
+  cudaStream_t cs = nullptr;      // comm stream (broadcast / reduce, chunked by image groups)
+  cudaEvent_t cev[6] = {};        // [0] start, [1..4] image groups, [5] adjoint spectra final
   cudaEvent_t fork[2] = {};
   int launches[2] = {0, 0};
   std::vector<void*> allocs;
@@ -631,14 +672,31 @@ ffst_status validate_call(ffst_plan* p, const void* a, const void* b, int batch,
   return find_queue(p, batch, q);
 }
 
+// Image groups of the library's collectives (sharded plans with an NCCL communicator): the
+// exchange of group g overlaps the kernels of the other groups.
+constexpr int COMM_GROUPS = 4;
+int comm_groups(int batch) { return std::min(batch, COMM_GROUPS); }
+void group_range(int batch, int G, int g, int* g0, int* g1) {
+  *g0 = (int)((long long)batch * g / G);
+  *g1 = (int)((long long)batch * (g + 1) / G);
+}
+ncclDataType_t nccl_type(const ffst_plan* p) { return p->d.dtype == FFST_F32 ? ncclFloat32 : ncclFloat64; }
+
+// nyq_gh != nullptr: compact (f1) format -- coeff holds the real parts, nyq_gh the Nyquist vectors.
+// With a communicator: img is read on rank 0 and broadcast (image groups on the comm stream, each
+// group's spectrum kernels start as soon as its images have arrived); other ranks receive into the
+// plan's staging buffer (img may be NULL there).
 ffst_status forward_impl(ffst_plan* p, const void* img, void* coeff, int batch, cudaStream_t s,
                          void* nyq_gh = nullptr) {
+  const bool coll = p->comm != nullptr;
+  const bool root = p->d.shard_rank == 0;
+  const void* src = coll && !root ? p->stage : img;
   Queue* q = nullptr;
-  TRY(validate_call(p, img, coeff, batch, &q));
+  TRY(validate_call(p, src, coeff, batch, &q));
   TRY(set_device(p));
   KParams k = base_params(p);
   k.batch = batch;
-  k.img = img;
+  k.img = src;
   k.coeff = coeff;
   if (nyq_gh != nullptr) {
     k.compact = 1;
@@ -656,8 +714,35 @@ ffst_status forward_impl(ffst_plan* p, const void* img, void* coeff, int batch, 
   TRY(trace_buffer(p, 0, q->n_fwd, &k));
   int nl = 0;
   if (p->timing) API_CUDA(cudaEventRecord(p->ev[0], s), "event");
-  API_CUDA(L_spectrum(p, k, batch, s), "spectrum kernels");
-  nl += 2;
+  if (coll) {
+    const size_t img_elems = (size_t)p->n * p->n;
+    const size_t h1n = (size_t)(p->n / 2 + 1) * p->n;
+    const int G = comm_groups(batch);
+    API_CUDA(cudaEventRecord(p->cev[0], s), "event");
+    API_CUDA(cudaStreamWaitEvent(p->cs, p->cev[0], 0), "stream wait");
+    for (int g = 0; g < G; ++g) {
+      int g0, g1;
+      group_range(batch, G, g, &g0, &g1);
+      const char* sb = static_cast<const char*>(src) + g0 * img_elems * p->rsz;
+      API_NCCL(ncclBroadcast(sb, const_cast<char*>(sb), (g1 - g0) * img_elems, nccl_type(p), 0, p->comm, p->cs),
+               "ncclBroadcast (images)");
+      API_CUDA(cudaEventRecord(p->cev[1 + g], p->cs), "event");
+    }
+    for (int g = 0; g < G; ++g) {
+      int g0, g1;
+      group_range(batch, G, g, &g0, &g1);
+      API_CUDA(cudaStreamWaitEvent(s, p->cev[1 + g], 0), "stream wait");
+      KParams kg = k;
+      kg.img = static_cast<const char*>(src) + g0 * img_elems * p->rsz;
+      kg.F = static_cast<char*>(p->F) + g0 * h1n * 2 * p->rsz;
+      kg.Fscr = static_cast<char*>(p->Fscr) + g0 * h1n * 2 * p->rsz;
+      API_CUDA(L_spectrum(p, kg, g1 - g0, s), "spectrum kernels");
+      nl += 2;
+    }
+  } else {
+    API_CUDA(L_spectrum(p, k, batch, s), "spectrum kernels");
+    nl += 2;
+  }
   if (!p->nyq.empty()) {
     API_CUDA(L_nyq_fwd(p, k, batch, s), "nyq_fwd kernel");
     ++nl;
@@ -673,10 +758,17 @@ ffst_status forward_impl(ffst_plan* p, const void* img, void* coeff, int batch, 
   return FFST_OK;
 }
 
-ffst_status inverse_impl(ffst_plan* p, const void* coeff, void* img_out, int batch, cudaStream_t s,
+// With a communicator: every rank forms its partial adjoint spectrum A_r (all accumulator lanes)
+// and Nyquist correction; the comm stream sums them onto `root` image group by image group
+// (ncclReduce, in place), and the root runs the final synthesis of group g while group g + 1 is
+// being reduced.  img_out is written on the root only (it may be NULL elsewhere).
+ffst_status inverse_impl(ffst_plan* p, const void* coeff, void* img_out, int batch, int root_rank, cudaStream_t s,
                          const void* nyq_gh = nullptr) {
+  const bool coll = p->comm != nullptr;
+  if (coll && (root_rank < 0 || root_rank >= p->d.shard_count)) return fail(FFST_ERR_INVALID_ARG, "root outside 0..shard_count-1");
+  const bool root = !coll || p->d.shard_rank == root_rank;
   Queue* q = nullptr;
-  TRY(validate_call(p, coeff, img_out, batch, &q));
+  TRY(validate_call(p, coeff, root ? img_out : p->stage, batch, &q));
   TRY(set_device(p));
   KParams k = base_params(p);
   k.batch = batch;
@@ -716,10 +808,49 @@ ffst_status inverse_impl(ffst_plan* p, const void* coeff, void* img_out, int bat
     API_CUDA(cudaEventRecord(p->fork[1], p->aux), "event");
     nl += 2;
   }
-  API_CUDA(L_final(p, k, batch, 0, s), "final column pass");
-  if (!p->nyq.empty()) API_CUDA(cudaStreamWaitEvent(s, p->fork[1], 0), "stream wait");
-  API_CUDA(L_final(p, k, batch, 1, s), "final row pass");
-  nl += 2;
+  if (!coll) {
+    API_CUDA(L_final(p, k, batch, 0, s), "final column pass");
+    if (!p->nyq.empty()) API_CUDA(cudaStreamWaitEvent(s, p->fork[1], 0), "stream wait");
+    API_CUDA(L_final(p, k, batch, 1, s), "final row pass");
+    nl += 2;
+  } else {
+    const size_t n = (size_t)p->n, h1n = (n / 2 + 1) * n;
+    if (!p->nyq.empty()) API_CUDA(cudaStreamWaitEvent(s, p->fork[1], 0), "stream wait");
+    API_CUDA(cudaEventRecord(p->cev[5], s), "event");              // A lanes and corr final
+    API_CUDA(cudaStreamWaitEvent(p->cs, p->cev[5], 0), "stream wait");
+    const int G = comm_groups(batch);
+    for (int g = 0; g < G; ++g) {
+      int g0, g1;
+      group_range(batch, G, g, &g0, &g1);
+      API_NCCL(ncclGroupStart(), "ncclGroupStart");
+      for (int l = 0; l < k.a_lanes; ++l) {
+        char* a = static_cast<char*>(p->A) + ((size_t)l * k.a_lane_elems + g0 * h1n) * 2 * p->rsz;
+        API_NCCL(ncclReduce(a, a, (g1 - g0) * h1n * 2, nccl_type(p), ncclSum, root_rank, p->comm, p->cs),
+                 "ncclReduce (adjoint spectra)");
+      }
+      if (!p->nyq.empty()) {
+        char* c = static_cast<char*>(p->corr) + g0 * 2 * n * p->rsz;
+        API_NCCL(ncclReduce(c, c, (g1 - g0) * 2 * n, nccl_type(p), ncclSum, root_rank, p->comm, p->cs),
+                 "ncclReduce (Nyquist correction)");
+      }
+      API_NCCL(ncclGroupEnd(), "ncclGroupEnd");
+      API_CUDA(cudaEventRecord(p->cev[1 + g], p->cs), "event");
+    }
+    for (int g = 0; g < G; ++g) {
+      API_CUDA(cudaStreamWaitEvent(s, p->cev[1 + g], 0), "stream wait");
+      if (!root) continue;
+      int g0, g1;
+      group_range(batch, G, g, &g0, &g1);
+      KParams kg = k;
+      kg.A = static_cast<char*>(p->A) + g0 * h1n * 2 * p->rsz;
+      kg.Fscr = static_cast<char*>(p->Fscr) + g0 * n * (size_t)p->geo.ncpf * 2 * p->rsz;
+      kg.img_out = static_cast<char*>(img_out) + g0 * n * n * p->rsz;
+      kg.corr = static_cast<char*>(p->corr) + g0 * 2 * n * p->rsz;
+      API_CUDA(L_final(p, kg, g1 - g0, 0, s), "final column pass");
+      API_CUDA(L_final(p, kg, g1 - g0, 1, s), "final row pass");
+      nl += 2;
+    }
+  }
   if (p->timing) API_CUDA(cudaEventRecord(p->ev[6], s), "event");
   p->launches[1] = nl;
   return FFST_OK;
@@ -850,6 +981,55 @@ ffst_status ffst_plane_is_nyquist(int n, int j0, int index, int* is_nyquist) {
   return FFST_OK;
 }
 
+ffst_status ffst_shard_planes(int n, int j0, int shard_count, int shard_rank, ffst_shard_policy policy, int* count,
+                              int* global_indices) {
+  if (!count) return fail(FFST_ERR_INVALID_ARG, "null output");
+  if (n < 4) return fail(FFST_ERR_INVALID_SIZE, "n < 4");
+  if (!is_pow2(n)) return fail(FFST_ERR_UNSUPPORTED, "n must be a power of two");
+  if (j0 == 0) j0 = default_j0(n);
+  if (j0 < 1 || j0 > 12) return fail(FFST_ERR_INVALID_ARG, "j0 outside 1..12");
+  if (policy != FFST_SHARD_LPT && policy != FFST_SHARD_ROUND_ROBIN) return fail(FFST_ERR_INVALID_ARG, "unknown policy");
+  const int eta = ffst_num_shearlets(j0);
+  if (shard_count < 1 || shard_count > eta || shard_rank < 0 || shard_rank >= shard_count)
+    return fail(FFST_ERR_INVALID_ARG, "bad shard_rank / shard_count");
+  const std::vector<int> owner = shard_owner(n, j0, eta, shard_count, policy);
+  int c = 0;
+  for (int i = 0; i < eta; ++i)
+    if (owner[i] == shard_rank) {
+      if (global_indices) global_indices[c] = i;
+      ++c;
+    }
+  *count = c;
+  return FFST_OK;
+}
+
+ffst_status ffst_nccl_unique_id(ffst_nccl_id* id) {
+  static_assert(sizeof(ffst_nccl_id) == sizeof(ncclUniqueId), "ffst_nccl_id must hold an ncclUniqueId");
+  if (!id) return fail(FFST_ERR_INVALID_ARG, "null id");
+  ncclUniqueId u;
+  API_NCCL(ncclGetUniqueId(&u), "ncclGetUniqueId");
+  std::memcpy(id, &u, sizeof(u));
+  return FFST_OK;
+}
+
+ffst_status ffst_nccl_comm_create(void** comm, int nranks, int rank, const ffst_nccl_id* id, int device) {
+  if (!comm || !id) return fail(FFST_ERR_INVALID_ARG, "null argument");
+  if (nranks < 1 || rank < 0 || rank >= nranks) return fail(FFST_ERR_INVALID_ARG, "bad rank / nranks");
+  API_CUDA(cudaSetDevice(device), "cudaSetDevice");
+  ncclUniqueId u;
+  std::memcpy(&u, id, sizeof(u));
+  ncclComm_t c = nullptr;
+  API_NCCL(ncclCommInitRank(&c, nranks, u, rank), "ncclCommInitRank");
+  *comm = c;
+  return FFST_OK;
+}
+
+ffst_status ffst_nccl_comm_destroy(void* comm) {
+  if (!comm) return FFST_OK;
+  API_NCCL(ncclCommDestroy(static_cast<ncclComm_t>(comm)), "ncclCommDestroy");
+  return FFST_OK;
+}
+
 ffst_status ffst_plan_destroy(ffst_plan* p) {
   if (!p) return FFST_OK;
   int cur = -1;
@@ -861,6 +1041,9 @@ ffst_status ffst_plan_destroy(ffst_plan* p) {
   for (auto& e : p->fork)
     if (e) cudaEventDestroy(e);
   if (p->aux) cudaStreamDestroy(p->aux);
+  for (auto& e : p->cev)
+    if (e) cudaEventDestroy(e);
+  if (p->cs) cudaStreamDestroy(p->cs);
   if (cur >= 0) cudaSetDevice(cur);
   delete p;
   return FFST_OK;
@@ -909,8 +1092,14 @@ static ffst_status plan_create_impl(ffst_plan** out, const ffst_plan_desc* d_in,
   p->rsz = d->dtype == FFST_F32 ? 4 : 8;
   p->delta = grid_delta(d->n, j0);
   p->geo = d->dtype == FFST_F32 ? geometry<float>(d->n) : geometry<double>(d->n);
+  if (d->shard_policy != FFST_SHARD_LPT && d->shard_policy != FFST_SHARD_ROUND_ROBIN)
+    return fail(FFST_ERR_INVALID_ARG, "unknown shard policy");
   const auto table = index_table(j0);
-  for (int i = d->shard_rank; i < eta; i += d->shard_count) {
+  // plane-to-rank map: LPT by default (user spectra: round robin, the order ffst_user.cuh reads)
+  const std::vector<int> owner = us ? shard_owner(d->n, j0, eta, d->shard_count, FFST_SHARD_ROUND_ROBIN)
+                                    : shard_owner(d->n, j0, eta, d->shard_count, d->shard_policy);
+  for (int i = 0; i < eta; ++i) {
+    if (owner[i] != d->shard_rank) continue;
     PlaneDev P{};
     P.gi = i;
     P.rec = (int)p->planes.size();
@@ -1086,6 +1275,19 @@ static ffst_status plan_create_impl(ffst_plan** out, const ffst_plan_desc* d_in,
   }
   e = cudaStreamCreateWithFlags(&p->aux, cudaStreamNonBlocking);
   if (e != cudaSuccess) return cleanup(cuda_fail(e, "stream create"));
+  if (d->nccl_comm != nullptr) {
+    // the library's exchange steps: the communicator must be the shard_count ranks, rank = shard_rank
+    p->comm = static_cast<ncclComm_t>(d->nccl_comm);
+    int cn = 0, cr = -1;
+    if (ncclCommCount(p->comm, &cn) != ncclSuccess || ncclCommUserRank(p->comm, &cr) != ncclSuccess)
+      return cleanup(fail(FFST_ERR_NCCL, "nccl_comm is not a valid communicator"));
+    if (cn != d->shard_count || cr != d->shard_rank)
+      return cleanup(fail(FFST_ERR_INVALID_ARG, "nccl_comm size / rank differ from shard_count / shard_rank"));
+    e = cudaStreamCreateWithFlags(&p->cs, cudaStreamNonBlocking);
+    for (auto& ev : p->cev)
+      if (e == cudaSuccess) e = cudaEventCreateWithFlags(&ev, cudaEventDisableTiming);
+    if (e != cudaSuccess) return cleanup(cuda_fail(e, "comm stream / events"));
+  }
   Queue* q = nullptr;
   st = build_queue(p, d->batch, &q);
   if (st != FFST_OK) return cleanup(st);
@@ -1181,36 +1383,42 @@ ffst_status ffst_sheartrans(ffst_plan* p, const void* img, void* coeff, void* st
   return forward_impl(p, img, coeff, p->d.batch, static_cast<cudaStream_t>(stream));
 }
 
-ffst_status ffst_inversesheartrans_batch(ffst_plan* p, const void* coeff, void* img, int batch, void* stream) {
+ffst_status ffst_inversesheartrans_batch(ffst_plan* p, const void* coeff, void* img, int batch, int root,
+                                         void* stream) {
   if (!p) return fail(FFST_ERR_INVALID_ARG, "null plan");
-  return inverse_impl(p, coeff, img, batch, static_cast<cudaStream_t>(stream));
+  return inverse_impl(p, coeff, img, batch, root, static_cast<cudaStream_t>(stream));
 }
 
-ffst_status ffst_inversesheartrans(ffst_plan* p, const void* coeff, void* img, void* stream) {
+ffst_status ffst_inversesheartrans(ffst_plan* p, const void* coeff, void* img, int root, void* stream) {
   if (!p) return fail(FFST_ERR_INVALID_ARG, "null plan");
-  return inverse_impl(p, coeff, img, p->d.batch, static_cast<cudaStream_t>(stream));
+  return inverse_impl(p, coeff, img, p->d.batch, root, static_cast<cudaStream_t>(stream));
 }
 
+// Host-buffer variants: sharded plans with a communicator read / write the host images on rank 0.
 ffst_status ffst_sheartrans_host(ffst_plan* p, const void* img_host, void* coeff, int batch, void* stream) {
-  if (!p || !img_host) return fail(FFST_ERR_INVALID_ARG, "null argument");
+  if (!p) return fail(FFST_ERR_INVALID_ARG, "null plan");
+  const bool reads = p->comm == nullptr || p->d.shard_rank == 0;
+  if (reads && !img_host) return fail(FFST_ERR_INVALID_ARG, "null argument");
   Queue* q = nullptr;
   TRY(validate_call(p, p->stage, coeff, batch, &q));          // everything checked before the copy
   TRY(set_device(p));
   cudaStream_t s = static_cast<cudaStream_t>(stream);
   const size_t bytes = (size_t)batch * p->n * p->n * p->rsz;
-  API_CUDA(cudaMemcpyAsync(p->stage, img_host, bytes, cudaMemcpyHostToDevice, s), "H2D image copy");
+  if (reads) API_CUDA(cudaMemcpyAsync(p->stage, img_host, bytes, cudaMemcpyHostToDevice, s), "H2D image copy");
   return forward_impl(p, p->stage, coeff, batch, s);
 }
 
 ffst_status ffst_inversesheartrans_host(ffst_plan* p, const void* coeff, void* img_host, int batch, void* stream) {
-  if (!p || !img_host) return fail(FFST_ERR_INVALID_ARG, "null argument");
+  if (!p) return fail(FFST_ERR_INVALID_ARG, "null plan");
+  const bool writes = p->comm == nullptr || p->d.shard_rank == 0;
+  if (writes && !img_host) return fail(FFST_ERR_INVALID_ARG, "null argument");
   Queue* q = nullptr;
   TRY(validate_call(p, coeff, p->stage, batch, &q));
   TRY(set_device(p));
   cudaStream_t s = static_cast<cudaStream_t>(stream);
-  TRY(inverse_impl(p, coeff, p->stage, batch, s));
+  TRY(inverse_impl(p, coeff, p->stage, batch, 0, s));
   const size_t bytes = (size_t)batch * p->n * p->n * p->rsz;
-  API_CUDA(cudaMemcpyAsync(img_host, p->stage, bytes, cudaMemcpyDeviceToHost, s), "D2H image copy");
+  if (writes) API_CUDA(cudaMemcpyAsync(img_host, p->stage, bytes, cudaMemcpyDeviceToHost, s), "D2H image copy");
   return FFST_OK;
 }
 
@@ -1225,7 +1433,24 @@ ffst_status ffst_inversesheartrans_compact(ffst_plan* p, const void* coeff_re, c
                                            int batch, void* stream) {
   if (!p || !nyq_gh) return fail(FFST_ERR_INVALID_ARG, "null argument");
   if (!aligned16(nyq_gh)) return fail(FFST_ERR_ALIGNMENT, "buffers must be 16-byte aligned");
-  return inverse_impl(p, coeff_re, img, batch, static_cast<cudaStream_t>(stream), nyq_gh);
+  return inverse_impl(p, coeff_re, img, batch, 0, static_cast<cudaStream_t>(stream), nyq_gh);
+}
+
+ffst_status ffst_expand_compact(ffst_plan* p, const void* coeff_re, const void* nyq_gh, void* coeff, int batch,
+                                void* stream) {
+  if (!p) return fail(FFST_ERR_INVALID_ARG, "null plan");
+  if (!coeff_re || !nyq_gh || !coeff) return fail(FFST_ERR_INVALID_ARG, "null buffer");
+  if (batch < 1 || batch > p->d.batch) return fail(FFST_ERR_INVALID_ARG, "batch outside 1..plan batch");
+  if (!aligned16(coeff_re) || !aligned16(nyq_gh) || !aligned16(coeff))
+    return fail(FFST_ERR_ALIGNMENT, "buffers must be 16-byte aligned");
+  if (p->n % 2 != 0) return fail(FFST_ERR_UNSUPPORTED, "compact format: even n only");
+  TRY(set_device(p));
+  KParams k = base_params(p);
+  const cudaError_t e = p->d.dtype == FFST_F32
+      ? launch_expand_compact<float>(k, coeff_re, nyq_gh, coeff, batch, static_cast<cudaStream_t>(stream))
+      : launch_expand_compact<double>(k, coeff_re, nyq_gh, coeff, batch, static_cast<cudaStream_t>(stream));
+  if (e != cudaSuccess) return cuda_fail(e, "expand_compact kernel");
+  return FFST_OK;
 }
 
 ffst_status ffst_plan_nyquist_planes(const ffst_plan* p, int* count, int* local_indices) {

@@ -117,6 +117,8 @@ template <typename T> cudaError_t launch_nyq_compact_sums(const KParams& p, int 
 template <typename T> cudaError_t launch_final(const KParams& p, int batch, int which, cudaStream_t s);
 template <typename T> cudaError_t launch_user_prepare(const UserPrep& u, int grid, cudaStream_t s);
 template <typename T> cudaError_t launch_spectra_export(const KParams& p, void* psi, int centred, cudaStream_t s);
+template <typename T> cudaError_t launch_expand_compact(const KParams& p, const void* re, const void* gh, void* out,
+                                                        int batch, cudaStream_t s);
 template <typename T> int max_active_main(int n, int device, int which);   // CTAs/SM of fwd (0) / inv (1)
 
 }  // namespace ffst

@@ -1246,6 +1246,33 @@ __global__ void __launch_bounds__(256) nyq_compact_sums_kernel(KParams p) {
   }
 }
 
+// Compact format (f1) -> complex cube: c_i(r, m1) = x_i(r, m1) + i [(-1)^r G_i(m1) + (-1)^m1 H_i(r)] on
+// the Nyquist planes, x_i + 0 i elsewhere.  Grid-stride over the cube, two
+// elements per thread (16-byte stores).
+template <typename T>
+__global__ void __launch_bounds__(256) expand_compact_kernel(const PlaneDev* planes, int n, int eta_l, int n_nyq,
+                                                             const T* re, const T* gh, cpx<T>* out, long long pairs) {
+  for (long long e = blockIdx.x * (long long)blockDim.x + threadIdx.x; e < pairs; e += (long long)gridDim.x * blockDim.x) {
+    const long long i0 = 2 * e;                      // element index (n even: a pair never spans rows)
+    const int m = (int)(i0 % n);
+    const long long row = i0 / n;
+    const int r = (int)(row % n);
+    const long long bp = row / n;                    // b * eta_l + local plane
+    const int lp = (int)(bp % eta_l), b = (int)(bp / eta_l);
+    const int q = planes[lp].nyq;
+    T y0 = T(0), y1 = T(0);
+    if (q >= 0) {
+      const T* g = gh + ((size_t)b * n_nyq + q) * 2 * n;
+      const T sr = (r & 1) ? T(-1) : T(1);
+      const T h = g[n + r];
+      y0 = sr * g[m] + h;                            // m even
+      y1 = sr * g[m + 1] - h;                        // m + 1 odd
+    }
+    const cpx<T> a = mk<T>(re[i0], y0), c = mk<T>(re[i0 + 1], y1);
+    store_pair_cs<T>(out + i0, a, c);
+  }
+}
+
 // materialise spectra (tests only): psi[i][row][col], grid-stride
 template <typename T, int N>
 __global__ void spectra_kernel(KParams p, T* psi, int centred_layout) {

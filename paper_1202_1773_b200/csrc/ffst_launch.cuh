@@ -1,5 +1,6 @@
 // ffst_launch.cuh — host launchers: runtime n -> compile-time N dispatch.
 #pragma once
+#include <algorithm>
 #include "ffst_kernels.cuh"
 #include "ffst_user.cuh"
 
@@ -141,6 +142,13 @@ template <typename T, int N> struct Launch {
     FFST_DISPATCH(T, p.n, final_(p, b, which, s), cudaErrorInvalidValue) }                                            \
   template <> cudaError_t launch_spectra_export<T>(const KParams& p, void* psi, int c, cudaStream_t s) {       \
     FFST_DISPATCH(T, p.n, spectra(p, psi, c, s), cudaErrorInvalidValue) }                                      \
+  template <> cudaError_t launch_expand_compact<T>(const KParams& p, const void* re, const void* gh, void* out,  \
+                                                   int batch, cudaStream_t s) {                                 \
+    const long long pairs = (long long)batch * p.eta_l * p.n * p.n / 2;                                       \
+    const int grid = (int)std::min<long long>((pairs + 255) / 256, 148LL * 16);                                \
+    expand_compact_kernel<T><<<grid < 1 ? 1 : grid, 256, 0, s>>>(p.planes, p.n, p.eta_l, p.n_nyq,             \
+        static_cast<const T*>(re), static_cast<const T*>(gh), static_cast<cpx<T>*>(out), pairs);              \
+    return cudaGetLastError(); }                                                                               \
   template <> cudaError_t launch_user_prepare<T>(const UserPrep& u, int grid, cudaStream_t s) {              \
     return user_prepare_<T>(u, grid, s); }                                                                     \
   template <> int max_active_main<T>(int n, int device, int which) {                                           \

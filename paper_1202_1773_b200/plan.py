@@ -17,6 +17,7 @@ KIND_NAMES = {0: "lowpass", 1: "h", 2: "v", 3: "x"}
 _DTYPES = {torch.float32: 0, torch.float64: 1}
 _CDTYPES = {torch.float32: torch.complex64, torch.float64: torch.complex128}
 _VARIANTS = {"classic": 0, "smooth": 1, "user": 2}
+_POLICIES = {"lpt": 0, "round_robin": 1}
 
 
 def scales_for_size(n: int) -> int:
@@ -51,6 +52,44 @@ def plane_support(n: int, index: int, j0: int = 0):
     return lo.value, hi.value
 
 
+def shard_planes(n: int, shard_count: int, shard_rank: int, policy: str = "lpt", j0: int = 0):
+    """Global 0-based indices of the planes rank `shard_rank` owns (host-only)."""
+    cnt = C.c_int()
+    check(lib.ffst_shard_planes(int(n), int(j0), int(shard_count), int(shard_rank), _POLICIES[policy],
+                                C.byref(cnt), None), "ffst_shard_planes")
+    idx = (C.c_int * max(1, cnt.value))()
+    check(lib.ffst_shard_planes(int(n), int(j0), int(shard_count), int(shard_rank), _POLICIES[policy],
+                                C.byref(cnt), idx), "ffst_shard_planes")
+    return [idx[i] for i in range(cnt.value)]
+
+
+class NcclComm:
+    """An NCCL communicator owned by the library's side of the boundary (ffst_nccl_comm_create):
+    rank 0 creates the unique id, the ranks exchange it out of band (torch.distributed), every rank
+    joins.  Passed to Plan(nccl_comm=...) so that the library runs the exchange steps itself."""
+
+    def __init__(self, nranks: int, rank: int, device: int, unique_id: bytes):
+        from ._lib import NcclId
+        nid = NcclId()
+        C.memmove(C.addressof(nid), unique_id, 128)
+        h = C.c_void_p()
+        check(lib.ffst_nccl_comm_create(C.byref(h), int(nranks), int(rank), C.byref(nid), int(device)),
+              "ffst_nccl_comm_create")
+        self.handle, self.nranks, self.rank = h, int(nranks), int(rank)
+
+    @staticmethod
+    def unique_id() -> bytes:
+        from ._lib import NcclId
+        nid = NcclId()
+        check(lib.ffst_nccl_unique_id(C.byref(nid)), "ffst_nccl_unique_id")
+        return C.string_at(C.addressof(nid), 128)
+
+    def close(self):
+        if getattr(self, "handle", None):
+            lib.ffst_nccl_comm_destroy(self.handle)
+            self.handle = None
+
+
 def plane_is_nyquist(n: int, index: int, j0: int = 0) -> bool:
     v = C.c_int()
     check(lib.ffst_plane_is_nyquist(int(n), int(j0), int(index), C.byref(v)), "ffst_plane_is_nyquist")
@@ -80,12 +119,14 @@ def _stream_handle(stream, device):
 class Plan:
     """A forward/inverse FFST plan for n x n images on one CUDA device.
 
-    ``shard_rank``/``shard_count`` select the planes i (0-based) with
-    i % shard_count == shard_rank (eta-sharding, DESIGN.md "Multi-GPU")."""
+    ``shard_rank``/``shard_count`` select the planes of ``shard_planes`` (eta-sharding, DESIGN.md
+    "Multi-GPU"; ``shard_policy`` "lpt" or "round_robin").  With ``nccl_comm`` (a ``NcclComm`` of
+    the shard_count ranks) the library broadcasts the images from rank 0 in ``forward`` and sums
+    the ranks' partial adjoints onto ``root`` in ``inverse``."""
 
     def __init__(self, n: int, batch: int = 1, dtype=torch.float32, device=None, j0: int = 0,
                  shard_rank: int = 0, shard_count: int = 1, variant: str = "classic",
-                 spectra=None, centred: bool = True):
+                 spectra=None, centred: bool = True, shard_policy: str = "lpt", nccl_comm=None):
         if not torch.cuda.is_available():
             raise RuntimeError("FFST Plan needs a CUDA device (no CPU fallback)")
         if dtype not in _DTYPES:
@@ -99,8 +140,12 @@ class Plan:
         elif variant not in _VARIANTS or variant == "user":
             raise ValueError("variant must be 'classic' (meyerShearletSpect) or 'smooth' (meyerNewShearletSpect)")
         self.variant = variant
+        if shard_policy not in _POLICIES:
+            raise ValueError("shard_policy must be 'lpt' or 'round_robin'")
+        self.comm = nccl_comm
         desc = PlanDesc(int(n), int(j0), int(batch), _DTYPES[dtype], _VARIANTS[variant], self.device.index,
-                        int(shard_rank), int(shard_count))
+                        int(shard_rank), int(shard_count), _POLICIES[shard_policy],
+                        nccl_comm.handle if nccl_comm is not None else None)
         handle = C.c_void_p()
         with torch.cuda.device(self.device):
             torch.cuda.init()
@@ -155,9 +200,22 @@ class Plan:
         return x.contiguous()
 
     # -------------------------------------------------------------- transforms
-    def forward(self, x, out=None, stream=None):
+    def forward(self, x, out=None, stream=None, batch: int | None = None):
         """Coefficient cube (B, eta_local, n, n) complex of images x (B, n, n)
-        (shearletTransformSpect, eq:shearletTransform)."""
+        (shearletTransformSpect, eq:shearletTransform).  With a communicator, x is read on rank 0
+        only (None elsewhere, with ``batch`` given) and broadcast by the library."""
+        if x is None:
+            if self.comm is None or self.shard_rank == 0:
+                raise ValueError("images required")
+            b = self.batch if batch is None else int(batch)
+            if b < 1 or b > self.batch:
+                raise ValueError(f"batch {b} outside 1..{self.batch}")
+            out = self.empty_coeffs(b) if out is None else out
+            _check_buf(out, (b, self.eta_local, self.n, self.n), self.cdtype, self.device, "output cube")
+            self.reserve(b)
+            check(lib.ffst_sheartrans_batch(self._h, None, C.c_void_p(out.data_ptr()), b,
+                                            _stream_handle(stream, self.device)), "ffst_sheartrans_batch")
+            return out
         x = self._check_images(x)
         b = x.shape[0]
         out = self.empty_coeffs(b) if out is None else out
@@ -167,9 +225,11 @@ class Plan:
                                         _stream_handle(stream, self.device)), "ffst_sheartrans_batch")
         return out
 
-    def inverse(self, c, out=None, stream=None):
-        """Re ifft2(sum_i psi_i fft2(c_i)) over the local planes (inverseShearletTransformSpect,
-        eq:inverseShearletTransform).  c: (B, eta_local, n, n) complex."""
+    def inverse(self, c, out=None, stream=None, root: int = 0):
+        """Re ifft2(sum_i psi_i fft2(c_i)) (inverseShearletTransformSpect, eq:inverseShearletTransform).
+        c: (B, eta_local, n, n) complex.  Sharded with a communicator: the full image, written on
+        ``root`` only (the return value elsewhere is an untouched buffer); without one: the
+        partial image of the local planes."""
         if c.dim() == 3:
             c = c.unsqueeze(0)
         if c.dtype != self.cdtype or c.device != self.device or c.shape[1:] != (self.eta_local, self.n, self.n):
@@ -182,7 +242,8 @@ class Plan:
         _check_buf(out, (b, self.n, self.n), self.dtype, self.device, "output images")
         self.reserve(b)
         check(lib.ffst_inversesheartrans_batch(self._h, C.c_void_p(c.data_ptr()), C.c_void_p(out.data_ptr()), b,
-                                               _stream_handle(stream, self.device)), "ffst_inversesheartrans_batch")
+                                               int(root), _stream_handle(stream, self.device)),
+              "ffst_inversesheartrans_batch")
         return out
 
     def forward_host(self, x_host, out=None, stream=None):
@@ -264,16 +325,21 @@ class Plan:
               "ffst_inversesheartrans_compact")
         return out
 
-    def expand_compact(self, re, gh):
+    def expand_compact(self, re, gh, out=None, stream=None):
         """The complex cube of a compact one: Im c_i(r, m1) = (-1)^r G_i(m1) + (-1)^m1 H_i(r) on the
-        Nyquist planes, 0 elsewhere (a format conversion with torch ops; not on the transform path)."""
-        c = torch.complex(re, torch.zeros_like(re))
-        sgn = 1.0 - 2.0 * (torch.arange(self.n, device=re.device) % 2).to(re.dtype)
-        for q, pl in enumerate(self.nyquist_planes()):
-            g, h = gh[:, q, 0], gh[:, q, 1]
-            im = sgn[None, :, None] * g[:, None, :] + sgn[None, None, :] * h[:, :, None]
-            c[:, pl] = torch.complex(re[:, pl], im)
-        return c
+        Nyquist planes, 0 elsewhere (ffst_expand_compact, one kernel)."""
+        b = re.shape[0] if re.dim() == 4 else 0
+        if b < 1 or b > self.batch:
+            raise ValueError(f"batch {b} outside 1..{self.batch}")
+        nn = max(1, len(self.nyquist_planes()))
+        _check_buf(re, (b, self.eta_local, self.n, self.n), self.dtype, self.device, "compact real parts")
+        _check_buf(gh, (b, nn, 2, self.n), self.dtype, self.device, "compact Nyquist vectors")
+        out = self.empty_coeffs(b) if out is None else out
+        _check_buf(out, (b, self.eta_local, self.n, self.n), self.cdtype, self.device, "output cube")
+        check(lib.ffst_expand_compact(self._h, C.c_void_p(re.data_ptr()), C.c_void_p(gh.data_ptr()),
+                                      C.c_void_p(out.data_ptr()), b, _stream_handle(stream, self.device)),
+              "ffst_expand_compact")
+        return out
 
     def spectra(self, centred: bool = True, stream=None):
         """The local spectra psi_hat_i as (eta_local, n, n) real (tests / diagnostics)."""

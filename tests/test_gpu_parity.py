@@ -12,6 +12,8 @@ import torch
 import oracle as O
 import synth
 
+import oracle_pool as OP  # noqa: E402  (tests/oracle_pool.py)
+
 pytestmark = pytest.mark.gpu
 
 TOL = {torch.float32: 1e-4, torch.float64: 1e-10}
@@ -152,20 +154,78 @@ def test_determinism_config2(F):
     assert torch.equal(r1[5:8], r_sub)
 
 
-def test_shards_sum_to_full(F):
-    # eta-sharding: each shard's cube holds its planes; partial images sum to the full inverse
+@pytest.mark.parametrize("policy", ["lpt", "round_robin"])
+def test_shards_sum_to_full(F, policy):
+    # eta-sharding: each shard's cube holds its planes (ffst_shard_planes); the partial images
+    # (no communicator: the caller reduces) sum to the full inverse
     n, batch, shards = 64, 2, 3
     x, xo = images(2, batch, n, torch.float64)
     full = F.Plan(n, batch, torch.float64)
     c_full = full.forward(x.cuda()).cpu()
     rec_sum = torch.zeros(batch, n, n, dtype=torch.float64)
+    owned = []
     for r in range(shards):
-        p = F.Plan(n, batch, torch.float64, shard_rank=r, shard_count=shards)
-        assert p.local_planes == list(range(r, full.eta, shards))
+        p = F.Plan(n, batch, torch.float64, shard_rank=r, shard_count=shards, shard_policy=policy)
+        assert p.local_planes == F.shard_planes(n, shards, r, policy)
+        owned += p.local_planes
         c = p.forward(x.cuda())
-        assert torch.allclose(c.cpu(), c_full[:, r::shards], atol=1e-13, rtol=0)
+        assert torch.allclose(c.cpu(), c_full[:, p.local_planes], atol=1e-13, rtol=0)
         rec_sum += p.inverse(c).cpu()
+    assert sorted(owned) == list(range(full.eta))
     assert np.max(np.abs(rec_sum.numpy() - xo)) < 1e-12
+
+
+@pytest.mark.parametrize("n,batch,dtype", [(64, 1, torch.float64), (256, 16, torch.float32), (128, 5, torch.float32)])
+def test_nccl_single_rank(F, n, batch, dtype):
+    # the library's own collectives (include/ffst.h "Multi-GPU") on a one-rank NCCL communicator
+    # (the one GPU of this box): image broadcast in image groups before the spectrum kernels,
+    # reduce of the adjoint spectra and Nyquist corrections, final synthesis on the root --
+    # bitwise the results of the plan without a communicator
+    comm = F.NcclComm(1, 0, torch.cuda.current_device(), F.NcclComm.unique_id())
+    try:
+        x, xo = images(2, batch, n, dtype)
+        xd = x.cuda()
+        plain = F.Plan(n, batch, dtype)
+        coll = F.Plan(n, batch, dtype, nccl_comm=comm)
+        c0 = plain.forward(xd)
+        c1 = coll.forward(xd)
+        assert torch.equal(c0, c1)
+        r0 = plain.inverse(c0)
+        r1 = coll.inverse(c1, root=0)
+        assert torch.equal(r0, r1)
+        assert plane_err(r1.cpu().numpy(), xo).max() <= TOL[dtype]
+        with pytest.raises(F.FFSTError):
+            coll.inverse(c1, root=1)                       # root outside the communicator
+        if batch > 1:                                      # a smaller batch (other image groups)
+            assert torch.equal(coll.forward(xd[1:]), c0[1:])
+            assert torch.equal(coll.inverse(c0[1:].contiguous()), plain.inverse(c0[1:].contiguous()))
+        coll.close()
+        plain.close()
+    finally:
+        comm.close()
+
+
+def test_reserved_batches_do_not_allocate(F):
+    # transforms never allocate device memory (include/ffst.h): a batch size is reserved first
+    # (Plan.reserve -> ffst_plan_reserve), after which its first call leaves device memory as is;
+    # an unreserved batch fails in the C ABI before anything is launched
+    import ctypes as C
+    n, batch = 128, 6
+    plan = F.Plan(n, batch, torch.float32)
+    x = torch.randn(3, n, n, device="cuda")
+    out_c = plan.empty_coeffs(3)
+    out_r = plan.empty_images(3)
+    with pytest.raises(F.FFSTError):
+        F.plan.check(F.lib.ffst_sheartrans_batch(plan._h, C.c_void_p(x.data_ptr()), C.c_void_p(out_c.data_ptr()),
+                                                 3, None), "unreserved")
+    plan.reserve(3)
+    torch.cuda.synchronize()
+    free0 = torch.cuda.mem_get_info()[0]
+    plan.forward(x, out=out_c)
+    plan.inverse(out_c, out=out_r)
+    torch.cuda.synchronize()
+    assert torch.cuda.mem_get_info()[0] == free0
+    assert float((out_r - x).abs().max() / x.abs().max()) <= 1e-4
 
 
 def test_host_variants(F):
@@ -227,42 +287,80 @@ def test_config2_full(F, env, monkeypatch):
     assert worst <= 1e-4, worst
 
 
-@pytest.mark.parametrize("cid,images_checked,plane_stride", [(3, (0, 63), 1), (4, (0, 31), 5)])
-def test_config_sampled(F, cid, images_checked, plane_stride):
-    # configs[2], configs[3] at their full batch (the bench launch configuration):
-    # sampled images x planes against the oracle, round trip and Parseval on every image.
+def _kind_scale_planes(n, j0=None):
+    """One plane of every (kind, j) pair, the low-pass, and the Nyquist planes of the finest
+    scale (0-based flat indices): every window code path and every Nyquist-plane kind."""
+    j0 = O.scales_for_size(n) if j0 is None else j0
+    eta = O.num_shearlets(j0)
+    first = {}
+    for i in range(eta):
+        kind, j, _ = O.index_to_params(j0, i + 1)
+        first.setdefault((kind, j), i)
+    return sorted(first.values()), eta
+
+
+@pytest.mark.parametrize("cid,images_checked", [(3, (0, 63)), (4, (0, 31))])
+def test_config_full_batch(F, cid, images_checked):
+    # configs[2], configs[3] at their full batch (the bench launch configuration): every plane of
+    # the first and last image against the oracle (forward), the full-batch inverse of the GPU
+    # cube element-wise against the oracle's inverse of the same cube on those images; round trip
+    # and Parseval on every image
     cfg = synth.config(cid)
     x, _ = images(cid, cfg.batch, cfg.n, torch.float32)
     plan = F.Plan(cfg.n, cfg.batch, torch.float32)
     xd = x.cuda()
     c = plan.forward(xd)
     rec = plan.inverse(c)
-    # properties at full size on every image
     err_rt = (rec - xd).abs().amax(dim=(1, 2)) / xd.abs().amax(dim=(1, 2))
     assert float(err_rt.max()) <= 1e-4
     energy_c = (c.abs() ** 2).double().sum(dim=(1, 2, 3))
     energy_f = (xd.double() ** 2).sum(dim=(1, 2))
     assert float(((energy_c - energy_f).abs() / energy_f).max()) <= 1e-4
-    j0 = O.scales_for_size(cfg.n)
-    eta = O.num_shearlets(j0)
-    planes = sorted(set(range(0, eta, plane_stride)) | {eta - 1, eta - 2})
+    eta = plan.eta
+    rec = rec.cpu().numpy()
     for b in images_checked:
         cb = c[b].cpu().numpy()
         x64 = x[b].double().numpy()
-        assert _check_forward_planes(cb, x64, planes, 1e-4, cfg.n) <= 1e-4
-        # inverse parity on a cube restricted to a few planes (others zeroed)
-        keep = planes[:3] + planes[-2:]
-        z = torch.zeros_like(c[b:b + 1])
-        z[0, keep] = c[b, keep]
-        sub = F.Plan(cfg.n, 1, torch.float32)
-        r = sub.inverse(z).cpu().numpy()[0]
-        ref = O.inverse(cb[keep].astype(np.complex128), planes=[i + 1 for i in keep]).real
-        assert plane_err(r, ref).max() <= 1e-4
-    del c, rec
+        ref = OP.forward_planes(x64, list(range(eta)))
+        worst = max(plane_err(cb[i], ref[i], np.max(np.abs(x64))) for i in range(eta))
+        assert worst <= 1e-4, (b, worst)
+        ref_inv = OP.inverse(cb.astype(np.complex128), list(range(eta))).real
+        assert plane_err(rec[b], ref_inv) <= 1e-4, b
+    del c
 
 
-def test_config5_sampled(F):
-    # configs[4]: 4096x4096 float32 single image, sampled planes, round trip, Parseval
+@pytest.mark.parametrize("cid", [2, 3, 4, 5])
+def test_adjoint_off_range_bench_geometry(F, cid):
+    # the inverse of an ARBITRARY complex cube (outside the forward's range: general imaginary
+    # parts, so the Nyquist correction's Im terms matter) at each config's full batch and launch
+    # geometry (queues, ring, accumulator lanes, pass-1 item sizes): non-zero on one plane of every
+    # (kind, j) pair plus finest-scale Nyquist planes of both cones, in the first and last image;
+    # compared element-wise with the oracle's inverse (eq:inverseShearletTransform, P:L1730-1764)
+    cfg = synth.config(cid)
+    n, B = cfg.n, cfg.batch
+    plan = F.Plan(n, B, torch.float32)
+    base, eta = _kind_scale_planes(n)
+    nyq = [i for i in range(eta) if F.plane_is_nyquist(n, i)]
+    sample = sorted(set(base) | {nyq[0], nyq[len(nyq) // 2], nyq[-1]})
+    checked = sorted({0, B - 1})
+    z = torch.zeros(B, eta, n, n, dtype=torch.complex64, device="cuda")
+    zo = {}
+    for b in checked:
+        zb = synth.random_cube((len(sample), n, n), 1000 * cid + b).astype(np.complex64)
+        z[b, sample] = torch.from_numpy(zb).cuda()
+        zo[b] = zb.astype(np.complex128)
+    rec = plan.inverse(z).cpu().numpy()
+    for b in checked:
+        ref = OP.inverse(zo[b], sample).real
+        assert plane_err(rec[b], ref) <= 1e-4, b
+    others = [b for b in range(B) if b not in checked]
+    if others:
+        assert np.max(np.abs(rec[others])) == 0.0
+
+
+def test_config5_forward_planes(F):
+    # configs[4]: 4096x4096 float32 single image; the forward against the oracle on one plane of
+    # every (kind, j) pair and on every finest-scale Nyquist plane; round trip and Parseval
     cfg = synth.config(5)
     x, _ = images(5, 1, cfg.n, torch.float32)
     plan = F.Plan(cfg.n, 1, torch.float32)
@@ -273,21 +371,24 @@ def test_config5_sampled(F):
     ec = float((c.abs() ** 2).double().sum())
     ef = float((xd.double() ** 2).sum())
     assert abs(ec - ef) / ef <= 1e-4
-    eta = plan.eta
-    nyq = [i for i in range(eta) if F.plane_is_nyquist(cfg.n, i)]
-    planes = sorted({0, 1, eta // 2, eta - 1, nyq[0], nyq[len(nyq) // 2]})
+    base, eta = _kind_scale_planes(cfg.n)
+    j0 = plan.j0
+    finest_nyq = [i for i in range(eta) if O.index_to_params(j0, i + 1)[1] == j0 - 1 and F.plane_is_nyquist(cfg.n, i)]
+    assert len(finest_nyq) >= 2 ** (j0 + 1) - 4
+    planes = sorted(set(base) | set(finest_nyq))
     x64 = x[0].double().numpy()
-    f_hat = O.dft2_centred(x64)
+    ref = OP.forward_planes(x64, planes)
+    worst = 0.0
     for i in planes:
-        g = c[0, i].cpu().numpy()
-        ref = O.forward_plane(x64, i + 1, f_hat=f_hat)
-        assert plane_err(g, ref, np.max(np.abs(x64))) <= 1e-4, i
+        worst = max(worst, plane_err(c[0, i].cpu().numpy(), ref[i], np.max(np.abs(x64))))
+    assert worst <= 1e-4, worst
 
 
 # ------------------------------------------------------------------ compact format
 
 @pytest.mark.parametrize("n,dtype,batch", [(8, torch.float64, 2), (64, torch.float64, 3), (32, torch.float32, 3),
-                                           (256, torch.float32, 16), (512, torch.float32, 4)])
+                                           (256, torch.float32, 16), (512, torch.float32, 4), (1024, torch.float32, 2),
+                                           (4096, torch.float32, 1)])
 def test_compact_format(F, n, dtype, batch):
     # the compact cube (real parts + Nyquist vectors) expands to the complex forward's cube, its
     # inverse equals the complex inverse of that cube, and the round trip is exact
@@ -304,10 +405,17 @@ def test_compact_format(F, n, dtype, batch):
     r_complex = plan.inverse(ce)
     assert float((r_compact - r_complex).abs().max() / r_complex.abs().max()) <= tol
     assert plane_err(r_compact.cpu().numpy(), xo).max() <= TOL[dtype]
-    # against the oracle on one image
-    psi = O.shearlet_spectra(n)
-    ref = O.forward(xo[0], psi=psi)
-    assert plane_err(ce[0].cpu().numpy(), ref, np.max(np.abs(xo[0]))).max() <= TOL[dtype]
+    # the expanded cube against the oracle on one image (every plane; sampled planes above 512)
+    if n <= 512:
+        ref = O.forward(xo[0], psi=O.shearlet_spectra(n))
+        assert plane_err(ce[0].cpu().numpy(), ref, np.max(np.abs(xo[0]))).max() <= TOL[dtype]
+    else:
+        base, eta = _kind_scale_planes(n)
+        nyq = plan.nyquist_planes()
+        planes = sorted(set(base) | {nyq[0], nyq[len(nyq) // 2], nyq[-1]})
+        ref = OP.forward_planes(xo[0], planes)
+        for i in planes:
+            assert plane_err(ce[0, i].cpu().numpy(), ref[i], np.max(np.abs(xo[0]))) <= TOL[dtype], i
 
 
 # ------------------------------------------------------------------ smooth variant
@@ -416,7 +524,8 @@ def _user_plan(F, psi, batch, dtype, centred=True, **kw):
     return F.Plan(psi.shape[-1], batch, dtype, spectra=t, centred=centred, **kw), t
 
 
-@pytest.mark.parametrize("n,dtype", [(16, torch.float64), (64, torch.float64), (256, torch.float32)])
+@pytest.mark.parametrize("n,dtype", [(16, torch.float64), (64, torch.float64), (256, torch.float32),
+                                     (1024, torch.float32)])
 def test_user_spectra_builtin_system(F, n, dtype):
     # the built-in spectra passed in as precomputed Psi reproduce the built-in plan
     psi = O.shearlet_spectra(n)
@@ -443,7 +552,8 @@ def test_user_spectra_builtin_system(F, n, dtype):
 
 @pytest.mark.parametrize("n,eta,dtype,batch,centred", [(4, 3, torch.float64, 2, True), (16, 7, torch.float64, 3, True),
                                                        (64, 13, torch.float64, 2, False), (256, 29, torch.float32, 4, True),
-                                                       (512, 9, torch.float32, 2, False)])
+                                                       (512, 9, torch.float32, 2, False), (1024, 17, torch.float32, 2, True),
+                                                       (4096, 5, torch.float32, 1, False)])
 def test_user_spectra_random_system(F, n, eta, dtype, batch, centred):
     # a random Parseval system with pruned column bands and asymmetric Nyquist lines
     psi = synth.random_spectra(n, eta, 100 + n)

@@ -529,3 +529,17 @@ def test_user_spectra_parseval_and_brute_force(n, eta):
             val = sum(psi[i, p, q] * fh[p, q] * np.exp(2j * np.pi * (u[q] * x[m] + u[p] * x[r]) / n)
                       for p in range(n) for q in range(n)) / n**2
             assert abs(val - c[i, r, m]) < 1e-12, (i, r, m)
+
+
+def test_oracle_pool_matches_oracle():
+    # the tests' parallel driver of the oracle (tests/oracle_pool.py) returns exactly what the
+    # oracle's own functions return (same terms, summed in the same plane order)
+    import oracle_pool as OP
+    n = 32
+    f = synth.make_batch(1, n=n)[0]
+    planes = [0, 3, 7, 12]
+    got = OP.forward_planes(f, planes)
+    for i in planes:
+        assert np.array_equal(got[i], O.forward_plane(f, i + 1))
+    z = synth.random_cube((len(planes), n, n), 5)
+    assert np.array_equal(OP.inverse(z, planes), O.inverse(z, planes=[i + 1 for i in planes]))
