@@ -64,7 +64,7 @@ typedef enum {
   FFST_ERR_OOM = 6,            /* workspace allocation failed at plan creation */
   FFST_ERR_CUDA = 7,           /* CUDA runtime error (see ffst_last_error_detail) */
   FFST_ERR_NCCL = 8,           /* NCCL failure (see ffst_last_error_detail) */
-  FFST_ERR_UNSUPPORTED = 9     /* n not a power of two, or more local planes than built */
+  FFST_ERR_UNSUPPORTED = 9     /* size or option outside the build (see each call), or more local planes than built */
 } ffst_status;
 
 typedef enum { FFST_F32 = 0, FFST_F64 = 1 } ffst_dtype;
@@ -88,7 +88,9 @@ typedef struct ffst_plan ffst_plan;   /* opaque */
 typedef enum { FFST_SHARD_LPT = 0, FFST_SHARD_ROUND_ROBIN = 1 } ffst_shard_policy;
 
 typedef struct {
-  int n;              /* image side, power of two, 4 <= n <= 4096 */
+  int n;              /* image side: a power of two 4..4096 (float64: ..2048), or any other n in 5..2048
+                         (the arbitrary-n path, full complex transforms with Bluestein
+                         line DFTs; no compact format) */
   int j0;             /* number of scales; 0 = default floor(log2(n)/2) */
   int batch;          /* maximum images per call, >= 1 */
   ffst_dtype dtype;   /* FFST_F32 or FFST_F64 */
@@ -147,7 +149,7 @@ ffst_status ffst_nccl_comm_destroy(void* comm);
 
 /* Create a plan: all tables (index order, pruning ranges, radial factors, Nyquist anti-window
  * edges, work queues) and all device workspace are built here; transforms allocate nothing.
- * Errors: INVALID_SIZE (n < 4 or above the built sizes), UNSUPPORTED (n not a power of two,
+ * Errors: INVALID_SIZE (n < 4 or above the built sizes), UNSUPPORTED (n not a power of two above 2048,
  * more than 256 local planes), INVALID_ARG (incl. an unknown variant), OOM, CUDA.
  * Environment (read here, tuning only; results are identical up to rounding order):
  *   FFST_RING_MB        intermediate ring budget (default 80; at least 12 slots)
@@ -168,12 +170,13 @@ ffst_status ffst_plan_destroy(ffst_plan* plan);
  * keeps its own Hermitian-half copy of the symmetric parts, eta_local x (n/2+1) x n reals, and
  * prunes each plane to its non-zero column range).  desc->variant and desc->j0 are ignored;
  * eta may be any count >= 1 (the plan's eta).  Sharding as for ffst_plan_create (all eta
- * planes are passed on every rank).  The spectra must be point-symmetric off the Nyquist lines,
- * psi(u) = psi(-u) for u1, u2 != -n/2 (the spectra of real shearlets; every built-in system is),
- * to within 1e-5 (float32) / 1e-12 (float64) absolute -- else INVALID_ARG; the Nyquist row and
- * column may be asymmetric (handled exactly).  The Parseval admission check of
- * P:L2219-2220 is computed but not enforced: ffst_plan_spectra_check.
- * Errors: as ffst_plan_create, plus INVALID_ARG (null psi, eta < 1, asymmetric spectra). */
+ * planes are passed on every rank).  Any real spectra are accepted: point-symmetric ones off the
+ * Nyquist lines (psi(u) = psi(-u) for u1, u2 != -n/2 to within 1e-5 (float32) / 1e-12 (float64),
+ * the spectra of real shearlets; every built-in system is) run on the Hermitian fast path (the
+ * Nyquist row and column may be asymmetric, handled exactly); any other set runs on
+ * the full complex path of arbitrary n (n <= 2048; above: INVALID_ARG).  The Parseval admission
+ * check of P:L2219-2220 is computed but not enforced: ffst_plan_spectra_check.
+ * Errors: as ffst_plan_create, plus INVALID_ARG (null psi, eta < 1, asymmetric spectra at n = 4096). */
 ffst_status ffst_plan_create_user(ffst_plan** out, const ffst_plan_desc* desc, int eta, const void* psi,
                                   int centred_layout);
 

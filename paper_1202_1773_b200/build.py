@@ -12,7 +12,7 @@ ROOT = PKG.parent
 CSRC = PKG / "csrc"
 BUILD = PKG / "_build"
 LIB = PKG / "libffst.so"
-SOURCES = ["ffst_api.cu", "ffst_kern_f32.cu", "ffst_kern_f64.cu"]
+SOURCES = ["ffst_api.cu", "ffst_kern_f32.cu", "ffst_kern_f64.cu", "ffst_gen_f32.cu", "ffst_gen_f64.cu"]
 NVCC = os.environ.get("NVCC", "/usr/local/cuda/bin/nvcc")
 
 

@@ -13,6 +13,7 @@
 
 #include <algorithm>
 #include <cmath>
+#include <complex>
 #include <cstdio>
 #include <cstdlib>
 #include <cstring>
@@ -21,6 +22,7 @@
 #include <vector>
 
 #include "../../include/ffst.h"
+#include "ffst_generic.cuh"
 #include "ffst_internal.h"
 
 using namespace ffst;
@@ -79,7 +81,8 @@ std::vector<Triple> index_table(int j0) {
   return t;
 }
 
-double grid_delta(int n, int j0) { return std::ldexp(1.0, 2 * j0) / (double)n; }   // P:L2180, N_odd - 1 = n
+// Delta = 2^(2 j0) / (N_odd - 1) with N_odd = n (odd n) or n + 1 (even n)
+double grid_delta(int n, int j0) { return std::ldexp(1.0, 2 * j0) / (double)(n % 2 ? n - 1 : n); }
 
 // Superset of the columns c = |u1| (0..n/2) where the plane can be non-zero.
 void plane_columns(int n, int j0, const Triple& tr, int* lo, int* hi) {
@@ -296,6 +299,12 @@ struct ffst_plan {
   cudaEvent_t fork[2] = {};
   int launches[2] = {0, 0};
   std::vector<void*> allocs;
+  // arbitrary-n path (ffst_generic.cuh): full complex 2-D transforms, Bluestein line DFTs
+  bool generic = false;
+  int gen_M = 0, gen_np = 0;      // Bluestein FFT length, planes per chunk
+  void *g_chirp = nullptr, *g_bhat = nullptr, *g_twm = nullptr, *g_usr = nullptr;
+  void *Ft = nullptr, *S = nullptr, *At = nullptr, *Wt = nullptr, *W2 = nullptr;
+  int* g_gidx = nullptr;
   // user spectra (f4, ffst_plan_create_user)
   void* d_usym = nullptr;         // [eta_l][n/2+1][n] T symmetric parts
   double tightness = -1, asymmetry = -1;   // admission check; -1: not computed yet
@@ -616,6 +625,8 @@ KParams base_params(ffst_plan* p) {
   k.rpi = p->rpi;
   k.a_lane_elems = (long long)p->d.batch * (p->n / 2 + 1) * p->n;
   if (const char* d = std::getenv("FFST_DBG")) k.dbg = std::atoi(d);
+  k.sync_mode = 3;
+  if (const char* sm = std::getenv("FFST_SYNC")) k.sync_mode = std::atoi(sm) & 3;   // measurement only
   return k;
 }
 
@@ -682,12 +693,19 @@ void group_range(int batch, int G, int g, int* g0, int* g1) {
 }
 ncclDataType_t nccl_type(const ffst_plan* p) { return p->d.dtype == FFST_F32 ? ncclFloat32 : ncclFloat64; }
 
+ffst_status forward_generic(ffst_plan* p, const void* img, void* coeff, int batch, cudaStream_t s);
+ffst_status inverse_generic(ffst_plan* p, const void* coeff, void* img_out, int batch, int root_rank, cudaStream_t s);
+
 // nyq_gh != nullptr: compact (f1) format -- coeff holds the real parts, nyq_gh the Nyquist vectors.
 // With a communicator: img is read on rank 0 and broadcast (image groups on the comm stream, each
 // group's spectrum kernels start as soon as its images have arrived); other ranks receive into the
 // plan's staging buffer (img may be NULL there).
 ffst_status forward_impl(ffst_plan* p, const void* img, void* coeff, int batch, cudaStream_t s,
                          void* nyq_gh = nullptr) {
+  if (p->generic) {
+    if (nyq_gh) return fail(FFST_ERR_UNSUPPORTED, "compact format: power-of-two n (fast path) only");
+    return forward_generic(p, img, coeff, batch, s);
+  }
   const bool coll = p->comm != nullptr;
   const bool root = p->d.shard_rank == 0;
   const void* src = coll && !root ? p->stage : img;
@@ -764,6 +782,10 @@ ffst_status forward_impl(ffst_plan* p, const void* img, void* coeff, int batch, 
 // being reduced.  img_out is written on the root only (it may be NULL elsewhere).
 ffst_status inverse_impl(ffst_plan* p, const void* coeff, void* img_out, int batch, int root_rank, cudaStream_t s,
                          const void* nyq_gh = nullptr) {
+  if (p->generic) {
+    if (nyq_gh) return fail(FFST_ERR_UNSUPPORTED, "compact format: power-of-two n (fast path) only");
+    return inverse_generic(p, coeff, img_out, batch, root_rank, s);
+  }
   const bool coll = p->comm != nullptr;
   if (coll && (root_rank < 0 || root_rank >= p->d.shard_count)) return fail(FFST_ERR_INVALID_ARG, "root outside 0..shard_count-1");
   const bool root = !coll || p->d.shard_rank == root_rank;
@@ -856,14 +878,230 @@ ffst_status inverse_impl(ffst_plan* p, const void* coeff, void* img_out, int bat
   return FFST_OK;
 }
 
-// User spectra (f4): run the prepare kernels (ffst_user.cuh) on the caller's eta planes, keep the
-// admission numbers, and replace each local plane's provisional geometry by its column hull and
-// Nyquist flag.  `anti` receives the anti parts of every local plane ([eta_l][2][n], float64).
 struct UserSpectra {
   int eta;
   const void* psi;
   int centred;
 };
+
+// ============================================================ arbitrary-n path (ffst_generic.cuh)
+
+// Host FFT (float64, radix 2, forward sign): the Bluestein kernel's spectrum FFT_M(b) (a plan table).
+void host_fft(std::vector<std::complex<double>>& a) {
+  const size_t M = a.size();
+  for (size_t i = 1, j = 0; i < M; ++i) {
+    size_t bit = M >> 1;
+    for (; j & bit; bit >>= 1) j ^= bit;
+    j ^= bit;
+    if (i < j) std::swap(a[i], a[j]);
+  }
+  const long double pi = 3.14159265358979323846264338327950288L;
+  for (size_t len = 2; len <= M; len <<= 1)
+    for (size_t i = 0; i < M; i += len)
+      for (size_t k = 0; k < len / 2; ++k) {
+        const long double ang = -2.0L * pi * (long double)k / (long double)len;
+        const std::complex<double> w((double)cosl(ang), (double)sinl(ang));
+        const std::complex<double> u = a[i + k], v = a[i + k + len / 2] * w;
+        a[i + k] = u + v;
+        a[i + k + len / 2] = u - v;
+      }
+}
+
+GenParams gen_params(const ffst_plan* p, int batch) {
+  GenParams g{};
+  g.n = p->n; g.M = p->gen_M; g.eta_l = p->eta_l; g.batch = batch;
+  g.planes = p->d_planes; g.rtab = p->d_rtab; g.j0 = p->j0;
+  g.variant = p->d.variant == FFST_SMOOTH ? 1 : 0;
+  g.usr = p->g_usr;
+  g.chirp = p->g_chirp; g.bhat = p->g_bhat; g.twm = p->g_twm;
+  return g;
+}
+
+cudaError_t G_rows(const ffst_plan* p, int op, const GenParams& g, const void* src, void* dst, int np, int p0, int first,
+                   double scale, int cube_side, int mats, cudaStream_t s) {
+  return p->d.dtype == FFST_F32
+             ? launch_gen_rows<float>(op, g, src, dst, np, p0, first, scale, cube_side, cube_side ? p->eta_l : 0, mats, s)
+             : launch_gen_rows<double>(op, g, src, dst, np, p0, first, scale, cube_side, cube_side ? p->eta_l : 0, mats, s);
+}
+cudaError_t G_transpose(const ffst_plan* p, const void* src, void* dst, int mats, cudaStream_t s) {
+  return p->d.dtype == FFST_F32 ? launch_gen_transpose<float>(src, dst, p->n, mats, s)
+                                : launch_gen_transpose<double>(src, dst, p->n, mats, s);
+}
+
+// Generic-path tables (chirp, FFT_M(b), twiddles) and workspace; user spectra copied to a
+// natural-order table of the local planes.
+ffst_status generic_setup(ffst_plan* p, const UserSpectra* us) {
+  const int n = p->n;
+  int M = 16;
+  while (M < 2 * n - 1) M *= 2;
+  if (M > 4096) return fail(FFST_ERR_UNSUPPORTED, "this n needs the arbitrary-n path, built up to n = 2048");
+  p->gen_M = M;
+  const size_t B = (size_t)p->d.batch, nn = (size_t)n * n, csz = 2 * p->rsz;
+  const size_t budget = (size_t)512 << 20;
+  p->gen_np = (int)std::max<size_t>(1, std::min<size_t>(p->eta_l, budget / (2 * B * nn * csz)));
+  void* ptr = nullptr;
+#define GALLOC(dst, bytes) do { TRY(dalloc(p, &ptr, (bytes))); dst = static_cast<decltype(dst)>(ptr); } while (0)
+  GALLOC(p->d_planes, p->planes.size() * sizeof(PlaneDev));
+  GALLOC(p->d_rtab, (size_t)(p->d.variant == FFST_SMOOTH ? 3 * p->j0 + 4 : p->j0 + 1) * (n / 2 + 1) * p->rsz);
+  GALLOC(p->g_chirp, (size_t)n * csz);
+  GALLOC(p->g_bhat, (size_t)M * csz);
+  GALLOC(p->g_twm, (size_t)M * csz);
+  GALLOC(p->Ft, B * nn * csz);
+  GALLOC(p->S, B * nn * csz);
+  GALLOC(p->At, B * nn * csz);
+  GALLOC(p->Wt, B * p->gen_np * nn * csz);
+  GALLOC(p->W2, B * p->gen_np * nn * csz);
+  GALLOC(p->stage, B * nn * p->rsz);
+  GALLOC(p->g_gidx, p->planes.size() * sizeof(int));
+  if (us) GALLOC(p->g_usr, (size_t)p->eta_l * nn * p->rsz);
+#undef GALLOC
+  // chirp c_m = exp(-i pi m^2 / n) (angle reduced through m^2 mod 2n), b_t = conj(c_|t|), FFT_M(b)
+  const long double pi = 3.14159265358979323846264338327950288L;
+  std::vector<std::complex<double>> ch(n), b(M, 0.0);
+  for (int m = 0; m < n; ++m) {
+    const long long q = ((long long)m * m) % (2LL * n);
+    const long double ang = -pi * (long double)q / (long double)n;
+    ch[m] = std::complex<double>((double)cosl(ang), (double)sinl(ang));
+  }
+  for (int t = 0; t < n; ++t) {
+    b[t] = std::conj(ch[t]);
+    if (t > 0) b[M - t] = std::conj(ch[t]);
+  }
+  host_fft(b);
+  std::vector<unsigned char> tw;
+  if (p->d.dtype == FFST_F32) fill_twiddles<float>(tw, M); else fill_twiddles<double>(tw, M);
+  auto upload_c = [&](void* dst, const std::vector<std::complex<double>>& v) {
+    if (p->d.dtype == FFST_F32) {
+      std::vector<float> f(2 * v.size());
+      for (size_t i = 0; i < v.size(); ++i) { f[2 * i] = (float)v[i].real(); f[2 * i + 1] = (float)v[i].imag(); }
+      return cudaMemcpy(dst, f.data(), f.size() * sizeof(float), cudaMemcpyHostToDevice);
+    }
+    return cudaMemcpy(dst, v.data(), v.size() * sizeof(std::complex<double>), cudaMemcpyHostToDevice);
+  };
+  cudaError_t e = upload_c(p->g_chirp, ch);
+  if (e == cudaSuccess) e = upload_c(p->g_bhat, b);
+  if (e == cudaSuccess) e = cudaMemcpy(p->g_twm, tw.data(), tw.size(), cudaMemcpyHostToDevice);
+  if (e == cudaSuccess) {
+    const std::vector<double> rt = radial_all(n, p->j0, p->d.variant);
+    if (p->d.dtype == FFST_F32) {
+      std::vector<float> rf(rt.begin(), rt.end());
+      e = cudaMemcpy(p->d_rtab, rf.data(), rf.size() * sizeof(float), cudaMemcpyHostToDevice);
+    } else {
+      e = cudaMemcpy(p->d_rtab, rt.data(), rt.size() * sizeof(double), cudaMemcpyHostToDevice);
+    }
+  }
+  std::vector<int> gidx;
+  for (auto& P : p->planes) gidx.push_back(P.gi);
+  if (e == cudaSuccess) e = cudaMemcpy(p->d_planes, p->planes.data(), p->planes.size() * sizeof(PlaneDev), cudaMemcpyHostToDevice);
+  if (e == cudaSuccess) e = cudaMemcpy(p->g_gidx, gidx.data(), gidx.size() * sizeof(int), cudaMemcpyHostToDevice);
+  if (e != cudaSuccess) return cuda_fail(e, "arbitrary-n plan upload");
+  if (us) {
+    void* st = nullptr;
+    e = cudaMalloc(&st, 2 * sizeof(unsigned long long));
+    if (e == cudaSuccess) e = cudaMemset(st, 0, 2 * sizeof(unsigned long long));
+    if (e == cudaSuccess)
+      e = p->d.dtype == FFST_F32
+              ? launch_gen_user<float>(us->psi, p->g_usr, n, p->g_gidx, p->eta_l, us->eta, us->centred,
+                                       static_cast<unsigned long long*>(st), 0)
+              : launch_gen_user<double>(us->psi, p->g_usr, n, p->g_gidx, p->eta_l, us->eta, us->centred,
+                                        static_cast<unsigned long long*>(st), 0);
+    unsigned long long h[2] = {0, 0};
+    if (e == cudaSuccess) e = cudaMemcpy(h, st, sizeof(h), cudaMemcpyDeviceToHost);
+    cudaFree(st);
+    if (e != cudaSuccess) return cuda_fail(e, "user spectra copy");
+    std::memcpy(&p->tightness, &h[0], sizeof(double));
+    std::memcpy(&p->asymmetry, &h[1], sizeof(double));
+  }
+  return FFST_OK;
+}
+
+// Forward, arbitrary n: F = DFT2(f) (rows, transpose, rows: Ft = F^T); per chunk of planes the
+// windowed first pass along omega_2 (lines of Ft) -> transpose -> second pass along omega_1
+// straight into the cube (1/n^2).  With a communicator: images broadcast from rank 0 first.
+ffst_status forward_generic(ffst_plan* p, const void* img, void* coeff, int batch, cudaStream_t s) {
+  const bool coll = p->comm != nullptr;
+  const void* src = coll && p->d.shard_rank != 0 ? p->stage : img;
+  if (!src || !coeff) return fail(FFST_ERR_INVALID_ARG, "null buffer");
+  if (batch < 1 || batch > p->d.batch) return fail(FFST_ERR_INVALID_ARG, "batch outside 1..plan batch");
+  if (!aligned16(src) || !aligned16(coeff)) return fail(FFST_ERR_ALIGNMENT, "buffers must be 16-byte aligned");
+  TRY(set_device(p));
+  const GenParams g = gen_params(p, batch);
+  const double inv_nn = 1.0 / ((double)p->n * p->n);
+  int nl = 0;
+  if (p->timing) API_CUDA(cudaEventRecord(p->ev[0], s), "event");
+  if (coll) {
+    API_CUDA(cudaEventRecord(p->cev[0], s), "event");
+    API_CUDA(cudaStreamWaitEvent(p->cs, p->cev[0], 0), "stream wait");
+    API_NCCL(ncclBroadcast(src, const_cast<void*>(src), (size_t)batch * p->n * p->n, nccl_type(p), 0, p->comm, p->cs),
+             "ncclBroadcast (images)");
+    API_CUDA(cudaEventRecord(p->cev[1], p->cs), "event");
+    API_CUDA(cudaStreamWaitEvent(s, p->cev[1], 0), "stream wait");
+  }
+  API_CUDA(G_rows(p, GEN_OP_SPEC, g, src, p->S, 1, 0, 0, 1.0, 0, batch, s), "arbitrary-n spectrum rows");
+  API_CUDA(G_transpose(p, p->S, p->Ft, batch, s), "transpose");
+  API_CUDA(G_rows(p, GEN_OP_DFT, g, p->Ft, p->Ft, 1, 0, 0, 1.0, 0, batch, s), "arbitrary-n spectrum columns");
+  nl += 3;
+  if (p->timing) API_CUDA(cudaEventRecord(p->ev[1], s), "event");
+  for (int p0 = 0; p0 < p->eta_l; p0 += p->gen_np) {
+    const int np = std::min(p->gen_np, p->eta_l - p0);
+    API_CUDA(G_rows(p, GEN_OP_FWD_COL, g, p->Ft, p->Wt, np, p0, 0, 1.0, 0, batch * np, s), "arbitrary-n forward pass 1");
+    API_CUDA(G_transpose(p, p->Wt, p->W2, batch * np, s), "transpose");
+    API_CUDA(G_rows(p, GEN_OP_IDFT, g, p->W2, coeff, np, p0, 0, inv_nn, 2, batch * np, s), "arbitrary-n forward pass 2");
+    nl += 3;
+  }
+  if (p->timing) {
+    API_CUDA(cudaEventRecord(p->ev[2], s), "event");
+  }
+  p->launches[0] = nl;
+  return FFST_OK;
+}
+
+// Inverse, arbitrary n: per chunk, DFT of the cube rows -> transpose -> per line of At the sum over
+// the chunk's planes of psi_i * DFT (eq:inverseShearletTransform); then f = Re IDFT2(A).  With a
+// communicator: At summed onto root (ncclReduce), the final synthesis on the root only.
+ffst_status inverse_generic(ffst_plan* p, const void* coeff, void* img_out, int batch, int root_rank, cudaStream_t s) {
+  const bool coll = p->comm != nullptr;
+  if (coll && (root_rank < 0 || root_rank >= p->d.shard_count)) return fail(FFST_ERR_INVALID_ARG, "root outside 0..shard_count-1");
+  const bool root = !coll || p->d.shard_rank == root_rank;
+  if (!coeff || (root && !img_out)) return fail(FFST_ERR_INVALID_ARG, "null buffer");
+  if (batch < 1 || batch > p->d.batch) return fail(FFST_ERR_INVALID_ARG, "batch outside 1..plan batch");
+  if (!aligned16(coeff) || (root && !aligned16(img_out))) return fail(FFST_ERR_ALIGNMENT, "buffers must be 16-byte aligned");
+  TRY(set_device(p));
+  const GenParams g = gen_params(p, batch);
+  const double inv_nn = 1.0 / ((double)p->n * p->n);
+  int nl = 0;
+  if (p->timing) API_CUDA(cudaEventRecord(p->ev[3], s), "event");
+  if (p->timing) API_CUDA(cudaEventRecord(p->ev[4], s), "event");
+  for (int p0 = 0; p0 < p->eta_l; p0 += p->gen_np) {
+    const int np = std::min(p->gen_np, p->eta_l - p0);
+    API_CUDA(G_rows(p, GEN_OP_DFT, g, coeff, p->W2, np, p0, 0, 1.0, 1, batch * np, s), "arbitrary-n inverse pass 1");
+    API_CUDA(G_transpose(p, p->W2, p->Wt, batch * np, s), "transpose");
+    API_CUDA(G_rows(p, GEN_OP_INV_COL, g, p->Wt, p->At, np, p0, p0 == 0, 1.0, 0, batch, s), "arbitrary-n inverse pass 2");
+    nl += 3;
+  }
+  if (p->timing) API_CUDA(cudaEventRecord(p->ev[5], s), "event");
+  if (coll) {
+    API_CUDA(cudaEventRecord(p->cev[5], s), "event");
+    API_CUDA(cudaStreamWaitEvent(p->cs, p->cev[5], 0), "stream wait");
+    API_NCCL(ncclReduce(p->At, p->At, (size_t)batch * p->n * p->n * 2, nccl_type(p), ncclSum, root_rank, p->comm, p->cs),
+             "ncclReduce (adjoint spectra)");
+    API_CUDA(cudaEventRecord(p->cev[1], p->cs), "event");
+    API_CUDA(cudaStreamWaitEvent(s, p->cev[1], 0), "stream wait");
+  }
+  if (root) {
+    API_CUDA(G_rows(p, GEN_OP_IDFT, g, p->At, p->S, 1, 0, 0, 1.0, 0, batch, s), "arbitrary-n final pass 1");
+    API_CUDA(G_transpose(p, p->S, p->Ft, batch, s), "transpose");
+    API_CUDA(G_rows(p, GEN_OP_FINAL, g, p->Ft, img_out, 1, 0, 0, inv_nn, 0, batch, s), "arbitrary-n final pass 2");
+    nl += 3;
+  }
+  if (p->timing) API_CUDA(cudaEventRecord(p->ev[6], s), "event");
+  p->launches[1] = nl;
+  return FFST_OK;
+}
+
+// User spectra (f4): run the prepare kernels (ffst_user.cuh) on the caller's eta planes, keep the
+// admission numbers, and replace each local plane's provisional geometry by its column hull and
+// Nyquist flag.  `anti` receives the anti parts of every local plane ([eta_l][2][n], float64).
 
 ffst_status user_prepare(ffst_plan* p, const UserSpectra& us, std::vector<double>& anti) {
   const int n = p->n, H = n / 2, L = p->eta_l;
@@ -962,7 +1200,6 @@ ffst_status ffst_params_to_index(int j0, int kind, int j, int k, int* index) {
 ffst_status ffst_plane_support(int n, int j0, int index, int* col_lo, int* col_hi) {
   if (!col_lo || !col_hi) return fail(FFST_ERR_INVALID_ARG, "null output");
   if (n < 4) return fail(FFST_ERR_INVALID_SIZE, "n < 4");
-  if (!is_pow2(n)) return fail(FFST_ERR_UNSUPPORTED, "n must be a power of two");
   if (j0 == 0) j0 = default_j0(n);
   if (j0 < 1 || j0 > 12) return fail(FFST_ERR_INVALID_ARG, "j0 outside 1..12");
   if (index < 0 || index >= ffst_num_shearlets(j0)) return fail(FFST_ERR_INDEX, "index outside 0..eta-1");
@@ -973,11 +1210,11 @@ ffst_status ffst_plane_support(int n, int j0, int index, int* col_lo, int* col_h
 ffst_status ffst_plane_is_nyquist(int n, int j0, int index, int* is_nyquist) {
   if (!is_nyquist) return fail(FFST_ERR_INVALID_ARG, "null output");
   if (n < 4) return fail(FFST_ERR_INVALID_SIZE, "n < 4");
-  if (!is_pow2(n)) return fail(FFST_ERR_UNSUPPORTED, "n must be a power of two");
   if (j0 == 0) j0 = default_j0(n);
   if (j0 < 1 || j0 > 12) return fail(FFST_ERR_INVALID_ARG, "j0 outside 1..12");
   if (index < 0 || index >= ffst_num_shearlets(j0)) return fail(FFST_ERR_INDEX, "index outside 0..eta-1");
-  *is_nyquist = plane_nyquist(n, j0, index_table(j0)[index], FFST_CLASSIC) ? 1 : 0;
+  // odd n: the grid is point-symmetric (no -n/2 bin), every plane is symmetric
+  *is_nyquist = n % 2 == 0 && plane_nyquist(n, j0, index_table(j0)[index], FFST_CLASSIC) ? 1 : 0;
   return FFST_OK;
 }
 
@@ -985,7 +1222,6 @@ ffst_status ffst_shard_planes(int n, int j0, int shard_count, int shard_rank, ff
                               int* global_indices) {
   if (!count) return fail(FFST_ERR_INVALID_ARG, "null output");
   if (n < 4) return fail(FFST_ERR_INVALID_SIZE, "n < 4");
-  if (!is_pow2(n)) return fail(FFST_ERR_UNSUPPORTED, "n must be a power of two");
   if (j0 == 0) j0 = default_j0(n);
   if (j0 < 1 || j0 > 12) return fail(FFST_ERR_INVALID_ARG, "j0 outside 1..12");
   if (policy != FFST_SHARD_LPT && policy != FFST_SHARD_ROUND_ROBIN) return fail(FFST_ERR_INVALID_ARG, "unknown policy");
@@ -1065,6 +1301,23 @@ ffst_status ffst_plan_create_user(ffst_plan** out, const ffst_plan_desc* d, int 
   return plan_create_impl(out, d, &us);
 }
 
+// The library's exchange steps (desc.nccl_comm): the communicator must be the shard_count ranks,
+// rank = shard_rank; a comm stream and its events.
+static ffst_status setup_comm(ffst_plan* p, const ffst_plan_desc* d) {
+  if (d->nccl_comm == nullptr) return FFST_OK;
+  p->comm = static_cast<ncclComm_t>(d->nccl_comm);
+  int cn = 0, cr = -1;
+  if (ncclCommCount(p->comm, &cn) != ncclSuccess || ncclCommUserRank(p->comm, &cr) != ncclSuccess)
+    return fail(FFST_ERR_NCCL, "nccl_comm is not a valid communicator");
+  if (cn != d->shard_count || cr != d->shard_rank)
+    return fail(FFST_ERR_INVALID_ARG, "nccl_comm size / rank differ from shard_count / shard_rank");
+  cudaError_t e = cudaStreamCreateWithFlags(&p->cs, cudaStreamNonBlocking);
+  for (auto& ev : p->cev)
+    if (e == cudaSuccess) e = cudaEventCreateWithFlags(&ev, cudaEventDisableTiming);
+  if (e != cudaSuccess) return cuda_fail(e, "comm stream / events");
+  return FFST_OK;
+}
+
 static ffst_status plan_create_impl(ffst_plan** out, const ffst_plan_desc* d_in, const UserSpectra* us) {
   *out = nullptr;
   ffst_plan_desc desc = *d_in;
@@ -1074,7 +1327,11 @@ static ffst_status plan_create_impl(ffst_plan** out, const ffst_plan_desc* d_in,
   if (d->dtype != FFST_F32 && d->dtype != FFST_F64) return fail(FFST_ERR_DTYPE, "dtype must be FFST_F32 or FFST_F64");
   const int maxn = d->dtype == FFST_F32 ? 4096 : 2048;
   if (d->n > maxn) return fail(FFST_ERR_INVALID_SIZE, "n above the largest built size (4096 f32, 2048 f64)");
-  if (!is_pow2(d->n)) return fail(FFST_ERR_UNSUPPORTED, "n must be a power of two in this build");
+  // arbitrary n (odd, or even but not a power of two): the full complex path
+  bool generic = !is_pow2(d->n);
+  if (generic && d->n > 2048) return fail(FFST_ERR_UNSUPPORTED, "n not a power of two: built up to n = 2048");
+  if (d->shard_policy != FFST_SHARD_LPT && d->shard_policy != FFST_SHARD_ROUND_ROBIN)
+    return fail(FFST_ERR_INVALID_ARG, "unknown shard policy");
   if (d->variant != FFST_CLASSIC && d->variant != FFST_SMOOTH && d->variant != FFST_USER)
     return fail(FFST_ERR_INVALID_ARG, "unknown variant");
   if (d->batch < 1) return fail(FFST_ERR_INVALID_ARG, "batch < 1");
@@ -1091,9 +1348,7 @@ static ffst_status plan_create_impl(ffst_plan** out, const ffst_plan_desc* d_in,
   p->n = d->n; p->j0 = j0; p->eta = eta; p->H = d->n / 2;
   p->rsz = d->dtype == FFST_F32 ? 4 : 8;
   p->delta = grid_delta(d->n, j0);
-  p->geo = d->dtype == FFST_F32 ? geometry<float>(d->n) : geometry<double>(d->n);
-  if (d->shard_policy != FFST_SHARD_LPT && d->shard_policy != FFST_SHARD_ROUND_ROBIN)
-    return fail(FFST_ERR_INVALID_ARG, "unknown shard policy");
+  if (!generic) p->geo = d->dtype == FFST_F32 ? geometry<float>(d->n) : geometry<double>(d->n);
   const auto table = index_table(j0);
   // plane-to-rank map: LPT by default (user spectra: round robin, the order ffst_user.cuh reads)
   const std::vector<int> owner = us ? shard_owner(d->n, j0, eta, d->shard_count, FFST_SHARD_ROUND_ROBIN)
@@ -1111,12 +1366,12 @@ static ffst_status plan_create_impl(ffst_plan** out, const ffst_plan_desc* d_in,
       int lo, hi;
       plane_columns(d->n, j0, table[i], &lo, &hi);
       P.c_lo = lo; P.ncols = hi - lo + 1;
-      if (plane_nyquist(d->n, j0, table[i], d->variant)) {
+      if (!generic && plane_nyquist(d->n, j0, table[i], d->variant)) {
         P.nyq = (int)p->nyq.size();
         p->nyq.push_back((int)p->planes.size());
       }
     }
-    P.ncols_pad = (P.ncols + p->geo.colpad - 1) / p->geo.colpad * p->geo.colpad;
+    P.ncols_pad = generic ? P.ncols : (P.ncols + p->geo.colpad - 1) / p->geo.colpad * p->geo.colpad;
     p->planes.push_back(P);
   }
   p->eta_l = (int)p->planes.size();
@@ -1131,6 +1386,39 @@ static ffst_status plan_create_impl(ffst_plan** out, const ffst_plan_desc* d_in,
   int dev = d->device;
   e = cudaDeviceGetAttribute(&p->sm_count, cudaDevAttrMultiProcessorCount, dev);
   if (e != cudaSuccess) return cleanup(cuda_fail(e, "device query"));
+  if (us && !generic && d->n <= 2048) {
+    // user spectra that are not point-symmetric off the Nyquist lines cannot use the Hermitian
+    // fast path: they run on the full complex (arbitrary-n) path, which takes any Psi
+    void* st = nullptr;
+    e = cudaMalloc(&st, 2 * sizeof(unsigned long long));
+    if (e == cudaSuccess) e = cudaMemset(st, 0, 2 * sizeof(unsigned long long));
+    if (e == cudaSuccess)
+      e = d->dtype == FFST_F32 ? launch_gen_user<float>(us->psi, nullptr, d->n, nullptr, 0, us->eta, us->centred,
+                                                         static_cast<unsigned long long*>(st), 0)
+                               : launch_gen_user<double>(us->psi, nullptr, d->n, nullptr, 0, us->eta, us->centred,
+                                                          static_cast<unsigned long long*>(st), 0);
+    unsigned long long h[2] = {0, 0};
+    if (e == cudaSuccess) e = cudaMemcpy(h, st, sizeof(h), cudaMemcpyDeviceToHost);
+    cudaFree(st);
+    if (e != cudaSuccess) return cleanup(cuda_fail(e, "user spectra symmetry probe"));
+    double asym = 0.0;
+    std::memcpy(&asym, &h[1], sizeof(double));
+    if (!(asym <= (d->dtype == FFST_F32 ? 1e-5 : 1e-12))) generic = true;
+  }
+  if (generic) {
+    p->generic = true;
+    p->geo = Geometry{};
+    ffst_status sg = generic_setup(p, us);
+    if (sg != FFST_OK) return cleanup(sg);
+    for (auto& ev : p->ev) {
+      e = cudaEventCreate(&ev);
+      if (e != cudaSuccess) return cleanup(cuda_fail(e, "event create"));
+    }
+    sg = setup_comm(p, d);
+    if (sg != FFST_OK) return cleanup(sg);
+    *out = p;
+    return FFST_OK;
+  }
   {
     const int af = d->dtype == FFST_F32 ? max_active_main<float>(d->n, dev, 0) : max_active_main<double>(d->n, dev, 0);
     const int ai = d->dtype == FFST_F32 ? max_active_main<float>(d->n, dev, 1) : max_active_main<double>(d->n, dev, 1);
@@ -1275,18 +1563,9 @@ static ffst_status plan_create_impl(ffst_plan** out, const ffst_plan_desc* d_in,
   }
   e = cudaStreamCreateWithFlags(&p->aux, cudaStreamNonBlocking);
   if (e != cudaSuccess) return cleanup(cuda_fail(e, "stream create"));
-  if (d->nccl_comm != nullptr) {
-    // the library's exchange steps: the communicator must be the shard_count ranks, rank = shard_rank
-    p->comm = static_cast<ncclComm_t>(d->nccl_comm);
-    int cn = 0, cr = -1;
-    if (ncclCommCount(p->comm, &cn) != ncclSuccess || ncclCommUserRank(p->comm, &cr) != ncclSuccess)
-      return cleanup(fail(FFST_ERR_NCCL, "nccl_comm is not a valid communicator"));
-    if (cn != d->shard_count || cr != d->shard_rank)
-      return cleanup(fail(FFST_ERR_INVALID_ARG, "nccl_comm size / rank differ from shard_count / shard_rank"));
-    e = cudaStreamCreateWithFlags(&p->cs, cudaStreamNonBlocking);
-    for (auto& ev : p->cev)
-      if (e == cudaSuccess) e = cudaEventCreateWithFlags(&ev, cudaEventDisableTiming);
-    if (e != cudaSuccess) return cleanup(cuda_fail(e, "comm stream / events"));
+  {
+    ffst_status sc = setup_comm(p, d);
+    if (sc != FFST_OK) return cleanup(sc);
   }
   Queue* q = nullptr;
   st = build_queue(p, d->batch, &q);
@@ -1333,6 +1612,30 @@ ffst_status ffst_plan_spectra_check(ffst_plan* p, double* tightness, double* asy
     // built-in systems: materialise the spectra once and reduce the same admission numbers
     if (p->d.shard_count != 1) return fail(FFST_ERR_UNSUPPORTED, "spectra check of a sharded built-in plan");
     TRY(set_device(p));
+    if (p->generic) {   // materialise the local (= all) spectra, reduce the admission numbers
+      const size_t bytes_g = (size_t)p->eta * p->n * p->n * p->rsz;
+      void *psi_g = nullptr, *st_g = nullptr;
+      cudaError_t eg = cudaMalloc(&psi_g, bytes_g);
+      if (eg == cudaSuccess) eg = cudaMalloc(&st_g, 2 * sizeof(unsigned long long));
+      if (eg == cudaSuccess) eg = cudaMemset(st_g, 0, 2 * sizeof(unsigned long long));
+      const GenParams g = gen_params(p, 1);
+      if (eg == cudaSuccess)
+        eg = p->d.dtype == FFST_F32 ? launch_gen_spectra<float>(g, psi_g, 0, 0) : launch_gen_spectra<double>(g, psi_g, 0, 0);
+      if (eg == cudaSuccess)
+        eg = p->d.dtype == FFST_F32
+                 ? launch_gen_user<float>(psi_g, nullptr, p->n, nullptr, 0, p->eta, 0, static_cast<unsigned long long*>(st_g), 0)
+                 : launch_gen_user<double>(psi_g, nullptr, p->n, nullptr, 0, p->eta, 0, static_cast<unsigned long long*>(st_g), 0);
+      unsigned long long hg[2] = {0, 0};
+      if (eg == cudaSuccess) eg = cudaMemcpy(hg, st_g, sizeof(hg), cudaMemcpyDeviceToHost);
+      cudaFree(psi_g);
+      cudaFree(st_g);
+      if (eg != cudaSuccess) { cudaGetLastError(); return cuda_fail(eg, "spectra check"); }
+      std::memcpy(&p->tightness, &hg[0], sizeof(double));
+      std::memcpy(&p->asymmetry, &hg[1], sizeof(double));
+      *tightness = p->tightness;
+      *asymmetry = p->asymmetry;
+      return FFST_OK;
+    }
     const size_t bytes = (size_t)p->eta * p->n * p->n * p->rsz;
     void *psi = nullptr, *st = nullptr;
     cudaError_t e = cudaMalloc(&psi, bytes);
@@ -1365,6 +1668,13 @@ ffst_status ffst_plan_spectra_check(ffst_plan* p, double* tightness, double* asy
 ffst_status ffst_shearlet_spectra(ffst_plan* p, void* psi, int centred, void* stream) {
   if (!p || !psi) return fail(FFST_ERR_INVALID_ARG, "null argument");
   TRY(set_device(p));
+  if (p->generic) {
+    const cudaError_t eg = p->d.dtype == FFST_F32
+        ? launch_gen_spectra<float>(gen_params(p, 1), psi, centred, static_cast<cudaStream_t>(stream))
+        : launch_gen_spectra<double>(gen_params(p, 1), psi, centred, static_cast<cudaStream_t>(stream));
+    if (eg != cudaSuccess) return cuda_fail(eg, "spectra kernel");
+    return FFST_OK;
+  }
   KParams k = base_params(p);
   cudaError_t e = p->d.dtype == FFST_F32
                       ? launch_spectra_export<float>(k, psi, centred, static_cast<cudaStream_t>(stream))
@@ -1443,7 +1753,7 @@ ffst_status ffst_expand_compact(ffst_plan* p, const void* coeff_re, const void* 
   if (batch < 1 || batch > p->d.batch) return fail(FFST_ERR_INVALID_ARG, "batch outside 1..plan batch");
   if (!aligned16(coeff_re) || !aligned16(nyq_gh) || !aligned16(coeff))
     return fail(FFST_ERR_ALIGNMENT, "buffers must be 16-byte aligned");
-  if (p->n % 2 != 0) return fail(FFST_ERR_UNSUPPORTED, "compact format: even n only");
+  if (p->generic) return fail(FFST_ERR_UNSUPPORTED, "compact format: power-of-two n (fast path) only");
   TRY(set_device(p));
   KParams k = base_params(p);
   const cudaError_t e = p->d.dtype == FFST_F32

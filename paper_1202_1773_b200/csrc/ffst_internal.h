@@ -79,6 +79,7 @@ struct KParams {
   const void* usym;             // user spectra: [eta_l][n/2+1][n] T symmetric parts (ffst_user.cuh), else nullptr
   int compact;                  // f1 compact format: cube of reals + Nyquist vectors (G, H) in nyq_fwd
   int dbg;                      // measurement only (FFST_DBG): bit 0 skip FFTs, bit 1 skip output stores
+  int sync_mode;                // dependency ordering: bit 0 acquire fence after waits, bit 1 release on WAR-only signals
   unsigned long long* trace;    // optional: per item {smid, t_start, t_ready, t_end} (globaltimer ns)
 };
 
@@ -120,5 +121,16 @@ template <typename T> cudaError_t launch_spectra_export(const KParams& p, void* 
 template <typename T> cudaError_t launch_expand_compact(const KParams& p, const void* re, const void* gh, void* out,
                                                         int batch, cudaStream_t s);
 template <typename T> int max_active_main(int n, int device, int which);   // CTAs/SM of fwd (0) / inv (1)
+
+// Arbitrary-n path (ffst_generic.cuh, ffst_gen_launch.cuh).
+struct GenParams;
+enum { GEN_OP_SPEC = 0, GEN_OP_DFT = 1, GEN_OP_IDFT = 2, GEN_OP_FWD_COL = 3, GEN_OP_INV_COL = 4, GEN_OP_FINAL = 5 };
+template <typename T> cudaError_t launch_gen_rows(int op, const GenParams& g, const void* src, void* dst, int np,
+                                                  int p0, int first, double scale, int cube_side, int cube_eta,
+                                                  int mats, cudaStream_t s);
+template <typename T> cudaError_t launch_gen_transpose(const void* src, void* dst, int n, int mats, cudaStream_t s);
+template <typename T> cudaError_t launch_gen_spectra(const GenParams& g, void* psi, int centred, cudaStream_t s);
+template <typename T> cudaError_t launch_gen_user(const void* psi, void* out, int n, const int* gidx, int eta_l,
+                                                  int eta, int centred, unsigned long long* stats, cudaStream_t s);
 
 }  // namespace ffst

@@ -135,10 +135,10 @@ __shared__ unsigned long long s_probe[4];   // intra-item probes (trace mode)
 // cooperative grid barrier).  So an item's reads of a producer's ring slot or accumulator lane,
 // and its writes into a slot that earlier readers release, are ordered after the dependency.
 // One fence per satisfied wait (per item), not per poll.
-__device__ __forceinline__ void spin_wait(const int* ctr, int target) {
+__device__ __forceinline__ void spin_wait(const int* ctr, int target, int sync_mode = 3) {
   const volatile int* v = ctr;
   while (*v < target) __nanosleep(40);
-  asm volatile("fence.acq_rel.gpu;" ::: "memory");
+  if (sync_mode & 1) asm volatile("fence.acq_rel.gpu;" ::: "memory");
 }
 __device__ __forceinline__ void red_release(int* ctr, int v) {
   asm volatile("red.release.gpu.global.add.s32 [%0], %1;" ::"l"(ctr), "r"(v) : "memory");
@@ -972,8 +972,8 @@ __device__ __forceinline__ void persistent_loop(const KParams& p) {
     if (p.trace != nullptr && threadIdx.x == 0) t_start = gtimer();
     if (I.type == 1) {
       if (threadIdx.x == 0) {
-        spin_wait(p.ctr + I.wait_ctr, I.wait_tgt);
-        if (I.wait2_ctr >= 0) spin_wait(p.ctr + I.wait2_ctr, 1);
+        spin_wait(p.ctr + I.wait_ctr, I.wait_tgt, p.sync_mode);
+        if (I.wait2_ctr >= 0) spin_wait(p.ctr + I.wait2_ctr, 1, p.sync_mode);
       }
       __syncthreads();
     }
@@ -982,7 +982,8 @@ __device__ __forceinline__ void persistent_loop(const KParams& p) {
     else K<T, N>::inv_item(p, I, s_planes, smem);
     __syncthreads();
     if (threadIdx.x == 0) {
-      red_release(p.ctr + I.sig_ctr, 1);     // RAW (another item reads what this one wrote) or WAR (slot reuse)
+      if (!FWD || I.type == 0 || (p.sync_mode & 2)) red_release(p.ctr + I.sig_ctr, 1);   // RAW or WAR
+      else asm volatile("red.relaxed.gpu.global.add.s32 [%0], %1;" ::"l"(p.ctr + I.sig_ctr), "r"(1) : "memory");
       if (I.sig2_ctr >= 0) red_release(p.ctr + I.sig2_ctr, 1);
     }
     if (p.trace != nullptr && threadIdx.x == 0) {
