@@ -51,7 +51,7 @@ def _uncropped(n, i):
     return O.ffst_oracle._spectrum_on_grid(w1, w2, kind, j, k)
 
 
-@pytest.mark.parametrize("n", [4, 8, 16, 32, 64, 128, 256])
+@pytest.mark.parametrize("n", [4, 8, 16, 32, 64, 128, 256, 33, 48, 65, 100])
 def test_pruning_range_is_a_superset(n):
     # the kernels evaluate sym(psi) only on columns |u1| in [lo, hi]; the oracle's
     # (uncropped) spectrum must vanish on every other column.
@@ -65,12 +65,16 @@ def test_pruning_range_is_a_superset(n):
         assert np.all(np.abs(cols) >= lo) and np.all(np.abs(cols) <= hi), (n, i, lo, hi)
 
 
-@pytest.mark.parametrize("n", [4, 8, 16, 32, 64, 128])
+@pytest.mark.parametrize("n", [4, 8, 16, 32, 64, 128, 33, 48, 65, 100])
 def test_nyquist_classification(n):
     # a plane has an anti-symmetric part on the even grid iff psi(u1,-n/2) != psi(u1,+n/2) or
     # psi(-n/2,u2) != psi(+n/2,u2) somewhere.
+    # odd n: the grid has no -n/2 bin: no plane has a Nyquist part
     j0 = O.scales_for_size(n)
     for i in range(O.num_shearlets(j0)):
+        if n % 2:
+            assert not F.plane_is_nyquist(n, i)
+            continue
         s = _uncropped(n, i)
         differs = (np.max(np.abs(s[0, :] - s[-1, :])) > 1e-12) or (np.max(np.abs(s[:, 0] - s[:, -1])) > 1e-12)
         assert F.plane_is_nyquist(n, i) == differs, (n, i)
@@ -80,6 +84,6 @@ def test_invalid_sizes_rejected():
     with pytest.raises(F.FFSTError):
         F.plane_support(3, 0)
     with pytest.raises(F.FFSTError):
-        F.plane_support(48, 0)           # not a power of two: UNSUPPORTED in this build
+        F.shard_planes(64, 30, 0)        # more shards than the 29 planes
     with pytest.raises(F.FFSTError):
         F.plane_support(64, 29)
