@@ -439,7 +439,7 @@ ffst_status build_queue(ffst_plan* p, int batch, Queue** out) {
   // ---- 3. items (self-contained; counters: [0] dispatch, [1 + c] pass-1 done, [1 + C + c] pass-2 done,
   //      [1 + 2C + g] inverse column-group flags)
   std::vector<std::vector<ItemDev>> f1(C), f2(C), i1(C), i2(C);
-  const int ngroups = (H + 1 + g.lpc - 1) / g.lpc;
+  const int ngroups = (H + 1 + g.igc - 1) / g.igc;
   std::vector<int> last_self((size_t)batch * K * ngroups, -1);
   int n_self = 0;
   auto mk_item = [](int type, int c, int group, int b, int pl, int np, int woff, int slot) {
@@ -461,7 +461,7 @@ ffst_status build_queue(ffst_plan* p, int batch, Queue** out) {
     }
     for (int gg = 0; gg < ngroups; ++gg) {
       bool touched = ch.first_of_image != 0;
-      const int g0 = gg * g.lpc, g1 = std::min(g0 + g.lpc, H + 1);
+      const int g0 = gg * g.igc, g1 = std::min(g0 + g.igc, H + 1);
       for (int u = ch.unit0; u < ch.unit0 + ch.nunits && !touched; ++u) {
         const PlaneDev& P = p->planes[units[u].p];
         if (g1 > P.c_lo && g0 < P.c_lo + P.ncols) touched = true;

@@ -101,7 +101,8 @@ struct Geometry {
   int rp2;           // fwd pass 2: rows per item
   int rpi;           // inv pass 1: rows per item
   int gr;            // inv pass 1: rows per tile
-  int lpc;           // inv pass 2: columns per item
+  int lpc;           // columns per round of the column kernels
+  int igc;           // inv pass 2: columns per item (column group of the accumulation chain)
   size_t smem_fwd, smem_inv, smem_aux;   // dynamic shared bytes of the kernels
   int colpad;        // forward intermediate: row stride = ncols rounded up to a multiple of colpad
   int ncpf;          // final column pass (aux kernels, Geo): padded row stride of its output

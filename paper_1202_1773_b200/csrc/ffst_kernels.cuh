@@ -46,7 +46,9 @@ struct Geo {
   static constexpr bool DIRECT = (long long)N * GCP * ESZ > 65536;
   static constexpr int TILE_CE = DIRECT ? 0 : TILE_C;     // tile elements allocated
   // forward pass 2 / final rows: rows per item (~128 KB of output)
-  static constexpr int RP2_ = (131072 / (N * ESZ)) > LPR ? (131072 / (N * ESZ)) : LPR;
+  // (n >= 2048: at least 16 rows -- per-item overhead and the Nyquist-term staging amortised)
+  static constexpr int RP2_A = (131072 / (N * ESZ)) > LPR ? (131072 / (N * ESZ)) : LPR;
+  static constexpr int RP2_ = (N >= 2048 && RP2_A < 16) ? 16 : RP2_A;
   static constexpr int RP2 = RP2_ < N ? RP2_ : N;
   static constexpr int RPF = LPR < N ? LPR : N;     // final row pass: one round per CTA (more CTAs)
   // inverse pass 1: rows per tile and per item
@@ -58,6 +60,10 @@ struct Geo {
   static constexpr int RPI = RPI_ < N ? RPI_ : N;
   // padded row stride of the final column pass output
   static constexpr int NCPF = ((H + 1 + GC - 1) / GC) * GC;
+  // inverse pass 2: column groups of LPC columns per round, IG rounds per item (n >= 2048: one
+  // column per round, so an item is four column FFTs over its chunk's planes)
+  static constexpr int IG = N >= 2048 ? 4 : 1;
+  static constexpr int IGC = IG * LPC;
   // per-thread window values (EC reals per thread), staged in shared memory so the window
   // arithmetic is not unrolled into the FFT's register footprint
   static constexpr int WBUF = NT * EC * (int)sizeof(T) / ESZ;      // in complex elements
@@ -795,47 +801,50 @@ struct K {
     const C* tw = static_cast<const C*>(p.tw);
     const T delta = (T)p.delta;
     const Radial<T> R = radial_of<T, N>(p);
-    const int g0 = I.group * G::LPC;
-    const int g1 = g0 + G::LPC < H + 1 ? g0 + G::LPC : H + 1;
-    const int cb = g0 + line;
-    const bool act = cb <= H;
-    const int u1 = cb == H ? -H : cb;
     const C* slot = static_cast<const C*>(p.W) + (size_t)I.slot * p.slot_elems;
     T* wbuf = reinterpret_cast<T*>(smem + G::SCR_C);
-    C acc[G::EC];
-#pragma unroll
-    for (int q = 0; q < G::EC; ++q) acc[q] = czero<T>();
-    int woff = I.woff;
 #pragma unroll 1
-    for (int u = 0; u < I.np; ++u) {
-      const PlaneDev& P = splanes[I.p + u];
-      const int cur = woff;
-      woff += N * P.ncols_pad;
-      if (g1 <= P.c_lo || g0 >= P.c_lo + P.ncols) continue;          // CTA-uniform
-      const bool in = act && cb >= P.c_lo && cb < P.c_lo + P.ncols;
-      const C* col = slot + cur + (size_t)(in ? cb - P.c_lo : 0) * N;
-      C r[G::EC];
+    for (int rd = 0; rd < G::IG; ++rd) {
+      const int g0 = I.group * G::IGC + rd * G::LPC;
+      if (g0 > H) break;                                             // CTA-uniform
+      const int g1 = g0 + G::LPC < H + 1 ? g0 + G::LPC : H + 1;
+      const int cb = g0 + line;
+      const bool act = cb <= H;
+      C acc[G::EC];
 #pragma unroll
-      for (int q = 0; q < G::EC; ++q) r[q] = in ? __ldcg(col + t + q * G::THC) : czero<T>();
-      window_lines(P, g0, in, wbuf, scr, R, delta, user_plane<T, N>(p, P));
-      LineFFT<T, N, false, N>::run(r, scr + line * G::SMC, t, tw);
-      if (in) {
+      for (int q = 0; q < G::EC; ++q) acc[q] = czero<T>();
+      int woff = I.woff;
+#pragma unroll 1
+      for (int u = 0; u < I.np; ++u) {
+        const PlaneDev& P = splanes[I.p + u];
+        const int cur = woff;
+        woff += N * P.ncols_pad;
+        if (g1 <= P.c_lo || g0 >= P.c_lo + P.ncols) continue;          // CTA-uniform
+        const bool in = act && cb >= P.c_lo && cb < P.c_lo + P.ncols;
+        const C* col = slot + cur + (size_t)(in ? cb - P.c_lo : 0) * N;
+        C r[G::EC];
+#pragma unroll
+        for (int q = 0; q < G::EC; ++q) r[q] = in ? __ldcg(col + t + q * G::THC) : czero<T>();
+        window_lines(P, g0, in, wbuf, scr, R, delta, user_plane<T, N>(p, P));
+        LineFFT<T, N, false, N>::run(r, scr + line * G::SMC, t, tw);
+        if (in) {
+#pragma unroll
+          for (int q = 0; q < G::EC; ++q) {
+            const T w = wbuf[q * NT + tid];
+            acc[q].x += w * r[q].x;
+            acc[q].y += w * r[q].y;
+          }
+        }
+        SyncOf<G::THC>::sync();
+      }
+      if (act) {
+        C* a = static_cast<C*>(p.A) + (size_t)I.pad1 * p.a_lane_elems + ((size_t)I.b * (H + 1) + cb) * N;
 #pragma unroll
         for (int q = 0; q < G::EC; ++q) {
-          const T w = wbuf[q * NT + tid];
-          acc[q].x += w * r[q].x;
-          acc[q].y += w * r[q].y;
+          const int idx = t + q * G::THC;
+          if (I.first) __stcg(a + idx, acc[q]);
+          else red_add<T>(a + idx, acc[q]);          // no read-modify-write latency
         }
-      }
-      SyncOf<G::THC>::sync();
-    }
-    if (act) {
-      C* a = static_cast<C*>(p.A) + (size_t)I.pad1 * p.a_lane_elems + ((size_t)I.b * (H + 1) + cb) * N;
-#pragma unroll
-      for (int q = 0; q < G::EC; ++q) {
-        const int idx = t + q * G::THC;
-        if (I.first) __stcg(a + idx, acc[q]);
-        else red_add<T>(a + idx, acc[q]);          // no read-modify-write latency
       }
     }
   }

@@ -25,7 +25,7 @@ template <typename T, int N> struct Launch {
   using G = Geo<T, N>;
   static Geometry geometry() {
     Geometry g{};
-    g.nt = G::NT; g.gc = G::GC; g.rp2 = G::RP2; g.rpi = G::RPI; g.gr = G::GR; g.lpc = G::LPC;
+    g.nt = G::NT; g.gc = G::GC; g.rp2 = G::RP2; g.rpi = G::RPI; g.gr = G::GR; g.lpc = G::LPC; g.igc = G::IGC;
     g.smem_fwd = G::SMEM_FWD; g.smem_inv = G::SMEM_INV; g.smem_aux = G::SMEM_AUX;
     g.colpad = G::GC; g.ncpf = G::NCPF;
     return g;
