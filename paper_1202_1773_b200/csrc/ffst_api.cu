@@ -299,6 +299,9 @@ struct ffst_plan {
   cudaEvent_t fork[2] = {};
   int launches[2] = {0, 0};
   std::vector<void*> allocs;
+  // small-n fused path (ffst_tiny.cuh): one CTA per (plane, image), n <= 64
+  bool tiny = false;
+  void* part = nullptr;           // [batch][eta_l][n][n] T partial images of its inverse
   // arbitrary-n path (ffst_generic.cuh): full complex 2-D transforms, Bluestein line DFTs
   bool generic = false;
   int gen_M = 0, gen_np = 0;      // Bluestein FFT length, planes per chunk
@@ -620,6 +623,7 @@ KParams base_params(ffst_plan* p) {
   k.tw = p->d_tw;
   k.rtab = p->d_rtab;
   k.F = p->F; k.Fscr = p->Fscr; k.A = p->A; k.W = p->W;
+  k.part = p->part;
   k.nyq_fwd = p->nyq_fwd; k.nyq_S = p->nyq_S; k.nyq_T = p->nyq_T; k.corr = p->corr; k.nyq_anti = p->nyq_anti; k.nyq_part = p->nyq_part;
   k.n_rowitems = p->n_rowitems;
   k.rpi = p->rpi;
@@ -732,6 +736,22 @@ ffst_status forward_impl(ffst_plan* p, const void* img, void* coeff, int batch, 
   TRY(trace_buffer(p, 0, q->n_fwd, &k));
   int nl = 0;
   if (p->timing) API_CUDA(cudaEventRecord(p->ev[0], s), "event");
+  if (p->tiny && nyq_gh == nullptr) {   // fused small-n path: one launch
+    if (coll) {
+      API_CUDA(cudaEventRecord(p->cev[0], s), "event");
+      API_CUDA(cudaStreamWaitEvent(p->cs, p->cev[0], 0), "stream wait");
+      API_NCCL(ncclBroadcast(src, const_cast<void*>(src), (size_t)batch * p->n * p->n, nccl_type(p), 0, p->comm, p->cs),
+               "ncclBroadcast (images)");
+      API_CUDA(cudaEventRecord(p->cev[1], p->cs), "event");
+      API_CUDA(cudaStreamWaitEvent(s, p->cev[1], 0), "stream wait");
+    }
+    if (p->timing) API_CUDA(cudaEventRecord(p->ev[1], s), "event");
+    API_CUDA(p->d.dtype == FFST_F32 ? launch_tiny<float>(k, batch, 0, s) : launch_tiny<double>(k, batch, 0, s),
+             "tiny forward kernel");
+    if (p->timing) API_CUDA(cudaEventRecord(p->ev[2], s), "event");
+    p->launches[0] = 1;
+    return FFST_OK;
+  }
   if (coll) {
     const size_t img_elems = (size_t)p->n * p->n;
     const size_t h1n = (size_t)(p->n / 2 + 1) * p->n;
@@ -814,6 +834,24 @@ ffst_status inverse_impl(ffst_plan* p, const void* coeff, void* img_out, int bat
   TRY(trace_buffer(p, 1, q->n_inv, &k));
   int nl = 0;
   if (p->timing) API_CUDA(cudaEventRecord(p->ev[3], s), "event");
+  if (p->tiny && nyq_gh == nullptr) {   // fused small-n path: partial images, summed in plane order
+    k.img_out = root ? img_out : p->stage;
+    if (p->timing) API_CUDA(cudaEventRecord(p->ev[4], s), "event");
+    API_CUDA(p->d.dtype == FFST_F32 ? launch_tiny<float>(k, batch, 1, s) : launch_tiny<double>(k, batch, 1, s),
+             "tiny inverse kernels");
+    if (p->timing) API_CUDA(cudaEventRecord(p->ev[5], s), "event");
+    if (coll) {   // the partial image sums of the ranks onto root (the inverse is linear in the planes)
+      API_CUDA(cudaEventRecord(p->cev[5], s), "event");
+      API_CUDA(cudaStreamWaitEvent(p->cs, p->cev[5], 0), "stream wait");
+      API_NCCL(ncclReduce(k.img_out, k.img_out, (size_t)batch * p->n * p->n, nccl_type(p), ncclSum, root_rank, p->comm,
+                          p->cs), "ncclReduce (images)");
+      API_CUDA(cudaEventRecord(p->cev[1], p->cs), "event");
+      API_CUDA(cudaStreamWaitEvent(s, p->cev[1], 0), "stream wait");
+    }
+    if (p->timing) API_CUDA(cudaEventRecord(p->ev[6], s), "event");
+    p->launches[1] = 2;
+    return FFST_OK;
+  }
   API_CUDA(cudaMemsetAsync(p->d_ctr, 0, (1 + 2 * (size_t)q->n_chunks + q->n_g) * sizeof(int), s), "counter reset");
   if (p->timing) API_CUDA(cudaEventRecord(p->ev[4], s), "event");
   API_CUDA(L_inv_main(p, k, p->grid_inv, s), "inv_main kernel");
@@ -1504,6 +1542,12 @@ static ffst_status plan_create_impl(ffst_plan** out, const ffst_plan_desc* d_in,
   ALLOC(p->nyq_anti, nn * 2 * N * p->rsz);
   ALLOC(p->nyq_part, B * 2 * std::min<size_t>(nn, 64) * N * csz);
   ALLOC(p->stage, B * N * N * p->rsz);
+  {
+    // the fused small-n path (FFST_TINY=0 keeps the persistent kernels; tuning / tests only)
+    const char* et = std::getenv("FFST_TINY");
+    p->tiny = d->n <= 64 && d->variant != FFST_USER && B * p->eta_l * N * N <= (64u << 20) && !(et && std::atoi(et) == 0);
+    if (p->tiny) ALLOC(p->part, B * p->eta_l * N * N * p->rsz);
+  }
 #undef ALLOC
   std::vector<unsigned char> tw;
   if (d->dtype == FFST_F32) fill_twiddles<float>(tw, d->n); else fill_twiddles<double>(tw, d->n);

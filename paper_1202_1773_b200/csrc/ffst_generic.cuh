@@ -97,7 +97,7 @@ enum { GEN_SPEC = 0, GEN_PLAIN = 1, GEN_FWD_COL = 2, GEN_INV_COL = 3, GEN_FINAL 
 template <typename T, int M, int MODE, bool INVDFT>
 __global__ void __launch_bounds__(256) gen_rows_kernel(GenParams g, const void* src, void* dst, int np, int p0,
                                                        int first, T scale, int cube_side, int cube_eta) {
-  extern __shared__ __align__(16) unsigned char smem_raw[];
+  extern __shared__ __align__(128) unsigned char smem_raw[];
   using B = Bluestein<T, M>;
   using C = cpx<T>;
   constexpr int TH = B::TH, E = B::E;

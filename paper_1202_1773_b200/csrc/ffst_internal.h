@@ -65,6 +65,7 @@ struct KParams {
   void* nyq_T;                  // [batch][n_nyq][n] T: alternating row sums
   void* corr;                   // [batch][2][n] T: inverse Nyquist corrections
   void* nyq_part;               // [batch][2][<=64][n] cpx<T>: partial Nyquist spectra (stage 1 -> 2)
+  void* part;                   // small-n fused path: [batch][eta_l][n][n] T partial images of the inverse
   const void* nyq_anti;         // [n_nyq][2][n] T: anti part of each Nyquist plane on the Nyquist row (0) /
                                 //   column (1), natural bin order (plan table)
   int n_rowitems;               // inverse pass-1 items per plane (row groups)
@@ -122,6 +123,7 @@ template <typename T> cudaError_t launch_spectra_export(const KParams& p, void* 
 template <typename T> cudaError_t launch_expand_compact(const KParams& p, const void* re, const void* gh, void* out,
                                                         int batch, cudaStream_t s);
 template <typename T> int max_active_main(int n, int device, int which);   // CTAs/SM of fwd (0) / inv (1)
+template <typename T> cudaError_t launch_tiny(const KParams& p, int batch, int which, cudaStream_t s);   // n <= 64
 
 // Arbitrary-n path (ffst_generic.cuh, ffst_gen_launch.cuh).
 struct GenParams;

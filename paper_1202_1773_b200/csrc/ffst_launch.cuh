@@ -1,7 +1,7 @@
 // ffst_launch.cuh — host launchers: runtime n -> compile-time N dispatch.
 #pragma once
 #include <algorithm>
-#include "ffst_kernels.cuh"
+#include "ffst_tiny.cuh"
 #include "ffst_user.cuh"
 
 namespace ffst {
@@ -94,6 +94,24 @@ template <typename T, int N> struct Launch {
     spectra_kernel<T, N><<<grid, 256, 0, s>>>(p, static_cast<T*>(psi), centred);
     return cudaGetLastError();
   }
+  // fused small-n path (n <= 64): which = 0 forward, 1 inverse (two launches)
+  static cudaError_t tiny(const KParams& p, int batch, int which, cudaStream_t s) {
+    if constexpr (N <= 64) {
+      using TY = Tiny<T, N>;
+      if (which == 0) {
+        FFST_CHECK(set_smem(tiny_fwd_kernel<T, N>, TY::SMEM));
+        tiny_fwd_kernel<T, N><<<dim3(p.eta_l, batch), TY::NT, TY::SMEM, s>>>(p);
+        return cudaGetLastError();
+      }
+      FFST_CHECK(set_smem(tiny_inv_kernel<T, N>, TY::SMEM));
+      tiny_inv_kernel<T, N><<<dim3(p.eta_l, batch), TY::NT, TY::SMEM, s>>>(p);
+      FFST_CHECK(cudaGetLastError());
+      tiny_sum_kernel<T, N><<<dim3((N * N + 255) / 256, batch), 256, 0, s>>>(p);
+      return cudaGetLastError();
+    } else {
+      return cudaErrorInvalidValue;
+    }
+  }
   static int max_active(int which) {
     int nb = 0;
     if (which == 0) {
@@ -142,6 +160,8 @@ template <typename T, int N> struct Launch {
     FFST_DISPATCH(T, p.n, final_(p, b, which, s), cudaErrorInvalidValue) }                                            \
   template <> cudaError_t launch_spectra_export<T>(const KParams& p, void* psi, int c, cudaStream_t s) {       \
     FFST_DISPATCH(T, p.n, spectra(p, psi, c, s), cudaErrorInvalidValue) }                                      \
+  template <> cudaError_t launch_tiny<T>(const KParams& p, int b, int which, cudaStream_t s) {                 \
+    FFST_DISPATCH(T, p.n, tiny(p, b, which, s), cudaErrorInvalidValue) }                                       \
   template <> cudaError_t launch_expand_compact<T>(const KParams& p, const void* re, const void* gh, void* out,  \
                                                    int batch, cudaStream_t s) {                                 \
     const long long pairs = (long long)batch * p.eta_l * p.n * p.n / 2;                                       \

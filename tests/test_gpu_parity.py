@@ -57,9 +57,15 @@ def test_spectra_match_oracle(F, n, dtype):
 
 # ------------------------------------------------------------------ forward / inverse, small sizes
 
+@pytest.mark.parametrize("tiny", ["1", "0"])
 @pytest.mark.parametrize("n", [4, 8, 16, 32, 64, 128])
 @pytest.mark.parametrize("dtype", [torch.float64, torch.float32])
-def test_forward_inverse_small(F, n, dtype):
+def test_forward_inverse_small(F, n, dtype, tiny, monkeypatch):
+    # both schedules of small n: the fused one-CTA-per-plane kernels (n <= 64, default) and the
+    # persistent two-pass kernels (FFST_TINY=0)
+    if n > 64 and tiny == "0":
+        pytest.skip("n > 64 always runs the persistent kernels")
+    monkeypatch.setenv("FFST_TINY", tiny)
     batch = 3
     x, xo = images(2, batch, n, dtype)
     plan = F.Plan(n, batch, dtype)
@@ -110,6 +116,25 @@ def test_inverse_random_cube_adjoint(F, dtype):
     lhs = np.real(np.sum(c * np.conj(zo)))
     rhs = np.sum(xo * rec)
     assert abs(lhs - rhs) <= (1e-9 if dtype == torch.float64 else 1e-4) * abs(lhs)
+
+
+def test_tiny_path_matches_persistent_and_is_deterministic(F, monkeypatch):
+    # the fused small-n kernels and the persistent kernels compute the same transform (to
+    # rounding); the fused inverse sums the planes in a fixed order: bitwise reproducible
+    n, batch = 64, 4
+    x, xo = images(2, batch, n, torch.float64)
+    xd = x.cuda()
+    monkeypatch.setenv("FFST_TINY", "0")
+    ref_plan = F.Plan(n, batch, torch.float64)
+    monkeypatch.setenv("FFST_TINY", "1")
+    plan = F.Plan(n, batch, torch.float64)
+    c0 = ref_plan.forward(xd)
+    c1 = plan.forward(xd)
+    assert float((c0 - c1).abs().max() / c0.abs().max()) <= 1e-13
+    r1 = plan.inverse(c1).clone()
+    assert torch.equal(r1, plan.inverse(c1))
+    assert float((r1 - ref_plan.inverse(c0)).abs().max()) <= 1e-13
+    assert torch.equal(plan.forward(xd[1:3]), c1[1:3])
 
 
 def test_constant_image(F):
