@@ -20,7 +20,7 @@ namespace ffst {
 template <typename T, int N>
 struct Tiny {
   using C = cpx<T>;
-  static constexpr int NT = 256;
+  static constexpr int NT = 512;   // (the window and the plane I/O run on all threads, the line FFTs on N * TH)
   static constexpr int E = RadixPlan<N>::E, TH = N / E;
   static constexpr int LPR = NT / TH < N ? NT / TH : N;      // lines per round
   static constexpr int ROUNDS = N / LPR;
@@ -58,7 +58,7 @@ struct Tiny {
 
 // grid (eta_l, batch), Tiny::NT threads
 template <typename T, int N>
-__global__ void __launch_bounds__(256) tiny_fwd_kernel(KParams p) {
+__global__ void __launch_bounds__(512) tiny_fwd_kernel(KParams p) {
   using TY = Tiny<T, N>;
   using C = cpx<T>;
   extern __shared__ __align__(128) unsigned char smem_raw[];
@@ -89,7 +89,7 @@ __global__ void __launch_bounds__(256) tiny_fwd_kernel(KParams p) {
 
 // grid (eta_l, batch): part[b][i] = Re ifft2(psi_i * fft2(c_i)) / n^2
 template <typename T, int N>
-__global__ void __launch_bounds__(256) tiny_inv_kernel(KParams p) {
+__global__ void __launch_bounds__(512) tiny_inv_kernel(KParams p) {
   using TY = Tiny<T, N>;
   using C = cpx<T>;
   extern __shared__ __align__(128) unsigned char smem_raw[];
