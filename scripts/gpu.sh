@@ -7,6 +7,7 @@
 #   bash scripts/gpu.sh launches <cfg> <tag>          ncu launch list (gpu__time_duration, serialised)
 #   bash scripts/gpu.sh prof <cfg> <tag> [kernel-regex] [skip] [count]   ncu --set full capture
 #   bash scripts/gpu.sh env "<A=1 B=2;A=2>" "<cfgs>"  bench each ';'-separated environment set
+#   bash scripts/gpu.sh traffic <cfg> <tag>           ncu DRAM bytes per launch of the main kernels
 cd "${GRAFT_REPO_ROOT:-$(dirname "$0")/..}"
 mkdir -p gpurun_out
 task=$1; shift
@@ -43,6 +44,11 @@ case "$task" in
     ncu -i /tmp/prof_$tag.ncu-rep --page details --csv > gpurun_out/prof_${tag}_details.csv 2>&1
     ncu -i /tmp/prof_$tag.ncu-rep --page source --csv --print-source cuda,sass > /tmp/src.csv 2>&1
     gzip -c /tmp/src.csv > gpurun_out/prof_${tag}_source.csv.gz ;;
+  traffic) c=$1; tag=$2   # DRAM bytes per launch of the two persistent kernels (one eager step after warm-up)
+    CMD="python bench.py --config $c --steps 1 --warmup 1 --no-cpu-baseline --no-cufft --no-graph"
+    timeout 1800 ncu --metrics dram__bytes_read.sum,dram__bytes_write.sum,gpu__time_duration.sum --clock-control none \
+      -k regex:"main_kernel|tiny_" --csv --log-file gpurun_out/traffic_$tag.csv $CMD > gpurun_out/traffic_$tag.log 2>&1
+    echo "ncu traffic exit $?" ;;
   env) IFS=';' read -ra SETS <<< "$1"; cfgs=$2
     for e in "${SETS[@]}"; do for c in $cfgs; do
       env $e timeout 600 python bench.py --config "$c" --steps 5 --warmup 3 --no-cpu-baseline --no-cufft \
