@@ -158,7 +158,9 @@ ffst_status ffst_nccl_comm_destroy(void* comm);
  *   FFST_ACC_LANES      accumulator lanes of the inverse (default: up to 4, 16 for batch <= 4, while <= 32 MB)
  *   FFST_VERBOSE        print the queue geometry and the persistent grids
  *   FFST_CTAS_PER_SM    cap on resident CTAs per SM of the persistent kernels (default: occupancy)
- * Measurement only (results are WRONG): FFST_QUEUE_ONLY=1|2 (one pass type), FFST_DBG bits. */
+ * Measurement only (results are WRONG): FFST_QUEUE_ONLY=1|2 (one pass type), FFST_DBG bits (1 skip the
+ * FFTs, 2 skip the item output stores, 4 window = 1 on the support columns, 8 skip the Nyquist sums),
+ * FFST_SYNC (0..3: drop the acquire fences / the WAR releases). */
 ffst_status ffst_plan_create(ffst_plan** out, const ffst_plan_desc* desc);
 ffst_status ffst_plan_destroy(ffst_plan* plan);
 

@@ -197,9 +197,16 @@ struct K {
   // The lists live in the FFT scratch of the warp's own line(s) (used only by that warp's FFT,
   // after this call; lines longer than a warp are separated by a CTA barrier at the end).
   static __device__ __forceinline__ void window_lines(const PlaneDev& P, int cb0, bool act, T* wbuf, C* scr,
-                                                      const Radial<T>& R, T delta, const T* us) {
+                                                      const Radial<T>& R, T delta, const T* us,
+                                                      bool dbg_skip_window = false) {
     const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5, t = tid % G::THC;
     const int cb = cb0 + tid / G::THC;
+    if (dbg_skip_window) {                   // measurement only (FFST_DBG bit 2): window = 1 on the column
+#pragma unroll
+      for (int q = 0; q < G::EC; ++q) wbuf[q * NT + tid] = act ? T(1) : T(0);
+      SyncOf<G::THC>::sync();
+      return;
+    }
     if (us != nullptr) {   // user spectra (f4): the plane's symmetric part from its table, every row
 #pragma unroll
       for (int q = 0; q < G::EC; ++q) wbuf[q * NT + tid] = act ? us[(size_t)cb * N + t + q * G::THC] : T(0);
@@ -258,7 +265,7 @@ struct K {
       C r[G::EC];
       if constexpr (MODE == MODE_MAIN) {
         T* wbuf = reinterpret_cast<T*>(tile + G::TILE_CE);
-        window_lines(P, c0 + rd * G::LPC, act, wbuf, scr, R, delta, user_plane<T, N>(p, P));
+        window_lines(P, c0 + rd * G::LPC, act, wbuf, scr, R, delta, user_plane<T, N>(p, P), p.dbg & 4);
         if (rd == 0) FFST_PROBE(p, 0);
 #pragma unroll
         for (int q = 0; q < G::EC; ++q) {
@@ -277,14 +284,14 @@ struct K {
         }
       }
       if (rd == 0) FFST_PROBE(p, 1);
-      LineFFT<T, N, true, N>::run(r, scr + line * G::SMC, t, tw);
+      if (!(p.dbg & 1)) LineFFT<T, N, true, N>::run(r, scr + line * G::SMC, t, tw);
       if (rd == 0) FFST_PROBE(p, 2);
       if constexpr (G::DIRECT) {
         if (rd == 0 && dep != nullptr) {       // ring-slot reuse: wait only before writing dst
           if (tid == 0) spin_wait(dep, dep_target);
           __syncthreads();
         }
-        if (act) {
+        if (act && !(p.dbg & 2)) {
 #pragma unroll
           for (int q = 0; q < G::EC; ++q) dst[(size_t)(t + q * G::THC) * dst_stride + dst_col0 + ci] = r[q];
         }
@@ -413,7 +420,7 @@ struct K {
         z[q] = mk<T>(a.x - e.y, a.y + e.x);                 // a + i e
       }
       if (rd == 0) FFST_PROBE(p, 0);
-      LineFFT<T, H, true, N>::run(z, scr + line * G::SMR, t, tw);
+      if (!(p.dbg & 1)) LineFFT<T, H, true, N>::run(z, scr + line * G::SMR, t, tw);
       if (rd == 0) FFST_PROBE(p, 1);
       if (act) {
         const T sr = (r & 1) ? T(-1) : T(1);
@@ -428,7 +435,7 @@ struct K {
               i0 = sr * sG[m1] + hr;
               i1 = sr * sG[m1 + 1] - hr;
             }
-            store_pair_cs<T>(out_c + (size_t)r * N + m1, mk<T>(x0, i0), mk<T>(x1, i1));
+            if (!(p.dbg & 2)) store_pair_cs<T>(out_c + (size_t)r * N + m1, mk<T>(x0, i0), mk<T>(x1, i1));
           } else if constexpr (MODE == MODE_COMPACT) {   // real part only; the Nyquist term is (G, H)
             __stcs(reinterpret_cast<cpx<T>*>(out_r + (size_t)r * N + m1), mk<T>(x0, x1));
           } else {
@@ -661,7 +668,7 @@ struct K {
     T* red = reinterpret_cast<T*>(tile + G::TILE_R);        // NT/32 scalars past the tile
     const int tid = threadIdx.x, line = tid / G::THC, t = tid % G::THC;
     const C* tw = static_cast<const C*>(p.tw);
-    const bool nyq = !REAL && nyq_idx >= 0;
+    const bool nyq = !REAL && nyq_idx >= 0 && !(p.dbg & 8);
     constexpr int RPR = 2 * G::LPC;
     T sacc[G::EC];
 #pragma unroll
@@ -721,7 +728,7 @@ struct K {
         }
         if (ti == 0 && rd == 0) FFST_PROBE(p, 0);
         C* sl = scr + line * G::SMC;
-        LineFFT<T, N, false, N>::run(z, sl, t, tw);
+        if (!(p.dbg & 1)) LineFFT<T, N, false, N>::run(z, sl, t, tw);
         if (ti == 0 && rd == 0) FFST_PROBE(p, 1);
         if (nyq) {   // alternating row sums t(r) = sum_m1 (-1)^m1 Im c(r, m1) over the line's lanes
 #pragma unroll
@@ -768,7 +775,7 @@ struct K {
       __syncthreads();
       const int rows_here = cnt - ti * G::GR < G::GR ? cnt - ti * G::GR : G::GR;
 #pragma unroll 1
-      for (int e = tid; e < ncols * G::GR; e += NT) {
+      for (int e = tid; e < (p.dbg & 2 ? 0 : ncols * G::GR); e += NT) {
         const int kk = e / G::GR, ri = e - kk * G::GR;
         if (ri < rows_here) dst[(size_t)kk * N + rt0 + ri] = tile[ri * G::TSTR + kk];
       }
@@ -825,8 +832,8 @@ struct K {
         C r[G::EC];
 #pragma unroll
         for (int q = 0; q < G::EC; ++q) r[q] = in ? __ldcg(col + t + q * G::THC) : czero<T>();
-        window_lines(P, g0, in, wbuf, scr, R, delta, user_plane<T, N>(p, P));
-        LineFFT<T, N, false, N>::run(r, scr + line * G::SMC, t, tw);
+        window_lines(P, g0, in, wbuf, scr, R, delta, user_plane<T, N>(p, P), p.dbg & 4);
+        if (!(p.dbg & 1)) LineFFT<T, N, false, N>::run(r, scr + line * G::SMC, t, tw);
         if (in) {
 #pragma unroll
           for (int q = 0; q < G::EC; ++q) {

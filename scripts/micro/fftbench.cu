@@ -1,6 +1,7 @@
 // Micro-benchmark of the line-FFT building block (ffst_fft.cuh) at n = 4096, float32:
 // batched 4096-point C2C rows, HBM in -> HBM out, no window, no scheduling.  Measurement only.
 #include <cstdio>
+#include <cstdlib>
 #include <cuda_runtime.h>
 #include "../../paper_1202_1773_b200/csrc/ffst_fft.cuh"
 using namespace ffst;
@@ -42,8 +43,8 @@ __global__ void k_copy(const float4* __restrict__ in, float4* __restrict__ out, 
     __stcs(out + i, __ldcs(in + i));
 }
 
-int main() {
-  const int rows = 4096 * 4;                     // 4 planes of 4096 x 4096 complex: 537 MB in, 537 MB out
+int main(int argc, char** argv) {
+  const int rows = argc > 1 ? atoi(argv[1]) : 4096 * 4;   // default 4 planes of 4096^2 complex: 537 MB in / out
   const size_t bytes = (size_t)rows * N * sizeof(C);
   C *in, *out, *tw;
   cudaMalloc(&in, bytes); cudaMalloc(&out, bytes); cudaMalloc(&tw, N * sizeof(C));
@@ -54,11 +55,12 @@ int main() {
   int sms; cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, 0);
   cudaEvent_t e0, e1; cudaEventCreate(&e0); cudaEventCreate(&e1);
   auto timeit = [&](const char* name, auto launch) {
+    const int reps = rows < 4096 ? 200 : 10;
     for (int i = 0; i < 3; ++i) launch();
     cudaEventRecord(e0);
-    for (int i = 0; i < 10; ++i) launch();
+    for (int i = 0; i < reps; ++i) launch();
     cudaEventRecord(e1); cudaEventSynchronize(e1);
-    float ms; cudaEventElapsedTime(&ms, e0, e1); ms /= 10;
+    float ms; cudaEventElapsedTime(&ms, e0, e1); ms /= reps;
     cudaError_t err = cudaGetLastError();
     printf("%-40s %8.3f ms  %7.0f GB/s  %6.1f ns/line  %s\n", name, ms, 2.0 * bytes / ms / 1e6, ms * 1e6 / rows,
            err == cudaSuccess ? "" : cudaGetErrorString(err));
