@@ -44,7 +44,8 @@ struct Geo {
   // 12 % warps active at n = 4096); forward pass 1 then stores each column straight from
   // registers (8-byte stores whose sectors the item's GC columns complete in L2)
   static constexpr bool DIRECT = (long long)N * GCP * ESZ > 65536;
-  static constexpr int TILE_CE = DIRECT ? 0 : TILE_C;     // tile elements allocated
+  // (DIRECT: the tile region holds one column, so that stores go out as 16-byte column pairs)
+  static constexpr int TILE_CE = DIRECT ? N * (LPC > 1 ? LPC / 2 : 1) : TILE_C;     // tile elements allocated
   // forward pass 2 / final rows: rows per item (~128 KB of output)
   // (n >= 2048: at least 16 rows -- per-item overhead and the Nyquist-term staging amortised)
   static constexpr int RP2_A = (131072 / (N * ESZ)) > LPR ? (131072 / (N * ESZ)) : LPR;
@@ -291,9 +292,54 @@ struct K {
           if (tid == 0) spin_wait(dep, dep_target);
           __syncthreads();
         }
-        if (act && !(p.dbg & 2)) {
+        // Columns go out in pairs as 16-byte stores (half the L2 write requests of 8-byte column
+        // stores, and half sectors instead of quarter sectors): the even column of a pair waits in
+        // shared memory (`tile`, one column) for the odd one.  LPC = 1: consecutive rounds, the
+        // same thread holds the same rows in both (no barrier); LPC = 2: the two lines of a round.
+        constexpr bool ROUNDPAIR = G::LPC == 1;
+        const int cpair = ROUNDPAIR ? ci - (rd & 1) : ci - line;      // even column of the pair
+        const bool aligned = ((dst_col0 + cpair) & 1) == 0;
+        const bool has_odd = cpair + 1 < cnt;
+        const bool skip = p.dbg & 2;
+        if constexpr (ROUNDPAIR) {
+          if (!(rd & 1) && has_odd && aligned) {                     // even column: park it
+            if (act) {
 #pragma unroll
-          for (int q = 0; q < G::EC; ++q) dst[(size_t)(t + q * G::THC) * dst_stride + dst_col0 + ci] = r[q];
+              for (int q = 0; q < G::EC; ++q) tile[t + q * G::THC] = r[q];
+            }
+          } else if ((rd & 1) && aligned) {                          // odd column: store the pair
+            if (act && !skip) {
+#pragma unroll
+              for (int q = 0; q < G::EC; ++q)
+                store_pair_cg<T>(dst + (size_t)(t + q * G::THC) * dst_stride + dst_col0 + cpair, tile[t + q * G::THC], r[q]);
+            }
+          } else if (act && !skip) {                                  // single column
+#pragma unroll
+            for (int q = 0; q < G::EC; ++q) dst[(size_t)(t + q * G::THC) * dst_stride + dst_col0 + ci] = r[q];
+          }
+        } else {                                                     // LPC even: lines 2m, 2m+1
+          static_assert(G::LPC % 2 == 0, "column pairs of a round");
+          C* park = tile + (line >> 1) * N;
+          const bool odd = line & 1;
+          if (odd && act && aligned) {
+#pragma unroll
+            for (int q = 0; q < G::EC; ++q) park[t + q * G::THC] = r[q];
+          }
+          __syncthreads();
+          if (!odd && act && !skip) {
+            if (has_odd && aligned) {
+#pragma unroll
+              for (int q = 0; q < G::EC; ++q)
+                store_pair_cg<T>(dst + (size_t)(t + q * G::THC) * dst_stride + dst_col0 + ci, r[q], park[t + q * G::THC]);
+            } else {
+#pragma unroll
+              for (int q = 0; q < G::EC; ++q) dst[(size_t)(t + q * G::THC) * dst_stride + dst_col0 + ci] = r[q];
+            }
+          }
+          if (odd && act && !aligned && !skip) {
+#pragma unroll
+            for (int q = 0; q < G::EC; ++q) dst[(size_t)(t + q * G::THC) * dst_stride + dst_col0 + ci] = r[q];
+          }
         }
       } else if (ci < G::GC) {
 #pragma unroll

@@ -385,6 +385,24 @@ def test_adjoint_off_range_bench_geometry(F, cid):
         assert np.max(np.abs(rec[others])) == 0.0
 
 
+@pytest.mark.parametrize("n", [1024, 2048])
+def test_float64_large(F, n):
+    # float64 at large n (the column passes store columns straight from registers, in pairs): one
+    # plane of every (kind, j) pair and Nyquist planes against the oracle at 1e-10, round trip
+    x, xo = images(4, 1, n, torch.float64)
+    plan = F.Plan(n, 1, torch.float64)
+    xd = x.cuda()
+    c = plan.forward(xd)
+    rec = plan.inverse(c)
+    assert float((rec - xd).abs().max() / xd.abs().max()) <= 1e-10
+    base, eta = _kind_scale_planes(n)
+    nyq = plan.nyquist_planes()
+    planes = sorted(set(base) | {nyq[0], nyq[-1]})
+    ref = OP.forward_planes(xo[0], planes)
+    for i in planes:
+        assert plane_err(c[0, i].cpu().numpy(), ref[i], np.max(np.abs(xo[0]))) <= 1e-10, i
+
+
 def test_config5_forward_planes(F):
     # configs[4]: 4096x4096 float32 single image; the forward against the oracle on one plane of
     # every (kind, j) pair and on every finest-scale Nyquist plane; round trip and Parseval
