@@ -91,14 +91,47 @@ template <> __device__ __forceinline__ void store_pair_cs<double>(double2* dst, 
   __stcs(dst, a);
   __stcs(dst + 1, b);
 }
-// fire-and-forget accumulation in L2 (the accumulation chain orders the additions: deterministic)
-template <typename T> __device__ __forceinline__ void red_add(cpx<T>* dst, cpx<T> v);
-template <> __device__ __forceinline__ void red_add<float>(float2* dst, float2 v) {
-  asm volatile("red.relaxed.gpu.global.add.v2.f32 [%0], {%1, %2};" ::"l"(dst), "f"(v.x), "f"(v.y) : "memory");
+// L2 residency hints (createpolicy): the adjoint's accumulator A is read-modify-written by every
+// plane and is kept (evict_last); at n >= 2048 the intermediate ring (12+ slots of 27-52 MB) cannot
+// stay in L2 and is streamed (evict_first) so that it does not push A out.
+__device__ __forceinline__ unsigned long long policy_evict_last() {
+  unsigned long long p;
+  asm volatile("createpolicy.fractional.L2::evict_last.L2::evict_unchanged.b64 %0, 1.0;" : "=l"(p));
+  return p;
 }
-template <> __device__ __forceinline__ void red_add<double>(double2* dst, double2 v) {
-  asm volatile("red.relaxed.gpu.global.add.f64 [%0], %1;" ::"l"(&dst->x), "d"(v.x) : "memory");
-  asm volatile("red.relaxed.gpu.global.add.f64 [%0], %1;" ::"l"(&dst->y), "d"(v.y) : "memory");
+__device__ __forceinline__ unsigned long long policy_evict_first() {
+  unsigned long long p;
+  asm volatile("createpolicy.fractional.L2::evict_first.L2::evict_unchanged.b64 %0, 1.0;" : "=l"(p));
+  return p;
+}
+
+// fire-and-forget accumulation in L2 (the accumulation chain orders the additions: deterministic)
+template <typename T> __device__ __forceinline__ void red_add(cpx<T>* dst, cpx<T> v, unsigned long long pol);
+template <> __device__ __forceinline__ void red_add<float>(float2* dst, float2 v, unsigned long long pol) {
+  asm volatile("red.relaxed.gpu.global.add.L2::cache_hint.v2.f32 [%0], {%1, %2}, %3;" ::"l"(dst), "f"(v.x), "f"(v.y),
+               "l"(pol) : "memory");
+}
+template <> __device__ __forceinline__ void red_add<double>(double2* dst, double2 v, unsigned long long pol) {
+  asm volatile("red.relaxed.gpu.global.add.L2::cache_hint.f64 [%0], %1, %2;" ::"l"(&dst->x), "d"(v.x), "l"(pol) : "memory");
+  asm volatile("red.relaxed.gpu.global.add.L2::cache_hint.f64 [%0], %1, %2;" ::"l"(&dst->y), "d"(v.y), "l"(pol) : "memory");
+}
+template <typename T> __device__ __forceinline__ void st_hint(cpx<T>* dst, cpx<T> v, unsigned long long pol);
+template <> __device__ __forceinline__ void st_hint<float>(float2* dst, float2 v, unsigned long long pol) {
+  asm volatile("st.global.cg.L2::cache_hint.v2.f32 [%0], {%1, %2}, %3;" ::"l"(dst), "f"(v.x), "f"(v.y), "l"(pol) : "memory");
+}
+template <> __device__ __forceinline__ void st_hint<double>(double2* dst, double2 v, unsigned long long pol) {
+  asm volatile("st.global.cg.L2::cache_hint.v2.f64 [%0], {%1, %2}, %3;" ::"l"(dst), "d"(v.x), "d"(v.y), "l"(pol) : "memory");
+}
+template <typename T> __device__ __forceinline__ cpx<T> ld_hint(const cpx<T>* src, unsigned long long pol);
+template <> __device__ __forceinline__ float2 ld_hint<float>(const float2* src, unsigned long long pol) {
+  float2 v;
+  asm volatile("ld.global.cg.L2::cache_hint.v2.f32 {%0, %1}, [%2], %3;" : "=f"(v.x), "=f"(v.y) : "l"(src), "l"(pol));
+  return v;
+}
+template <> __device__ __forceinline__ double2 ld_hint<double>(const double2* src, unsigned long long pol) {
+  double2 v;
+  asm volatile("ld.global.cg.L2::cache_hint.v2.f64 {%0, %1}, [%2], %3;" : "=d"(v.x), "=d"(v.y) : "l"(src), "l"(pol));
+  return v;
 }
 template <typename T> __device__ __forceinline__ void store_pair_cg(cpx<T>* dst, cpx<T> a, cpx<T> b);
 template <> __device__ __forceinline__ void store_pair_cg<float>(float2* dst, float2 a, float2 b) {
@@ -821,9 +854,13 @@ struct K {
       __syncthreads();
       const int rows_here = cnt - ti * G::GR < G::GR ? cnt - ti * G::GR : G::GR;
 #pragma unroll 1
+      const unsigned long long pf = policy_evict_first();
       for (int e = tid; e < (p.dbg & 2 ? 0 : ncols * G::GR); e += NT) {
         const int kk = e / G::GR, ri = e - kk * G::GR;
-        if (ri < rows_here) dst[(size_t)kk * N + rt0 + ri] = tile[ri * G::TSTR + kk];
+        if (ri < rows_here) {
+          if constexpr (N >= 2048) st_hint<T>(dst + (size_t)kk * N + rt0 + ri, tile[ri * G::TSTR + kk], pf);
+          else dst[(size_t)kk * N + rt0 + ri] = tile[ri * G::TSTR + kk];
+        }
       }
       __syncthreads();
       if (ti == 0) FFST_PROBE(p, 3);
@@ -876,8 +913,14 @@ struct K {
         const bool in = act && cb >= P.c_lo && cb < P.c_lo + P.ncols;
         const C* col = slot + cur + (size_t)(in ? cb - P.c_lo : 0) * N;
         C r[G::EC];
+        if constexpr (N >= 2048) {
+          const unsigned long long pf = policy_evict_first();
 #pragma unroll
-        for (int q = 0; q < G::EC; ++q) r[q] = in ? __ldcg(col + t + q * G::THC) : czero<T>();
+          for (int q = 0; q < G::EC; ++q) r[q] = in ? ld_hint<T>(col + t + q * G::THC, pf) : czero<T>();
+        } else {
+#pragma unroll
+          for (int q = 0; q < G::EC; ++q) r[q] = in ? __ldcg(col + t + q * G::THC) : czero<T>();
+        }
         window_lines(P, g0, in, wbuf, scr, R, delta, user_plane<T, N>(p, P), p.dbg & 4);
         if (!(p.dbg & 1)) LineFFT<T, N, false, N>::run(r, scr + line * G::SMC, t, tw);
         if (in) {
@@ -892,11 +935,12 @@ struct K {
       }
       if (act) {
         C* a = static_cast<C*>(p.A) + (size_t)I.pad1 * p.a_lane_elems + ((size_t)I.b * (H + 1) + cb) * N;
+        const unsigned long long pl = policy_evict_last();
 #pragma unroll
         for (int q = 0; q < G::EC; ++q) {
           const int idx = t + q * G::THC;
-          if (I.first) __stcg(a + idx, acc[q]);
-          else red_add<T>(a + idx, acc[q]);          // no read-modify-write latency
+          if (I.first) st_hint<T>(a + idx, acc[q], pl);
+          else red_add<T>(a + idx, acc[q], pl);      // no read-modify-write latency
         }
       }
     }
