@@ -159,7 +159,8 @@ ffst_status ffst_nccl_comm_destroy(void* comm);
  *   FFST_VERBOSE        print the queue geometry and the persistent grids
  *   FFST_CTAS_PER_SM    cap on resident CTAs per SM of the persistent kernels (default: occupancy)
  * Measurement only (results are WRONG): FFST_QUEUE_ONLY=1|2 (one pass type), FFST_DBG bits (1 skip the
- * FFTs, 2 skip the item output stores, 4 window = 1 on the support columns, 8 skip the Nyquist sums),
+ * FFTs, 2 skip the item output stores, 4 window = 1 on the support columns, 8 skip the Nyquist sums,
+ * 32 the plain (not pipelined) inverse pass 1),
  * FFST_SYNC (0..3: drop the acquire fences / the WAR releases). */
 ffst_status ffst_plan_create(ffst_plan** out, const ffst_plan_desc* desc);
 ffst_status ffst_plan_destroy(ffst_plan* plan);

@@ -853,8 +853,8 @@ struct K {
       if (dep != nullptr && ti == 0 && tid == 0) spin_wait(dep, dep_target);   // slot reuse: before the first write
       __syncthreads();
       const int rows_here = cnt - ti * G::GR < G::GR ? cnt - ti * G::GR : G::GR;
-#pragma unroll 1
       const unsigned long long pf = policy_evict_first();
+#pragma unroll 1
       for (int e = tid; e < (p.dbg & 2 ? 0 : ncols * G::GR); e += NT) {
         const int kk = e / G::GR, ri = e - kk * G::GR;
         if (ri < rows_here) {
@@ -879,6 +879,96 @@ struct K {
         outp[m] = v;
       }
       __syncthreads();
+    }
+  }
+
+  // Inverse pass 1, pipelined variant (float32, n >= 1024, planes without a Nyquist part -- their
+  // imaginary parts are not needed -- and the compact rows): the real parts of the NEXT round's
+  // two rows are loaded into registers (2 x EC floats) before the current round's FFT, so the
+  // HBM fetch of the cube overlaps the arithmetic (the plain variant loads, then computes).
+  // Same results as row_r2c_pair.
+  template <bool REAL = false>
+  static __device__ void row_r2c_pair_pipe(const KParams& p, const C* __restrict__ src_c, int c_lo, int ncols,
+                                           int r0, int cnt, C* dst, C* smem, const int* dep, int dep_target) {
+    C* scr = smem;
+    C* tile = smem + G::SCRX;
+    const int tid = threadIdx.x, line = tid / G::THC, t = tid % G::THC;
+    const C* tw = static_cast<const C*>(p.tw);
+    constexpr int RPR = 2 * G::LPC;
+    constexpr int ROUNDS = G::GR / RPR > 0 ? G::GR / RPR : 1;
+    constexpr int STRIDE = REAL ? 1 : 2;                   // floats per element (real parts only)
+    const T* base = reinterpret_cast<const T*>(src_c);
+    const int nrounds = (cnt + RPR - 1) / RPR;
+    T ca[G::EC], cb[G::EC];
+    {
+      const int ri = 2 * line;
+      const bool act = ri < cnt;
+      const T* pa = base + (size_t)STRIDE * (act ? r0 + ri : r0) * N;
+#pragma unroll
+      for (int q = 0; q < G::EC; ++q) {
+        const int m = STRIDE * (t + q * G::THC);
+        ca[q] = act ? __ldcs(pa + m) : T(0);
+        cb[q] = act ? __ldcs(pa + STRIDE * N + m) : T(0);
+      }
+    }
+    const unsigned long long pf = policy_evict_first();
+#pragma unroll 1
+    for (int i = 0; i < nrounds; ++i) {
+      T na[G::EC], nb[G::EC];
+      {
+        const int ri = (i + 1) * RPR + 2 * line;
+        const bool act = i + 1 < nrounds && ri < cnt;
+        const T* pa = base + (size_t)STRIDE * (act ? r0 + ri : r0) * N;
+#pragma unroll
+        for (int q = 0; q < G::EC; ++q) {
+          const int m = STRIDE * (t + q * G::THC);
+          na[q] = act ? __ldcs(pa + m) : T(0);
+          nb[q] = act ? __ldcs(pa + STRIDE * N + m) : T(0);
+        }
+      }
+      const int rd = i % ROUNDS, ti = i / ROUNDS;
+      const int ri = rd * RPR + 2 * line;                  // first row of the pair inside the tile
+      const bool act = ti * G::GR + ri < cnt;
+      C z[G::EC];
+#pragma unroll
+      for (int q = 0; q < G::EC; ++q) z[q] = mk<T>(ca[q], cb[q]);
+      C* sl = scr + line * G::SMC;
+      if (!(p.dbg & 1)) LineFFT<T, N, false, N>::run(z, sl, t, tw);
+      SyncOf<G::THC>::sync();
+#pragma unroll
+      for (int q = 0; q < G::EC; ++q) sl[Pad<T>::at(t + q * G::THC)] = z[q];
+      SyncOf<G::THC>::sync();
+      if (act) {
+#pragma unroll 2
+        for (int kk = t; kk < ncols; kk += G::THC) {
+          const int k = c_lo + kk;                         // 0..H
+          const C zk = sl[Pad<T>::at(k)];
+          const C zm = sl[Pad<T>::at(k == 0 ? 0 : N - k)];
+          tile[ri * G::TSTR + kk] = mk<T>(T(0.5) * (zk.x + zm.x), T(0.5) * (zk.y - zm.y));
+          tile[(ri + 1) * G::TSTR + kk] = mk<T>(T(0.5) * (zk.y + zm.y), T(0.5) * (zm.x - zk.x));
+        }
+      }
+      SyncOf<G::THC>::sync();
+      if (rd == ROUNDS - 1 || i + 1 == nrounds) {          // the tile is complete: -> W (column-major)
+        if (dep != nullptr && ti == 0 && tid == 0) spin_wait(dep, dep_target);   // slot reuse
+        __syncthreads();
+        const int rt0 = r0 + ti * G::GR;
+        const int rows_here = cnt - ti * G::GR < G::GR ? cnt - ti * G::GR : G::GR;
+#pragma unroll 1
+        for (int e = tid; e < (p.dbg & 2 ? 0 : ncols * G::GR); e += NT) {
+          const int kk = e / G::GR, r = e - kk * G::GR;
+          if (r < rows_here) {
+            if constexpr (N >= 2048) st_hint<T>(dst + (size_t)kk * N + rt0 + r, tile[r * G::TSTR + kk], pf);
+            else dst[(size_t)kk * N + rt0 + r] = tile[r * G::TSTR + kk];
+          }
+        }
+        __syncthreads();
+      }
+#pragma unroll
+      for (int q = 0; q < G::EC; ++q) {
+        ca[q] = na[q];
+        cb[q] = nb[q];
+      }
     }
   }
 
@@ -1004,6 +1094,7 @@ struct K {
     }
   }
 
+  static constexpr bool PIPE_INV = sizeof(T) == 4 && N >= 1024;   // pipelined inverse pass 1
   static __device__ void inv_item(const KParams& p, const ItemDev& I, const PlaneDev* splanes, C* smem) {
     if (I.type == 0) {
       const PlaneDev& P = splanes[I.p];
@@ -1012,6 +1103,13 @@ struct K {
       const int cnt = N - r0 < p.rpi ? N - r0 : p.rpi;
       if (p.compact) {   // f1 format: real rows; the Nyquist sums come from (G, H) (nyq_compact_sums)
         const T* srcr = static_cast<const T*>(p.coeff) + ((size_t)I.b * p.eta_l + I.p) * N * N;
+        if constexpr (G::PAIR_INV && PIPE_INV) {
+          if (!(p.dbg & 32)) {
+            row_r2c_pair_pipe<true>(p, reinterpret_cast<const C*>(srcr), P.c_lo, P.ncols, r0, cnt, w, smem,
+                                    I.wait_ctr >= 0 ? p.ctr + I.wait_ctr : nullptr, I.wait_tgt);
+            return;
+          }
+        }
         if constexpr (G::PAIR_INV)
           row_r2c_pair<true>(p, reinterpret_cast<const C*>(srcr), P.c_lo, P.ncols, r0, cnt, w, I.b, -1, I.group, smem,
                              I.wait_ctr >= 0 ? p.ctr + I.wait_ctr : nullptr, I.wait_tgt);
@@ -1021,6 +1119,13 @@ struct K {
         return;
       }
       const C* src = static_cast<const C*>(p.coeff) + ((size_t)I.b * p.eta_l + I.p) * N * N;
+      if constexpr (G::PAIR_INV && PIPE_INV) {
+        if (P.nyq < 0 && !(p.dbg & 32)) {      // no Nyquist part: only the real parts are needed
+          row_r2c_pair_pipe<false>(p, src, P.c_lo, P.ncols, r0, cnt, w, smem,
+                                   I.wait_ctr >= 0 ? p.ctr + I.wait_ctr : nullptr, I.wait_tgt);
+          return;
+        }
+      }
       if constexpr (G::PAIR_INV)
         row_r2c_pair(p, src, P.c_lo, P.ncols, r0, cnt, w, I.b, P.nyq, I.group, smem,
                      I.wait_ctr >= 0 ? p.ctr + I.wait_ctr : nullptr, I.wait_tgt);
