@@ -76,8 +76,6 @@ struct Geo {
   static_assert(RPI % GR == 0, "RPI must be a multiple of GR");
   static_assert(!PAIR || (GR % (2 * LPC) == 0 || GR < 2 * LPC), "row-pair rounds must tile GR");
   static_assert(SCR_C * ESZ >= LPC * N * (int)sizeof(T), "row-pair column-sum scratch");
-  static_assert(THC <= 32 ? (32 / THC) * SMC * ESZ >= 64 * EC : SMC * ESZ >= (THC / 32) * 64 * EC,
-                "candidate lists must fit the warp's FFT scratch");
   static_assert(GC % LPC == 0 || LPC > GC, "GC vs LPC");
 };
 
@@ -189,18 +187,6 @@ __device__ __forceinline__ void red_release(int* ctr, int v) {
 // even for idle lanes (clamped row / column indices).  Observed with cuda-gdb: a hoisted __ldg of
 // the user-spectra table through a null pointer (illegal address, n = 16, 32).
 //
-// Candidate-list entries live in the FFT scratch (complex-typed) of the warp's own lines; they
-// are stored and loaded with asm volatile + "memory" clobber so that no type-based alias analysis
-// can move the FFT's scratch accesses across them.
-__device__ __forceinline__ void sts_u16(unsigned short* a, unsigned short v) {
-  asm volatile("st.shared.u16 [%0], %1;" ::"r"((unsigned)__cvta_generic_to_shared(a)), "h"(v) : "memory");
-}
-__device__ __forceinline__ unsigned short lds_u16(const unsigned short* a) {
-  unsigned short v;
-  asm volatile("ld.shared.u16 %0, [%1];" : "=h"(v) : "r"((unsigned)__cvta_generic_to_shared(a)) : "memory");
-  return v;
-}
-
 // the plan's radial tables (classic rows; smooth rows after them when p.variant == 1)
 template <typename T, int N>
 __device__ __forceinline__ Radial<T> radial_of(const KParams& p) {
@@ -223,17 +209,14 @@ struct K {
   static constexpr int NT = G::NT;
 
   // Window sym_i of the CTA's column lines into wbuf[q * NT + tid] (thread tid's element q = row
-  // t + q THC of column cb0 + tid / THC).  The support is ~10 % of the rows: each warp first
-  // compacts its candidate elements (exact integer prefilter, ballot + prefix count) into `list`,
-  // then evaluates them converged, 32 at a time -- instead of every lane paying the divergent
-  // window code on every element.  All threads of the CTA call it; act = the thread's column is
-  // one to window.
-  // The lists live in the FFT scratch of the warp's own line(s) (used only by that warp's FFT,
-  // after this call; lines longer than a warp are separated by a CTA barrier at the end).
+  // t + q THC of column cb0 + tid / THC).  The support is ~10 % of the rows: the line's threads
+  // enumerate only the candidate rows (integer intervals from col_bounds) and evaluate them
+  // converged -- no per-element test.  All threads of the CTA call it; act = the thread's column
+  // is one to window.
   static __device__ __forceinline__ void window_lines(const PlaneDev& P, int cb0, bool act, T* wbuf, C* scr,
                                                       const Radial<T>& R, T delta, const T* us,
                                                       bool dbg_skip_window = false) {
-    const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5, t = tid % G::THC;
+    const int tid = threadIdx.x, t = tid % G::THC;
     const int cb = cb0 + tid / G::THC;
     if (dbg_skip_window) {                   // measurement only (FFST_DBG bit 2): window = 1 on the column
 #pragma unroll
@@ -248,28 +231,35 @@ struct K {
       return;
     }
     const int u1 = cb == H ? -H : cb;
-    const int w0 = warp * 32;    // first thread of the warp
-    unsigned short* wl = reinterpret_cast<unsigned short*>(scr + (w0 / G::THC) * G::SMC) +
-                         ((w0 % G::THC) / 32) * (32 * G::EC);
-    ColBounds bnd{1, 0, 1, 0};
-    if (act) bnd = col_bounds<T>(P, u1, H, delta);
-    int count = 0;
 #pragma unroll
-    for (int q = 0; q < G::EC; ++q) {
-      const int rb = t + q * G::THC;
-      const bool cand = act && (cb == H || rb == H || col_candidate(bnd, centred(rb, N)));
-      wbuf[q * NT + tid] = T(0);
-      const unsigned m = __ballot_sync(0xffffffffu, cand);
-      if (cand) sts_u16(wl + count + __popc(m & ((1u << lane) - 1u)), (unsigned short)((q << 5) | lane));
-      count += __popc(m);
-    }
-    __syncwarp();
+    for (int q = 0; q < G::EC; ++q) wbuf[q * NT + tid] = T(0);
+    SyncOf<G::THC>::sync();
+    if (act) {
+      if (cb == H) {                         // the Nyquist column: every row (the thread's own)
 #pragma unroll 1
-    for (int k = lane; k < count; k += 32) {
-      const int e = lds_u16(wl + k);
-      const int q = e >> 5, tid2 = warp * 32 + (e & 31);
-      const int cb2 = cb0 + tid2 / G::THC, rb2 = tid2 % G::THC + q * G::THC;
-      wbuf[q * NT + tid2] = window_sym<T>(P, cb2 == H ? -H : cb2, centred(rb2, N), H, R);
+        for (int q = 0; q < G::EC; ++q) wbuf[q * NT + tid] = window_sym<T>(P, u1, centred(t + q * G::THC, N), H, R);
+      } else {
+        // The candidate rows of the column (a superset of the support, exact integer bounds) are
+        // at most three u2 intervals -- the horizontal wedge [hlo, hhi] and the vertical band
+        // alo <= |u2| <= ahi on either side -- plus the Nyquist row u2 = -n/2: the line's threads
+        // enumerate them and write each value into the slot of the thread that owns the row
+        // (an overlap of two intervals writes the same value twice).
+        const ColBounds bnd = col_bounds<T>(P, u1, H, delta);
+        const int h0 = bnd.hlo > -H ? bnd.hlo : -H, h1 = bnd.hhi < H - 1 ? bnd.hhi : H - 1;
+        const int nh = h1 >= h0 ? h1 - h0 + 1 : 0;
+        const int ap = bnd.ahi < H - 1 ? bnd.ahi : H - 1, an = bnd.ahi < H ? bnd.ahi : H;
+        const int np = ap >= bnd.alo ? ap - bnd.alo + 1 : 0, nn = an >= bnd.alo ? an - bnd.alo + 1 : 0;
+        const int K = nh + np + nn + 1;
+        const int lbase = tid - t;           // first thread of this line
+#pragma unroll 1
+        for (int i = t; i < K; i += G::THC) {
+          const int u2 = i < nh ? h0 + i
+                       : i < nh + np ? bnd.alo + (i - nh)
+                       : i < nh + np + nn ? -(bnd.alo + (i - nh - np)) : -H;
+          const int rb = u2 < 0 ? u2 + N : u2;
+          wbuf[(rb / G::THC) * NT + lbase + rb % G::THC] = window_sym<T>(P, u1, u2, H, R);
+        }
+      }
     }
     SyncOf<G::THC>::sync();
   }
@@ -294,7 +284,6 @@ struct K {
       const int ci = rd * G::LPC + line;
       const bool act = ci < cnt;
       const int cb = c0 + ci;
-      const int u1 = cb == H ? -H : cb;
       const C* col = src + (size_t)(act ? cb : c0) * N;   // in range even for idle lines (hoisted loads)
       C r[G::EC];
       if constexpr (MODE == MODE_MAIN) {
@@ -1333,7 +1322,6 @@ __global__ void __launch_bounds__(256) nyq_inv_kernel(KParams p) {
   extern __shared__ __align__(128) unsigned char smem_raw[];
   using G = Geo<T, N>;
   using C = cpx<T>;
-  constexpr int H = N / 2;
   const int which = blockIdx.x, b = blockIdx.y;
   const int tid = threadIdx.x, line = tid / G::THC, t = tid % G::THC;
   const C* tw = static_cast<const C*>(p.tw);
