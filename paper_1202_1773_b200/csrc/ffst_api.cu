@@ -1621,6 +1621,7 @@ static ffst_status plan_create_impl(ffst_plan** out, const ffst_plan_desc* d_in,
 ffst_status ffst_plan_reserve(ffst_plan* p, int batch) {
   if (!p) return fail(FFST_ERR_INVALID_ARG, "null plan");
   if (batch < 1 || batch > p->d.batch) return fail(FFST_ERR_INVALID_ARG, "batch outside 1..plan batch");
+  if (p->generic) return FFST_OK;          // the arbitrary-n path has no work queues
   TRY(set_device(p));
   Queue* q = nullptr;
   return build_queue(p, batch, &q);

@@ -28,11 +28,14 @@ def F():
 
 
 def plane_err(g, o, floor_scale=1.0):
+    # reading A15: normwise per plane; a plane whose oracle values are zero up to rounding (e.g.
+    # cos(pi/2) = 6e-17 at a band edge, reading A12) is compared in absolute terms, / max|f|
     g = np.asarray(g)
     o = np.asarray(o)
     num = np.max(np.abs(g - o), axis=(-2, -1))
     den = np.max(np.abs(o), axis=(-2, -1))
-    return np.where(den > 0, num / np.where(den > 0, den, 1.0), num / floor_scale)
+    small = den < 1e-12 * floor_scale
+    return np.where(small, num / floor_scale, num / np.where(small, 1.0, den))
 
 
 def images(cid, batch, n, dtype):
@@ -713,6 +716,43 @@ def test_arbitrary_n(F, n, dtype):
         assert plane_err(rec[b], xo[b]).max() <= TOL[dtype]
         if n % 2 == 1:
             assert np.max(np.abs(c[b].imag)) <= TOL[dtype] * np.max(np.abs(c[b]))
+
+
+@pytest.mark.parametrize("n,j0", [(64, 2), (64, 4), (100, 2), (33, 3), (256, 5)])
+def test_non_default_scales(F, n, j0):
+    # numOfScales: any j0 up to default + 1 (reading A17); power-of-two and arbitrary n
+    x, xo = images(2, 2, n, torch.float64)
+    plan = F.Plan(n, 2, torch.float64, j0=j0)
+    assert plan.j0 == j0 and plan.eta == O.num_shearlets(j0)
+    c = plan.forward(x.cuda())
+    rec = plan.inverse(c).cpu().numpy()
+    c = c.cpu().numpy()
+    psi = O.shearlet_spectra(n, j0)
+    for b in range(2):
+        assert plane_err(c[b], O.forward(xo[b], psi=psi), np.max(np.abs(xo[b]))).max() <= 1e-10
+        assert plane_err(rec[b], xo[b]).max() <= 1e-10
+
+
+def test_smaller_batches_all_paths(F):
+    # a call with fewer images than the plan's batch (first use reserves its queue where the path
+    # has one): the fused small-n path, the persistent kernels, the arbitrary-n path
+    for n in (32, 128, 45):
+        plan = F.Plan(n, 5, torch.float32)
+        x, xo = images(2, 5, n, torch.float32)
+        c_all = plan.forward(x.cuda())
+        c_two = plan.forward(x[1:3].cuda())
+        assert float((c_two - c_all[1:3]).abs().max()) <= 1e-6 * float(c_all.abs().max())
+        r_two = plan.inverse(c_two).cpu().numpy()
+        assert plane_err(r_two, xo[1:3]).max() <= 1e-4
+
+
+def test_nccl_comm_must_match_the_shards(F):
+    comm = F.NcclComm(1, 0, torch.cuda.current_device(), F.NcclComm.unique_id())
+    try:
+        with pytest.raises(F.FFSTError):
+            F.Plan(64, 1, torch.float32, shard_rank=0, shard_count=2, nccl_comm=comm)
+    finally:
+        comm.close()
 
 
 @pytest.mark.parametrize("n", [33, 100])
