@@ -478,7 +478,8 @@ def run_gpu(args, cfg):
     # dominant kernel roofline: the persistent forward / inverse kernels (per-rank cube stream)
     fm, im = float(np.mean(fwd_main)), float(np.mean(inv_main))
     local_cube = B * eta_l * N * N * 2 * rsz
-    dom_name, dom_ms = ("fwd_main", fm) if fm >= im else ("inv_main", im)
+    names = ("tiny_fwd", "tiny_inv") if plan.path == "fused_small" else ("fwd_main", "inv_main")
+    dom_name, dom_ms = (names[0], fm) if fm >= im else (names[1], im)
     achieved = local_cube / (dom_ms / 1000.0) / 1e9
     traffic = None
     tpath = os.path.join(ROOT, "profiles", "traffic.json")
@@ -601,6 +602,7 @@ def run_gpu(args, cfg):
                          "unit": "GB/s", "frac": achieved / peak, "traffic": traffic,
                          "peak_source": peak_src,
                          "bytes_per_launch": local_cube,
+                         "path": plan.path,
                          "kernel_ms": {"fwd_main": fm, "inv_main": im,
                                        "fwd_total": float(np.mean(fwd_tot)), "inv_total": float(np.mean(inv_tot))}},
             "cpu_baseline": cpu,

@@ -203,6 +203,15 @@ ffst_status ffst_plan_local_planes(const ffst_plan* plan, int* count, int* globa
 ffst_status ffst_plan_workspace_bytes(const ffst_plan* plan, size_t* bytes);
 ffst_status ffst_plan_info(const ffst_plan* plan, int* n, int* j0, int* eta, int* eta_local, int* batch);
 
+/* The schedule the plan's complex transforms run on:
+ * PERSISTENT   power-of-two n >= 128 (and n <= 64 with FFST_TINY=0, or user spectra): the two
+ *              persistent work-queue kernels per direction (Hermitian halving, pruning);
+ * FUSED_SMALL  power-of-two n <= 64: one CTA per (plane, image) in shared memory (the compact
+ *              format still uses the persistent kernels);
+ * ARBITRARY_N  any other n (or asymmetric user spectra): full complex transforms, Bluestein DFTs. */
+typedef enum { FFST_PATH_PERSISTENT = 0, FFST_PATH_FUSED_SMALL = 1, FFST_PATH_ARBITRARY_N = 2 } ffst_path;
+ffst_status ffst_plan_path(const ffst_plan* plan, int* path);
+
 /* ---- transforms (device buffers) ---------------------------------------- */
 
 /* Materialise the local spectra psi_hat_i (tests / diagnostics only; the

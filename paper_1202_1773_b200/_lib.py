@@ -64,6 +64,7 @@ _SIGS = {
     "ffst_plan_local_planes": (_i, [_vp, _p, _p]),
     "ffst_plan_workspace_bytes": (_i, [_vp, C.POINTER(_sz)]),
     "ffst_plan_info": (_i, [_vp, _p, _p, _p, _p, _p]),
+    "ffst_plan_path": (_i, [_vp, _p]),
     "ffst_shearlet_spectra": (_i, [_vp, _vp, _i, _vp]),
     "ffst_sheartrans": (_i, [_vp, _vp, _vp, _vp]),
     "ffst_sheartrans_batch": (_i, [_vp, _vp, _vp, _i, _vp]),

@@ -684,6 +684,10 @@ ffst_status validate_call(ffst_plan* p, const void* a, const void* b, int batch,
   if (!a || !b) return fail(FFST_ERR_INVALID_ARG, "null buffer");
   if (batch < 1 || batch > p->d.batch) return fail(FFST_ERR_INVALID_ARG, "batch outside 1..plan batch");
   if (!aligned16(a) || !aligned16(b)) return fail(FFST_ERR_ALIGNMENT, "buffers must be 16-byte aligned");
+  if (p->generic) {                 // the arbitrary-n path has no work queues
+    *q = nullptr;
+    return FFST_OK;
+  }
   return find_queue(p, batch, q);
 }
 
@@ -1648,6 +1652,12 @@ ffst_status ffst_plan_info(const ffst_plan* p, int* n, int* j0, int* eta, int* e
   if (eta) *eta = p->eta;
   if (eta_local) *eta_local = p->eta_l;
   if (batch) *batch = p->d.batch;
+  return FFST_OK;
+}
+
+ffst_status ffst_plan_path(const ffst_plan* p, int* path) {
+  if (!p || !path) return fail(FFST_ERR_INVALID_ARG, "null argument");
+  *path = p->generic ? FFST_PATH_ARBITRARY_N : p->tiny ? FFST_PATH_FUSED_SMALL : FFST_PATH_PERSISTENT;
   return FFST_OK;
 }
 

@@ -169,6 +169,9 @@ class Plan:
         cnt = C.c_int()
         check(lib.ffst_plan_local_planes(self._h, C.byref(cnt), idx), "ffst_plan_local_planes")
         self.local_planes = list(idx)
+        pth = C.c_int()
+        check(lib.ffst_plan_path(self._h, C.byref(pth)), "ffst_plan_path")
+        self.path = {0: "persistent", 1: "fused_small", 2: "arbitrary_n"}[pth.value]
         self.shard_rank, self.shard_count = int(shard_rank), int(shard_count)
         self._reserved = {self.batch}
 

@@ -256,8 +256,10 @@ def test_reserved_batches_do_not_allocate(F):
     assert float((out_r - x).abs().max() / x.abs().max()) <= 1e-4
 
 
-def test_host_variants(F):
-    n, batch = 64, 2
+@pytest.mark.parametrize("n", [64, 128, 45])
+def test_host_variants(F, n):
+    # the host-buffer entry points on the fused small-n, persistent and arbitrary-n paths
+    batch = 2
     x, xo = images(2, batch, n, torch.float32)
     plan = F.Plan(n, batch, torch.float32)
     c = plan.forward_host(x.pin_memory())
@@ -736,8 +738,9 @@ def test_non_default_scales(F, n, j0):
 def test_smaller_batches_all_paths(F):
     # a call with fewer images than the plan's batch (first use reserves its queue where the path
     # has one): the fused small-n path, the persistent kernels, the arbitrary-n path
-    for n in (32, 128, 45):
+    for n, path in ((32, "fused_small"), (128, "persistent"), (45, "arbitrary_n")):
         plan = F.Plan(n, 5, torch.float32)
+        assert plan.path == path
         x, xo = images(2, 5, n, torch.float32)
         c_all = plan.forward(x.cuda())
         c_two = plan.forward(x[1:3].cuda())
