@@ -37,6 +37,47 @@ __global__ void __launch_bounds__(NT, MINB) k_rows(const C* __restrict__ in, C* 
   }
 }
 
+// software-pipelined: the next line's 16 loads are issued before the current line's FFT
+template <int NT, int MINB, bool TWS, bool TWG = false>
+__global__ void __launch_bounds__(NT, MINB) k_rows_pf(const C* __restrict__ in, C* __restrict__ out, int rows, const C* tw) {
+  extern __shared__ __align__(16) unsigned char sm_raw[];
+  C* sm = reinterpret_cast<C*>(sm_raw);
+  constexpr int TH = 256, LPB = NT / TH;
+  const int line = threadIdx.x / TH, t = threadIdx.x % TH;
+  C* scr = sm + line * Pad<float>::len(N);
+  const C* twp = tw;
+  if constexpr (TWS) {
+    C* st = sm + LPB * Pad<float>::len(N);
+    for (int i = threadIdx.x; i < N; i += NT) st[i] = tw[i];
+    __syncthreads();
+    twp = st;
+  }
+  const int step = gridDim.x * LPB;
+  int r = blockIdx.x * LPB + line;
+  C nx[16];
+  {
+    const C* src = in + (size_t)(r < rows ? r : 0) * N;
+#pragma unroll
+    for (int q = 0; q < 16; ++q) nx[q] = __ldcs(src + t + q * TH);
+  }
+  for (int r0 = blockIdx.x * LPB; r0 < rows; r0 += step) {
+    C v[16];
+#pragma unroll
+    for (int q = 0; q < 16; ++q) v[q] = nx[q];
+    const int rn = r + step;
+    const C* srcn = in + (size_t)(rn < rows ? rn : 0) * N;
+#pragma unroll
+    for (int q = 0; q < 16; ++q) nx[q] = __ldcs(srcn + t + q * TH);
+    LineFFT<float, N, false, N, TWS || TWG>::run(v, scr, t, twp);
+    if (r < rows) {
+#pragma unroll
+      for (int q = 0; q < 16; ++q) __stcs(out + (size_t)r * N + t + q * TH, v[q]);
+    }
+    __syncthreads();
+    r = rn;
+  }
+}
+
 // loads only / stores only references
 __global__ void k_copy(const float4* __restrict__ in, float4* __restrict__ out, size_t n4) {
   for (size_t i = blockIdx.x * (size_t)blockDim.x + threadIdx.x; i < n4; i += (size_t)gridDim.x * blockDim.x)
@@ -76,5 +117,19 @@ int main(int argc, char** argv) {
   }
   RUN(256, 1, false) RUN(256, 2, false) RUN(256, 3, false) RUN(256, 4, false)
   RUN(256, 2, true) RUN(256, 3, true) RUN(512, 1, false) RUN(512, 2, false)
+#define RUNPF(NT, MINB, TWS)                                                                                 \
+  {                                                                                                          \
+    const size_t smem = (NT / 256) * Pad<float>::len(N) * sizeof(C) + (TWS ? N * sizeof(C) : 0);            \
+    cudaFuncSetAttribute(k_rows_pf<NT, MINB, TWS>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);  \
+    int nb = 0; cudaOccupancyMaxActiveBlocksPerMultiprocessor(&nb, k_rows_pf<NT, MINB, TWS>, NT, smem);       \
+    char name[96]; snprintf(name, sizeof name, "rows-pf NT=%d minB=%d tws=%d (%d CTA/SM)", NT, MINB, TWS, nb); \
+    timeit(name, [&] { k_rows_pf<NT, MINB, TWS><<<sms * nb, NT, smem>>>(in, out, rows, tw); });               \
+  }
+  RUNPF(256, 1, false) RUNPF(256, 2, false) RUNPF(256, 2, true) RUNPF(256, 3, false)
+  {
+    const size_t smem = Pad<float>::len(N) * sizeof(C);
+    cudaFuncSetAttribute(k_rows_pf<256, 2, false, true>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+    timeit("rows-pf twg (products, global table)", [&] { k_rows_pf<256, 2, false, true><<<sms * 2, 256, smem>>>(in, out, rows, tw); });
+  }
   return 0;
 }
