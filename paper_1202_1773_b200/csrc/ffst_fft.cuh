@@ -145,7 +145,7 @@ template <int TH> struct SyncOf {
 };
 
 // TWS: the twiddle table is in shared memory (plain loads) instead of global (read-only path).
-template <typename T, int L, bool INV, int TWN, bool TWS = false, int EM = 16>
+template <typename T, int L, bool INV, int TWN, bool TWS = false, int EM = 16, bool TW2 = false>
 struct LineFFT {
   using RP = RadixPlan<L, EM>;
   static constexpr int E = RP::E;
@@ -178,9 +178,15 @@ struct LineFFT {
         const int k = v & (NS - 1);
         if constexpr (TWS) {
           // one table read per butterfly, w^q by products (w^2q = (w^q)^2, w^(q+1) = w^q w):
-          // shared-memory bandwidth is the scarce resource on this path, the FMA pipe is not
+          // shared-memory bandwidth is the scarce resource on this path, the FMA pipe is not.
+          // TW2 (two-level table in shared memory, TWN/64 + 64 entries): w^m = hi[m / 64] lo[m % 64]
           cpx<T> wp[R];
-          wp[1] = tw[k * (TWN / (NS * R))];
+          if constexpr (TW2) {
+            const int m = k * (TWN / (NS * R));
+            wp[1] = cmul<T>(tw[m >> 6], tw[TWN / 64 + (m & 63)]);
+          } else {
+            wp[1] = tw[k * (TWN / (NS * R))];
+          }
 #pragma unroll
           for (int q = 2; q < R; ++q) wp[q] = (q & 1) ? cmul<T>(wp[q - 1], wp[1]) : cmul<T>(wp[q / 2], wp[q / 2]);
 #pragma unroll

@@ -208,6 +208,29 @@ struct K {
   static constexpr int H = N / 2;
   static constexpr int NT = G::NT;
 
+  // Line FFTs take their twiddles from a two-level table in shared memory for n >= 256:
+  // w^m = hi[m / 64] lo[m % 64] (n/64 + 64 entries), one table read pair per butterfly and the
+  // powers w^q by products (ffst_fft.cuh TW2).  Measured on the bare 4096-point block: 12.6 ->
+  // 10.9 ns per line (scripts/micro/fftbench.cu).  Every kernel that runs a K item fills it first.
+  static constexpr bool TW2 = N >= 256;
+  static __device__ __forceinline__ C* tw2tab() {
+    __shared__ C tab[TW2 ? N / 64 + 64 : 1];
+    return tab;
+  }
+  static __device__ __forceinline__ void tw2_fill(const KParams& p) {
+    if constexpr (TW2) {
+      const C* tw = static_cast<const C*>(p.tw);
+      C* tab = tw2tab();
+      for (int i = threadIdx.x; i < N / 64 + 64; i += blockDim.x) tab[i] = i < N / 64 ? tw[64 * i] : tw[i - N / 64];
+      __syncthreads();
+    }
+  }
+  template <int L, bool INV>
+  static __device__ __forceinline__ void fft(C (&r)[LineFFT<T, L, INV, N>::E], C* sm, int t, const C* tw) {
+    if constexpr (TW2) LineFFT<T, L, INV, N, true, 16, true>::run(r, sm, t, tw2tab());
+    else LineFFT<T, L, INV, N>::run(r, sm, t, tw);
+  }
+
   // Window sym_i of the CTA's column lines into wbuf[q * NT + tid] (thread tid's element q = row
   // t + q THC of column cb0 + tid / THC).  The support is ~10 % of the rows: the line's threads
   // enumerate only the candidate rows (integer intervals from col_bounds) and evaluate them
@@ -307,7 +330,7 @@ struct K {
         }
       }
       if (rd == 0) FFST_PROBE(p, 1);
-      if (!(p.dbg & 1)) LineFFT<T, N, true, N>::run(r, scr + line * G::SMC, t, tw);
+      if (!(p.dbg & 1)) fft<N, true>(r, scr + line * G::SMC, t, tw);
       if (rd == 0) FFST_PROBE(p, 2);
       if constexpr (G::DIRECT) {
         if (rd == 0 && dep != nullptr) {       // ring-slot reuse: wait only before writing dst
@@ -413,7 +436,7 @@ struct K {
         const T w = wbuf[q * NT + tid];
         r[q] = w != T(0) ? cscale<T>(__ldg(col + t + q * G::THC), w) : czero<T>();
       }
-      LineFFT<T, N, true, N>::run(r, scr + line * G::SMC, t, tw);
+      fft<N, true>(r, scr + line * G::SMC, t, tw);
       const int* dep = img == 0 ? dep0 : dep1;
       C* dst = img == 0 ? dst0 : dst1;
       if constexpr (G::DIRECT) {
@@ -488,7 +511,7 @@ struct K {
         z[q] = mk<T>(a.x - e.y, a.y + e.x);                 // a + i e
       }
       if (rd == 0) FFST_PROBE(p, 0);
-      if (!(p.dbg & 1)) LineFFT<T, H, true, N>::run(z, scr + line * G::SMR, t, tw);
+      if (!(p.dbg & 1)) fft<H, true>(z, scr + line * G::SMR, t, tw);
       if (rd == 0) FFST_PROBE(p, 1);
       if (act) {
         const T sr = (r & 1) ? T(-1) : T(1);
@@ -579,7 +602,7 @@ struct K {
             z[q] = act ? *reinterpret_cast<const cpx<T>*>(src_r + (size_t)(act ? r : r0) * N + 2 * (t + q * G::THR)) : czero<T>();
         }
         if (ti == 0 && rd == 0) FFST_PROBE(p, 0);
-        LineFFT<T, H, false, N>::run(z, scr + line * G::SMR, t, tw);
+        fft<H, false>(z, scr + line * G::SMR, t, tw);
         if (ti == 0 && rd == 0) FFST_PROBE(p, 1);
         if (nyq) {
           // alternating row sum t(r) = sum_m1 (-1)^m1 Im c(r, m1), reduced over the line
@@ -693,7 +716,7 @@ struct K {
         z[q] = up ? mk<T>(a.x + b.y, b.x - a.y) : mk<T>(a.x - b.y, a.y + b.x);
       }
       if (rd == 0) FFST_PROBE(p, 0);
-      LineFFT<T, N, true, N>::run(z, scr + line * G::SMC, t, tw);
+      fft<N, true>(z, scr + line * G::SMC, t, tw);
       if (rd == 0) FFST_PROBE(p, 1);
       if (act) {
         C* oa = out_c + (size_t)ra * N;
@@ -796,7 +819,7 @@ struct K {
         }
         if (ti == 0 && rd == 0) FFST_PROBE(p, 0);
         C* sl = scr + line * G::SMC;
-        if (!(p.dbg & 1)) LineFFT<T, N, false, N>::run(z, sl, t, tw);
+        if (!(p.dbg & 1)) fft<N, false>(z, sl, t, tw);
         if (ti == 0 && rd == 0) FFST_PROBE(p, 1);
         if (nyq) {   // alternating row sums t(r) = sum_m1 (-1)^m1 Im c(r, m1) over the line's lanes
 #pragma unroll
@@ -922,7 +945,7 @@ struct K {
 #pragma unroll
       for (int q = 0; q < G::EC; ++q) z[q] = mk<T>(ca[q], cb[q]);
       C* sl = scr + line * G::SMC;
-      if (!(p.dbg & 1)) LineFFT<T, N, false, N>::run(z, sl, t, tw);
+      if (!(p.dbg & 1)) fft<N, false>(z, sl, t, tw);
       SyncOf<G::THC>::sync();
 #pragma unroll
       for (int q = 0; q < G::EC; ++q) sl[Pad<T>::at(t + q * G::THC)] = z[q];
@@ -1001,7 +1024,7 @@ struct K {
           for (int q = 0; q < G::EC; ++q) r[q] = in ? __ldcg(col + t + q * G::THC) : czero<T>();
         }
         window_lines(P, g0, in, wbuf, scr, R, delta, user_plane<T, N>(p, P), p.dbg & 4);
-        if (!(p.dbg & 1)) LineFFT<T, N, false, N>::run(r, scr + line * G::SMC, t, tw);
+        if (!(p.dbg & 1)) fft<N, false>(r, scr + line * G::SMC, t, tw);
         if (in) {
 #pragma unroll
           for (int q = 0; q < G::EC; ++q) {
@@ -1036,7 +1059,7 @@ struct K {
     C r[G::EC];
 #pragma unroll
     for (int q = 0; q < G::EC; ++q) r[q] = act ? col[t + q * G::THC] : czero<T>();
-    LineFFT<T, N, false, N>::run(r, scr + line * G::SMC, t, tw);
+    fft<N, false>(r, scr + line * G::SMC, t, tw);
     if (act) {
       C* f = static_cast<C*>(p.F) + ((size_t)b * (H + 1) + cb) * N;
 #pragma unroll
@@ -1156,6 +1179,7 @@ __device__ __forceinline__ void persistent_loop(const KParams& p) {
   cpx<T>* smem = reinterpret_cast<cpx<T>*>(smem_raw);
   __shared__ int s_item[2];
   __shared__ PlaneDev s_planes[MAX_PLANES_SMEM];
+  K<T, N>::tw2_fill(p);
   for (int i = threadIdx.x; i < p.eta_l; i += blockDim.x) s_planes[i] = p.planes[i];
   if (threadIdx.x == 0) {
     s_item[0] = atomicAdd(p.ctr, 1);
@@ -1214,6 +1238,7 @@ __global__ void __launch_bounds__(256, 2) inv_main_kernel(KParams p) {
 template <typename T, int N>
 __global__ void __launch_bounds__(256) spec_rows_kernel(KParams p) {
   extern __shared__ __align__(128) unsigned char smem_raw[];
+  K<T, N>::tw2_fill(p);
   using G = Geo<T, N>;
   const int b = blockIdx.y, g = blockIdx.x;
   const int r0 = g * G::RPI;
@@ -1228,6 +1253,7 @@ __global__ void __launch_bounds__(256) spec_rows_kernel(KParams p) {
 template <typename T, int N>
 __global__ void __launch_bounds__(256) spec_cols_kernel(KParams p) {
   extern __shared__ __align__(128) unsigned char smem_raw[];
+  K<T, N>::tw2_fill(p);
   K<T, N>::col_fft_plain(p, blockIdx.y, blockIdx.x, reinterpret_cast<cpx<T>*>(smem_raw));
 }
 
@@ -1235,6 +1261,7 @@ __global__ void __launch_bounds__(256) spec_cols_kernel(KParams p) {
 template <typename T, int N>
 __global__ void __launch_bounds__(256) fin_cols_kernel(KParams p, int cpb) {
   extern __shared__ __align__(128) unsigned char smem_raw[];
+  K<T, N>::tw2_fill(p);
   using G = Geo<T, N>;
   const int b = blockIdx.y;
   const int c0 = blockIdx.x * cpb;              // cpb <= GC columns per CTA (fewer for small problems)
@@ -1251,6 +1278,7 @@ __global__ void __launch_bounds__(256) fin_cols_kernel(KParams p, int cpb) {
 template <typename T, int N>
 __global__ void __launch_bounds__(256) fin_rows_kernel(KParams p) {
   extern __shared__ __align__(128) unsigned char smem_raw[];
+  K<T, N>::tw2_fill(p);
   using G = Geo<T, N>;
   const int b = blockIdx.y;
   const int r0 = blockIdx.x * G::RPF;

@@ -38,7 +38,7 @@ __global__ void __launch_bounds__(NT, MINB) k_rows(const C* __restrict__ in, C* 
 }
 
 // software-pipelined: the next line's 16 loads are issued before the current line's FFT
-template <int NT, int MINB, bool TWS, bool TWG = false>
+template <int NT, int MINB, bool TWS, bool TWG = false, bool TW2 = false>
 __global__ void __launch_bounds__(NT, MINB) k_rows_pf(const C* __restrict__ in, C* __restrict__ out, int rows, const C* tw) {
   extern __shared__ __align__(16) unsigned char sm_raw[];
   C* sm = reinterpret_cast<C*>(sm_raw);
@@ -49,6 +49,13 @@ __global__ void __launch_bounds__(NT, MINB) k_rows_pf(const C* __restrict__ in, 
   if constexpr (TWS) {
     C* st = sm + LPB * Pad<float>::len(N);
     for (int i = threadIdx.x; i < N; i += NT) st[i] = tw[i];
+    __syncthreads();
+    twp = st;
+  }
+  if constexpr (TW2) {                     // hi[m] = w^(64 m), lo[m] = w^m
+    C* st = sm + LPB * Pad<float>::len(N);
+    for (int i = threadIdx.x; i < N / 64; i += NT) st[i] = tw[64 * i];
+    for (int i = threadIdx.x; i < 64; i += NT) st[N / 64 + i] = tw[i];
     __syncthreads();
     twp = st;
   }
@@ -68,7 +75,7 @@ __global__ void __launch_bounds__(NT, MINB) k_rows_pf(const C* __restrict__ in, 
     const C* srcn = in + (size_t)(rn < rows ? rn : 0) * N;
 #pragma unroll
     for (int q = 0; q < 16; ++q) nx[q] = __ldcs(srcn + t + q * TH);
-    LineFFT<float, N, false, N, TWS || TWG>::run(v, scr, t, twp);
+    LineFFT<float, N, false, N, TWS || TWG || TW2, 16, TW2>::run(v, scr, t, twp);
     if (r < rows) {
 #pragma unroll
       for (int q = 0; q < 16; ++q) __stcs(out + (size_t)r * N + t + q * TH, v[q]);
@@ -130,6 +137,12 @@ int main(int argc, char** argv) {
     const size_t smem = Pad<float>::len(N) * sizeof(C);
     cudaFuncSetAttribute(k_rows_pf<256, 2, false, true>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
     timeit("rows-pf twg (products, global table)", [&] { k_rows_pf<256, 2, false, true><<<sms * 2, 256, smem>>>(in, out, rows, tw); });
+  }
+  {
+    const size_t smem = Pad<float>::len(N) * sizeof(C) + (N / 64 + 64) * sizeof(C);
+    cudaFuncSetAttribute(k_rows_pf<256, 2, false, false, true>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+    timeit("rows-pf tw2 (two-level shared table)", [&] { k_rows_pf<256, 2, false, false, true><<<sms * 2, 256, smem>>>(in, out, rows, tw); });
+    cudaFuncSetAttribute(k_rows<256, 2, false>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
   }
   return 0;
 }
