@@ -629,6 +629,8 @@ KParams base_params(ffst_plan* p) {
   k.rpi = p->rpi;
   k.a_lane_elems = (long long)p->d.batch * (p->n / 2 + 1) * p->n;
   if (const char* d = std::getenv("FFST_DBG")) k.dbg = std::atoi(d);
+  k.ring_stream = (long long)p->W_elems * 2 * (long long)p->rsz > (96LL << 20) ? 1 : 0;
+  if (const char* rs = std::getenv("FFST_RING_STREAM")) k.ring_stream = std::atoi(rs) != 0;   // tuning only
   k.sync_mode = 3;
   if (const char* sm = std::getenv("FFST_SYNC")) k.sync_mode = std::atoi(sm) & 3;   // measurement only
   return k;

@@ -80,6 +80,7 @@ struct KParams {
   const void* usym;             // user spectra: [eta_l][n/2+1][n] T symmetric parts (ffst_user.cuh), else nullptr
   int compact;                  // f1 compact format: cube of reals + Nyquist vectors (G, H) in nyq_fwd
   int dbg;                      // measurement only (FFST_DBG): bit 0 skip FFTs, bit 1 skip output stores
+  int ring_stream;              // the intermediate ring is larger than L2: stream it (evict_first)
   int sync_mode;                // dependency ordering: bit 0 acquire fence after waits, bit 1 release on WAR-only signals
   unsigned long long* trace;    // optional: per item {smid, t_start, t_ready, t_end} (globaltimer ns)
 };

@@ -90,8 +90,8 @@ template <> __device__ __forceinline__ void store_pair_cs<double>(double2* dst, 
   __stcs(dst + 1, b);
 }
 // L2 residency hints (createpolicy): the adjoint's accumulator A is read-modify-written by every
-// plane and is kept (evict_last); at n >= 2048 the intermediate ring (12+ slots of 27-52 MB) cannot
-// stay in L2 and is streamed (evict_first) so that it does not push A out.
+// plane and is kept (evict_last); an intermediate ring that cannot stay in L2 (KParams.ring_stream:
+// n >= 2048, 12+ slots of 27-52 MB) is streamed (evict_first) so that it does not push A out.
 __device__ __forceinline__ unsigned long long policy_evict_last() {
   unsigned long long p;
   asm volatile("createpolicy.fractional.L2::evict_last.L2::evict_unchanged.b64 %0, 1.0;" : "=l"(p));
@@ -870,7 +870,7 @@ struct K {
       for (int e = tid; e < (p.dbg & 2 ? 0 : ncols * G::GR); e += NT) {
         const int kk = e / G::GR, ri = e - kk * G::GR;
         if (ri < rows_here) {
-          if constexpr (N >= 2048) st_hint<T>(dst + (size_t)kk * N + rt0 + ri, tile[ri * G::TSTR + kk], pf);
+          if (p.ring_stream) st_hint<T>(dst + (size_t)kk * N + rt0 + ri, tile[ri * G::TSTR + kk], pf);
           else dst[(size_t)kk * N + rt0 + ri] = tile[ri * G::TSTR + kk];
         }
       }
@@ -970,7 +970,7 @@ struct K {
         for (int e = tid; e < (p.dbg & 2 ? 0 : ncols * G::GR); e += NT) {
           const int kk = e / G::GR, r = e - kk * G::GR;
           if (r < rows_here) {
-            if constexpr (N >= 2048) st_hint<T>(dst + (size_t)kk * N + rt0 + r, tile[r * G::TSTR + kk], pf);
+            if (p.ring_stream) st_hint<T>(dst + (size_t)kk * N + rt0 + r, tile[r * G::TSTR + kk], pf);
             else dst[(size_t)kk * N + rt0 + r] = tile[r * G::TSTR + kk];
           }
         }
@@ -1015,7 +1015,7 @@ struct K {
         const bool in = act && cb >= P.c_lo && cb < P.c_lo + P.ncols;
         const C* col = slot + cur + (size_t)(in ? cb - P.c_lo : 0) * N;
         C r[G::EC];
-        if constexpr (N >= 2048) {
+        if (p.ring_stream) {
           const unsigned long long pf = policy_evict_first();
 #pragma unroll
           for (int q = 0; q < G::EC; ++q) r[q] = in ? ld_hint<T>(col + t + q * G::THC, pf) : czero<T>();
