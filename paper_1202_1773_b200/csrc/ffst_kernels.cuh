@@ -225,6 +225,15 @@ struct K {
       __syncthreads();
     }
   }
+  // w^k = exp(-2 pi i k / N): from the shared two-level table (n >= 256), else the global table
+  static __device__ __forceinline__ C twk(int kk, const C* tw) {
+    if constexpr (TW2) {
+      const C* tab = tw2tab();
+      return cmul<T>(tab[kk >> 6], tab[N / 64 + (kk & 63)]);
+    } else {
+      return __ldg(tw + kk);
+    }
+  }
   template <int L, bool INV>
   static __device__ __forceinline__ void fft(C (&r)[LineFFT<T, L, INV, N>::E], C* sm, int t, const C* tw) {
     if constexpr (TW2) LineFFT<T, L, INV, N, true, 16, true>::run(r, sm, t, tw2tab());
@@ -507,7 +516,7 @@ struct K {
         const C xk = z[q], xm = zm[q];
         const C a = mk<T>(xk.x + xm.x, xk.y - xm.y);      // xk + conj(xm)
         const C d = mk<T>(xk.x - xm.x, xk.y + xm.y);      // xk - conj(xm)
-        const C e = cmulc<T>(d, __ldg(tw + k));            // d * exp(+2 pi i k / N)
+        const C e = cmulc<T>(d, twk(k, tw));                // d * exp(+2 pi i k / N)
         z[q] = mk<T>(a.x - e.y, a.y + e.x);                 // a + i e
       }
       if (rd == 0) FFST_PROBE(p, 0);
