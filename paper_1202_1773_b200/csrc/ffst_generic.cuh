@@ -51,14 +51,27 @@ __device__ __forceinline__ T gen_window(const GenParams& g, const PlaneDev& P, i
 // INVDFT: sign +.  Unnormalised.
 template <typename T, int M>
 struct Bluestein {
-  using LF = LineFFT<T, M, false, M>;
-  using LI = LineFFT<T, M, true, M>;
+  // M >= 256: twiddles from a two-level shared table (as the power-of-two kernels, ffst_kernels.cuh)
+  static constexpr bool TW2 = M >= 256;
+  using LF = LineFFT<T, M, false, M, TW2, 16, TW2>;
+  using LI = LineFFT<T, M, true, M, TW2, 16, TW2>;
   static constexpr int E = LF::E, TH = M / E;
+  static __device__ __forceinline__ cpx<T>* tw2tab() {
+    __shared__ cpx<T> tab[TW2 ? M / 64 + 64 : 1];
+    return tab;
+  }
+  static __device__ __forceinline__ void tw2_fill(const GenParams& g) {
+    if constexpr (TW2) {
+      const cpx<T>* tw = static_cast<const cpx<T>*>(g.twm);
+      for (int i = threadIdx.x; i < M / 64 + 64; i += blockDim.x) tw2tab()[i] = i < M / 64 ? tw[64 * i] : tw[i - M / 64];
+      __syncthreads();
+    }
+  }
   template <bool INVDFT>
   static __device__ __forceinline__ void run(cpx<T> (&r)[E], int L, cpx<T>* scr, int t, const GenParams& g) {
     const cpx<T>* ch = static_cast<const cpx<T>*>(g.chirp);
     const cpx<T>* bh = static_cast<const cpx<T>*>(g.bhat);
-    const cpx<T>* tw = static_cast<const cpx<T>*>(g.twm);
+    const cpx<T>* tw = TW2 ? tw2tab() : static_cast<const cpx<T>*>(g.twm);
 #pragma unroll
     for (int q = 0; q < E; ++q) {
       const int m = t + q * TH;
@@ -109,6 +122,7 @@ __global__ void __launch_bounds__(256) gen_rows_kernel(GenParams g, const void* 
   const int rr = act ? row : 0;
   C* scr = reinterpret_cast<C*>(smem_raw) + line * Pad<T>::len(M);
   const size_t nn = (size_t)n * n;
+  B::tw2_fill(g);
   C r[E];
   if constexpr (MODE == GEN_INV_COL) {
     const int b = blockIdx.y;
