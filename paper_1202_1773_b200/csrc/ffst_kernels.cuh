@@ -44,14 +44,28 @@ struct Geo {
   // 12 % warps active at n = 4096); forward pass 1 then stores each column straight from
   // registers (8-byte stores whose sectors the item's GC columns complete in L2)
   static constexpr bool DIRECT = (long long)N * GCP * ESZ > 65536;
-  // (DIRECT: the tile region holds one column, so that stores go out as 16-byte column pairs)
-  static constexpr int TILE_CE = DIRECT ? N * (LPC > 1 ? LPC / 2 : 1) : TILE_C;     // tile elements allocated
+  // DIRECT sizes: the forward intermediate W (and the final pass's Fscr) is column-major
+  // ([column][N rows], like the inverse's): pass 1 stores each column line coalesced straight from
+  // registers, and the row pass reads tiles of TRF rows (32-byte column segments at float32)
+  // through shared memory.  (A row-major W needs one L2 write request per element here.)
+  // Within W the rows come in blocks of TB: element (row r, column c) at ((r / TB) stride + c) TB + r % TB
+  // (stride = the padded column count), so that a row item's TRF-row tiles read one contiguous
+  // block (DRAM locality: plain column-major would read 32-byte segments 32 KB apart at n = 4096).
+  static constexpr bool WCOL = DIRECT;
+  static constexpr int TILE_CE = DIRECT ? 0 : TILE_C;     // tile elements allocated (pass 1)
   // forward pass 2 / final rows: rows per item (~128 KB of output)
   // (n >= 2048: at least 16 rows -- per-item overhead and the Nyquist-term staging amortised)
   static constexpr int RP2_A = (131072 / (N * ESZ)) > LPR ? (131072 / (N * ESZ)) : LPR;
   static constexpr int RP2_ = (N >= 2048 && RP2_A < 16) ? 16 : RP2_A;
   static constexpr int RP2 = RP2_ < N ? RP2_ : N;
-  static constexpr int RPF = LPR < N ? LPR : N;     // final row pass: one round per CTA (more CTAs)
+  // column-major row pass (WCOL): rows per shared tile
+  static constexpr int TRF_ = LPR > 4 ? LPR : 4;
+  static constexpr int TRF = TRF_ < N ? TRF_ : N;
+  static constexpr int RPT = TRF / LPR > 0 ? TRF / LPR : 1;     // rounds per tile
+  static constexpr int TB = TRF;                                  // row block of the WCOL layout
+  static FFST_HD size_t wat(int r, int c, int stride) { return ((size_t)(r / TB) * stride + c) * TB + r % TB; }
+  static constexpr int RPF_ = WCOL ? TRF : LPR;      // final row pass: one tile / round per CTA (more CTAs)
+  static constexpr int RPF = RPF_ < N ? RPF_ : N;
   // inverse pass 1: rows per tile and per item
   static constexpr int GR_ = LPR > (32 / ESZ) ? LPR : (32 / ESZ);
   static constexpr int GR = GR_ < N ? GR_ : N;
@@ -68,12 +82,14 @@ struct Geo {
   // per-thread window values (EC reals per thread), staged in shared memory so the window
   // arithmetic is not unrolled into the FFT's register footprint
   static constexpr int WBUF = NT * EC * (int)sizeof(T) / ESZ;      // in complex elements
-  static constexpr int NYQB = (N + RP2) * (int)sizeof(T) / ESZ + 1;   // staged Nyquist terms (complex units)
+  // staged Nyquist terms (complex units); WCOL: the row tile instead (the terms are read through L1)
+  static constexpr int NYQB = WCOL ? TRF * TSTR : (N + RP2) * (int)sizeof(T) / ESZ + 1;
   static constexpr size_t SMEM_FWD = (size_t)((SCR_C + TILE_CE + WBUF) > (SCRX + NYQB) ? (SCR_C + TILE_CE + WBUF) : (SCRX + NYQB)) * ESZ;
   static constexpr size_t SMEM_INV = (size_t)((SCRX + TILE_R) > (SCR_C + WBUF) ? (SCRX + TILE_R) : (SCR_C + WBUF)) * ESZ + 256;
   static constexpr size_t SMEM_AUX = SMEM_FWD > SMEM_INV ? SMEM_FWD : SMEM_INV;
   static constexpr size_t SMEM_NYQ = (size_t)(SCR_C + NT * EC) * ESZ;
   static_assert(RPI % GR == 0, "RPI must be a multiple of GR");
+  static_assert(!WCOL || (RP2 % TRF == 0 && (TRF % LPR == 0 || TRF == N) && N % TRF == 0), "row tiles must tile the row items");
   static_assert(!PAIR || (GR % (2 * LPC) == 0 || GR < 2 * LPC), "row-pair rounds must tile GR");
   static_assert(SCR_C * ESZ >= LPC * N * (int)sizeof(T), "row-pair column-sum scratch");
   static_assert(GC % LPC == 0 || LPC > GC, "GC vs LPC");
@@ -149,6 +165,21 @@ template <> __device__ __forceinline__ void load_pair_cs<double>(const double2* 
   a = __ldcs(src);
   b = __ldcs(src + 1);
 }
+
+// Asynchronous global -> shared copies (LDGSTS): no registers held while in flight.
+template <typename T> __device__ __forceinline__ void cp_async_el(cpx<T>* dst_smem, const cpx<T>* src, unsigned long long pol,
+                                                                 bool hint) {
+  const unsigned d = (unsigned)__cvta_generic_to_shared(dst_smem);
+  if (sizeof(cpx<T>) == 8) {
+    if (hint) asm volatile("cp.async.ca.shared.global.L2::cache_hint [%0], [%1], 8, %2;" ::"r"(d), "l"(src), "l"(pol) : "memory");
+    else asm volatile("cp.async.ca.shared.global [%0], [%1], 8;" ::"r"(d), "l"(src) : "memory");
+  } else {
+    if (hint) asm volatile("cp.async.cg.shared.global.L2::cache_hint [%0], [%1], 16, %2;" ::"r"(d), "l"(src), "l"(pol) : "memory");
+    else asm volatile("cp.async.cg.shared.global [%0], [%1], 16;" ::"r"(d), "l"(src) : "memory");
+  }
+}
+__device__ __forceinline__ void cp_async_commit() { asm volatile("cp.async.commit_group;" ::: "memory"); }
+__device__ __forceinline__ void cp_async_wait_all() { asm volatile("cp.async.wait_all;" ::: "memory"); }
 
 __device__ __forceinline__ unsigned long long gtimer() {
   unsigned long long t;
@@ -298,8 +329,10 @@ struct K {
 
   // ------------------------------------------------------------------ column IFFT item
   // MAIN: forward pass 1 — column bins [c0, c0+cnt) of plane P: X(u) = sym_P(u) F(u),
-  //       IFFT along u2, rows -> W (row-major, stride P.ncols_pad, column c - P.c_lo).
-  // AUX:  final pass 1 — column bins of A[b] (no window) -> Fscr[b] (row-major, stride NCPF).
+  //       IFFT along u2, rows -> W (row-major, stride P.ncols_pad, column c - P.c_lo; WCOL:
+  //       column-major in row blocks, Geo::wat).
+  // AUX:  final pass 1 — column bins of A[b] (no window) -> Fscr[b] (row-major, stride NCPF;
+  //       WCOL: column-major).
   template <int MODE>
   static __device__ void col_ifft(const KParams& p, int b, const PlaneDev& P, int c0, int cnt,
                                   const C* __restrict__ src, C* dst, int dst_stride, int dst_col0,
@@ -341,58 +374,21 @@ struct K {
       if (rd == 0) FFST_PROBE(p, 1);
       if (!(p.dbg & 1)) fft<N, true>(r, scr + line * G::SMC, t, tw);
       if (rd == 0) FFST_PROBE(p, 2);
-      if constexpr (G::DIRECT) {
+      if constexpr (G::WCOL) {
         if (rd == 0 && dep != nullptr) {       // ring-slot reuse: wait only before writing dst
           if (tid == 0) spin_wait(dep, dep_target);
           __syncthreads();
         }
-        // Columns go out in pairs as 16-byte stores (half the L2 write requests of 8-byte column
-        // stores, and half sectors instead of quarter sectors): the even column of a pair waits in
-        // shared memory (`tile`, one column) for the odd one.  LPC = 1: consecutive rounds, the
-        // same thread holds the same rows in both (no barrier); LPC = 2: the two lines of a round.
-        constexpr bool ROUNDPAIR = G::LPC == 1;
-        const int cpair = ROUNDPAIR ? ci - (rd & 1) : ci - line;      // even column of the pair
-        const bool aligned = ((dst_col0 + cpair) & 1) == 0;
-        const bool has_odd = cpair + 1 < cnt;
-        const bool skip = p.dbg & 2;
-        if constexpr (ROUNDPAIR) {
-          if (!(rd & 1) && has_odd && aligned) {                     // even column: park it
-            if (act) {
+        // column-major destination: the line's elements t + q THC are contiguous (coalesced stores)
+        if (act && !(p.dbg & 2)) {
+          const int c = dst_col0 + ci;
+          if (MODE == MODE_MAIN && p.ring_stream) {
+            const unsigned long long pf = policy_evict_first();
 #pragma unroll
-              for (int q = 0; q < G::EC; ++q) tile[t + q * G::THC] = r[q];
-            }
-          } else if ((rd & 1) && aligned) {                          // odd column: store the pair
-            if (act && !skip) {
+            for (int q = 0; q < G::EC; ++q) st_hint<T>(dst + G::wat(t + q * G::THC, c, dst_stride), r[q], pf);
+          } else {
 #pragma unroll
-              for (int q = 0; q < G::EC; ++q)
-                store_pair_cg<T>(dst + (size_t)(t + q * G::THC) * dst_stride + dst_col0 + cpair, tile[t + q * G::THC], r[q]);
-            }
-          } else if (act && !skip) {                                  // single column
-#pragma unroll
-            for (int q = 0; q < G::EC; ++q) dst[(size_t)(t + q * G::THC) * dst_stride + dst_col0 + ci] = r[q];
-          }
-        } else {                                                     // LPC even: lines 2m, 2m+1
-          static_assert(G::LPC % 2 == 0, "column pairs of a round");
-          C* park = tile + (line >> 1) * N;
-          const bool odd = line & 1;
-          if (odd && act && aligned) {
-#pragma unroll
-            for (int q = 0; q < G::EC; ++q) park[t + q * G::THC] = r[q];
-          }
-          __syncthreads();
-          if (!odd && act && !skip) {
-            if (has_odd && aligned) {
-#pragma unroll
-              for (int q = 0; q < G::EC; ++q)
-                store_pair_cg<T>(dst + (size_t)(t + q * G::THC) * dst_stride + dst_col0 + ci, r[q], park[t + q * G::THC]);
-            } else {
-#pragma unroll
-              for (int q = 0; q < G::EC; ++q) dst[(size_t)(t + q * G::THC) * dst_stride + dst_col0 + ci] = r[q];
-            }
-          }
-          if (odd && act && !aligned && !skip) {
-#pragma unroll
-            for (int q = 0; q < G::EC; ++q) dst[(size_t)(t + q * G::THC) * dst_stride + dst_col0 + ci] = r[q];
+            for (int q = 0; q < G::EC; ++q) __stcg(dst + G::wat(t + q * G::THC, c, dst_stride), r[q]);
           }
         }
       } else if (ci < G::GC) {
@@ -401,7 +397,7 @@ struct K {
       }
       __syncthreads();
     }
-    if constexpr (!G::DIRECT) {
+    if constexpr (!G::WCOL) {
       if (dep != nullptr) {                    // ring-slot reuse: wait only before writing dst
         if (tid == 0) spin_wait(dep, dep_target);
         __syncthreads();
@@ -448,12 +444,12 @@ struct K {
       fft<N, true>(r, scr + line * G::SMC, t, tw);
       const int* dep = img == 0 ? dep0 : dep1;
       C* dst = img == 0 ? dst0 : dst1;
-      if constexpr (G::DIRECT) {
+      if constexpr (G::WCOL) {
         if (tid == 0 && dep != nullptr) spin_wait(dep, img == 0 ? tgt0 : tgt1);   // ring-slot reuse
         __syncthreads();
-        if (act) {
+        if (act) {                              // column-major destination (coalesced)
 #pragma unroll
-          for (int q = 0; q < G::EC; ++q) dst[(size_t)(t + q * G::THC) * dst_stride + dst_col0 + ci] = r[q];
+          for (int q = 0; q < G::EC; ++q) __stcg(dst + G::wat(t + q * G::THC, dst_col0 + ci, dst_stride), r[q]);
         }
       } else {
         if (ci < G::GC) {
@@ -474,8 +470,9 @@ struct K {
 
   // ------------------------------------------------------------------ row C2R item
   // Rows [r0, r0+cnt) of an intermediate holding Hermitian-half bins [c_lo, c_lo+ncols)
-  // (row-major, stride `stride`).  MAIN: complex coefficient rows (+ Nyquist imaginary
-  // term); AUX: real image rows minus the adjoint's Nyquist correction.
+  // (row-major, stride `stride`; WCOL: column-major in row blocks of TB, Geo::wat, read in tiles of
+  // TRF rows through shared memory).  MAIN: complex coefficient rows (+ Nyquist imaginary term);
+  // AUX: real image rows minus the adjoint's Nyquist correction.
   template <int MODE>
   static __device__ void row_c2r(const KParams& p, const C* __restrict__ src, int stride, int c_lo, int ncols,
                                  int r0, int cnt, C* out_c, T* out_r, const T* nyqG, const T* nyqH,
@@ -484,30 +481,66 @@ struct K {
     const int tid = threadIdx.x, line = tid / G::THR, t = tid % G::THR;
     const C* tw = static_cast<const C*>(p.tw);
     const T scale = T(1) / (T(N) * T(N));
-    constexpr int ROUNDS = G::RP2 / G::LPR > 0 ? G::RP2 / G::LPR : 1;
+    constexpr int ROUNDS_ = (G::WCOL && G::RPF > G::RP2 ? G::RPF : G::RP2) / G::LPR;
+    constexpr int ROUNDS = ROUNDS_ > 0 ? ROUNDS_ : 1;
     const int rounds = (cnt + G::LPR - 1) / G::LPR < ROUNDS ? (cnt + G::LPR - 1) / G::LPR : ROUNDS;
-    // Nyquist terms of this item staged in shared memory: G(m1) for all m1, H(r) for its rows
+    // Nyquist terms of this item: staged in shared memory (G(m1) for all m1, H(r) for its rows),
+    // or, WCOL (the region holds the row tile), read through L1
     T* sG = reinterpret_cast<T*>(smem + G::SCRX);
     T* sH = sG + N;
-    if (nyqG != nullptr) {
+    C* tile = smem + G::SCRX;                  // WCOL: [TRF][TSTR]
+    if (!G::WCOL && nyqG != nullptr) {
       for (int m = tid; m < N; m += NT) sG[m] = nyqG[m];
       for (int i = tid; i < cnt; i += NT) sH[i] = nyqH[r0 + i];
       __syncthreads();
     }
+    constexpr int RPT = G::RPT;                // WCOL: rounds per tile
+    const bool stream = MODE == MODE_MAIN && p.ring_stream;
+    const unsigned long long pf = policy_evict_first();
+    // WCOL: the TRF rows from tr0 on (column segments of one row block) -> tile rows, asynchronously
+    auto issue_tile = [&](int tr0) {
+      const int rows_here = cnt - tr0 < G::TRF ? cnt - tr0 : G::TRF;
+#pragma unroll 4
+      for (int e = tid; e < ncols * G::TRF; e += NT) {
+        const int kk = e / G::TRF, rr = e - kk * G::TRF;
+        if (rr < rows_here) cp_async_el<T>(tile + rr * G::TSTR + kk, src + G::wat(r0 + tr0 + rr, kk, stride), pf, stream);
+      }
+      cp_async_commit();
+    };
+    if constexpr (G::WCOL) issue_tile(0);
 #pragma unroll 1
     for (int rd = 0; rd < rounds; ++rd) {
       const int ri = rd * G::LPR + line;
       const bool act = ri < cnt;
       const int r = r0 + (act ? ri : 0);
-      const C* row = src + (size_t)r * stride - c_lo;
       C z[G::ER], zm[G::ER];
-      // phase 1: issue every load of the round (no use in between: all in flight together)
+      if constexpr (G::WCOL) {
+        if (rd % RPT == 0) {                   // this round's tile has landed
+          cp_async_wait_all();
+          __syncthreads();
+        }
+        const C* trow = tile + ((rd % RPT) * G::LPR + line) * G::TSTR - c_lo;
 #pragma unroll
-      for (int q = 0; q < G::ER; ++q) {
-        const int k = t + q * G::THR, km = H - k;
-        const bool ik = act && k >= c_lo && k < c_lo + ncols, ikm = act && km >= c_lo && km < c_lo + ncols;
-        z[q] = ik ? __ldcg(row + (ik ? k : c_lo)) : czero<T>();
-        zm[q] = ikm ? __ldcg(row + (ikm ? km : c_lo)) : czero<T>();
+        for (int q = 0; q < G::ER; ++q) {
+          const int k = t + q * G::THR, km = H - k;
+          const bool ik = act && k >= c_lo && k < c_lo + ncols, ikm = act && km >= c_lo && km < c_lo + ncols;
+          z[q] = ik ? trow[k] : czero<T>();
+          zm[q] = ikm ? trow[km] : czero<T>();
+        }
+        if (rd % RPT == RPT - 1 && rd + 1 < rounds) {   // every read of this tile done: the next one
+          __syncthreads();                              // streams in behind this round's FFT
+          issue_tile((rd + 1) * G::LPR);
+        }
+      } else {
+        const C* row = src + (size_t)r * stride - c_lo;
+        // phase 1: issue every load of the round (no use in between: all in flight together)
+#pragma unroll
+        for (int q = 0; q < G::ER; ++q) {
+          const int k = t + q * G::THR, km = H - k;
+          const bool ik = act && k >= c_lo && k < c_lo + ncols, ikm = act && km >= c_lo && km < c_lo + ncols;
+          z[q] = ik ? __ldcg(row + (ik ? k : c_lo)) : czero<T>();
+          zm[q] = ikm ? __ldcg(row + (ikm ? km : c_lo)) : czero<T>();
+        }
       }
       // phase 2: Hermitian pre-processing of the half-length C2R
 #pragma unroll
@@ -524,27 +557,32 @@ struct K {
       if (rd == 0) FFST_PROBE(p, 1);
       if (act) {
         const T sr = (r & 1) ? T(-1) : T(1);
+        // (cached loads may be hoisted above their guard: valid addresses without Nyquist terms too)
+        const T* gsafe = nyqG != nullptr ? nyqG : reinterpret_cast<const T*>(tw);
+        const T* hsafe = nyqG != nullptr ? nyqH : reinterpret_cast<const T*>(tw);
+        T hr = T(0);
+        if (nyqG != nullptr) hr = G::WCOL ? __ldg(hsafe + r) : sH[ri];
 #pragma unroll
         for (int q = 0; q < G::ER; ++q) {
           const int m1 = 2 * (t + q * G::THR);
           const T x0 = z[q].x * scale, x1 = z[q].y * scale;
-          if constexpr (MODE == MODE_MAIN) {
-            T i0 = T(0), i1 = T(0);
-            if (nyqG != nullptr) {
-              const T hr = sH[ri];
-              i0 = sr * sG[m1] + hr;
-              i1 = sr * sG[m1 + 1] - hr;
+          T c0 = T(0), c1 = T(0);
+          if (MODE != MODE_COMPACT && nyqG != nullptr) {
+            T g0, g1;
+            if constexpr (G::WCOL) {
+              const cpx<T> gg = __ldg(reinterpret_cast<const cpx<T>*>(gsafe + m1));
+              g0 = gg.x; g1 = gg.y;
+            } else {
+              g0 = sG[m1]; g1 = sG[m1 + 1];
             }
-            if (!(p.dbg & 2)) store_pair_cs<T>(out_c + (size_t)r * N + m1, mk<T>(x0, i0), mk<T>(x1, i1));
+            c0 = sr * g0 + hr;
+            c1 = sr * g1 - hr;
+          }
+          if constexpr (MODE == MODE_MAIN) {
+            if (!(p.dbg & 2)) store_pair_cs<T>(out_c + (size_t)r * N + m1, mk<T>(x0, c0), mk<T>(x1, c1));
           } else if constexpr (MODE == MODE_COMPACT) {   // real part only; the Nyquist term is (G, H)
             __stcs(reinterpret_cast<cpx<T>*>(out_r + (size_t)r * N + m1), mk<T>(x0, x1));
           } else {
-            T c0 = T(0), c1 = T(0);
-            if (nyqG != nullptr) {
-              const T hr = sH[ri];
-              c0 = sr * sG[m1] + hr;
-              c1 = sr * sG[m1 + 1] - hr;
-            }
             cpx<T> v = mk<T>(x0 - c0, x1 - c1);
             *reinterpret_cast<cpx<T>*>(out_r + (size_t)r * N + m1) = v;
           }
