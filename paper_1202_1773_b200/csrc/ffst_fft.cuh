@@ -122,6 +122,10 @@ template <typename T, int EM = 16> struct Pad {
   static constexpr int SH = sizeof(cpx<T>) == 8 ? (EM == 8 ? 3 : 4) : 3;
   static FFST_HD int at(int i) { return i + (i >> SH); }
   static constexpr int len(int L) { return L + (L >> SH) + 1; }
+  // at(i0 + q S) = at(i0) + q step(S) for i0 >= 0 when S is a multiple of the pad period (or S = 1 and
+  // i0 a multiple of it, q below it): strided accesses become base + immediate offsets
+  static constexpr bool linear(int S, int Q) { return S % (1 << SH) == 0 || (S == 1 && Q <= (1 << SH)); }
+  static constexpr int step(int S) { return S % (1 << SH) == 0 ? S + (S >> SH) : 1; }
 };
 
 // Pass plan of a length-L line with EM (8 or 16) elements per thread: radix-EM passes with the
@@ -165,10 +169,14 @@ struct LineFFT {
 #pragma unroll
         for (int q = 0; q < R; ++q) x[b * R + q] = r[b + q * NB];
     } else {
+      using PD = Pad<T, EM>;
+      static_assert(PD::linear(L / R, R), "strided reads: linear padded addresses");
 #pragma unroll
-      for (int b = 0; b < NB; ++b)
+      for (int b = 0; b < NB; ++b) {
+        const cpx<T>* s0 = sm + PD::at(t + b * TH);
 #pragma unroll
-        for (int q = 0; q < R; ++q) x[b * R + q] = sm[Pad<T, EM>::at(t + b * TH + q * (L / R))];
+        for (int q = 0; q < R; ++q) x[b * R + q] = s0[q * PD::step(L / R)];
+      }
     }
 #pragma unroll
     for (int b = 0; b < NB; ++b) {
@@ -213,8 +221,15 @@ struct LineFFT {
         const int v = t + b * TH;
         const int k = v & (NS - 1);
         const int base = (v - k) * R + k;
+        using PD = Pad<T, EM>;
+        if constexpr (PD::linear(NS, R) && (NS > 1 || R % (1 << PD::SH) == 0)) {
+          cpx<T>* d0 = sm + PD::at(base);
 #pragma unroll
-        for (int q = 0; q < R; ++q) sm[Pad<T, EM>::at(base + q * NS)] = x[b * R + q];
+          for (int q = 0; q < R; ++q) d0[q * PD::step(NS)] = x[b * R + q];
+        } else {
+#pragma unroll
+          for (int q = 0; q < R; ++q) sm[PD::at(base + q * NS)] = x[b * R + q];
+        }
       }
       SyncOf<TH>::sync();                            // writes visible to the next pass
       pass<S + 1, NS * R>(r, sm, t, tw);

@@ -64,6 +64,11 @@ struct Geo {
   static constexpr int RPT = TRF / LPR > 0 ? TRF / LPR : 1;     // rounds per tile
   static constexpr int TB = TRF;                                  // row block of the WCOL layout
   static FFST_HD size_t wat(int r, int c, int stride) { return ((size_t)(r / TB) * stride + c) * TB + r % TB; }
+  // The inverse's intermediate stays plain column-major: in the row-block layout the row pass stores
+  // each tile as one contiguous chunk (config 5 inverse pass 1 12.7 -> 11.5 ms), but the column pass
+  // then loads 32-byte pieces of eight lines per warp instruction (pass 2 4.5 -> 8.0 ms).
+  static constexpr bool WBLK_INV = false;
+  static FFST_HD size_t iat(int r, int c, int ncols) { return WBLK_INV ? wat(r, c, ncols) : (size_t)c * N + r; }
   static constexpr int RPF_ = WCOL ? TRF : LPR;      // final row pass: one tile / round per CTA (more CTAs)
   static constexpr int RPF = RPF_ < N ? RPF_ : N;
   // inverse pass 1: rows per tile and per item
@@ -695,7 +700,7 @@ struct K {
 #pragma unroll 1
       for (int e = tid; e < ncols * G::GR; e += NT) {
         const int kk = e / G::GR, ri = e - kk * G::GR;
-        if (ri < rows_here) dst[(size_t)kk * N + rt0 + ri] = tile[ri * G::TSTR + kk];
+        if (ri < rows_here) dst[MODE == MODE_MAIN ? G::iat(rt0 + ri, kk, ncols) : (size_t)kk * N + rt0 + ri] = tile[ri * G::TSTR + kk];
       }
       __syncthreads();
       if (ti == 0) FFST_PROBE(p, 3);
@@ -917,8 +922,8 @@ struct K {
       for (int e = tid; e < (p.dbg & 2 ? 0 : ncols * G::GR); e += NT) {
         const int kk = e / G::GR, ri = e - kk * G::GR;
         if (ri < rows_here) {
-          if (p.ring_stream) st_hint<T>(dst + (size_t)kk * N + rt0 + ri, tile[ri * G::TSTR + kk], pf);
-          else dst[(size_t)kk * N + rt0 + ri] = tile[ri * G::TSTR + kk];
+          if (p.ring_stream) st_hint<T>(dst + G::iat(rt0 + ri, kk, ncols), tile[ri * G::TSTR + kk], pf);
+          else dst[G::iat(rt0 + ri, kk, ncols)] = tile[ri * G::TSTR + kk];
         }
       }
       __syncthreads();
@@ -1017,8 +1022,8 @@ struct K {
         for (int e = tid; e < (p.dbg & 2 ? 0 : ncols * G::GR); e += NT) {
           const int kk = e / G::GR, r = e - kk * G::GR;
           if (r < rows_here) {
-            if (p.ring_stream) st_hint<T>(dst + (size_t)kk * N + rt0 + r, tile[r * G::TSTR + kk], pf);
-            else dst[(size_t)kk * N + rt0 + r] = tile[r * G::TSTR + kk];
+            if (p.ring_stream) st_hint<T>(dst + G::iat(rt0 + r, kk, ncols), tile[r * G::TSTR + kk], pf);
+            else dst[G::iat(rt0 + r, kk, ncols)] = tile[r * G::TSTR + kk];
           }
         }
         __syncthreads();
@@ -1060,15 +1065,16 @@ struct K {
         woff += N * P.ncols_pad;
         if (g1 <= P.c_lo || g0 >= P.c_lo + P.ncols) continue;          // CTA-uniform
         const bool in = act && cb >= P.c_lo && cb < P.c_lo + P.ncols;
-        const C* col = slot + cur + (size_t)(in ? cb - P.c_lo : 0) * N;
+        const C* ws = slot + cur;
+        const int cc = in ? cb - P.c_lo : 0;
         C r[G::EC];
         if (p.ring_stream) {
           const unsigned long long pf = policy_evict_first();
 #pragma unroll
-          for (int q = 0; q < G::EC; ++q) r[q] = in ? ld_hint<T>(col + t + q * G::THC, pf) : czero<T>();
+          for (int q = 0; q < G::EC; ++q) r[q] = in ? ld_hint<T>(ws + G::iat(t + q * G::THC, cc, P.ncols), pf) : czero<T>();
         } else {
 #pragma unroll
-          for (int q = 0; q < G::EC; ++q) r[q] = in ? __ldcg(col + t + q * G::THC) : czero<T>();
+          for (int q = 0; q < G::EC; ++q) r[q] = in ? __ldcg(ws + G::iat(t + q * G::THC, cc, P.ncols)) : czero<T>();
         }
         window_lines(P, g0, in, wbuf, scr, R, delta, user_plane<T, N>(p, P), p.dbg & 4);
         if (!(p.dbg & 1)) fft<N, false>(r, scr + line * G::SMC, t, tw);
