@@ -626,6 +626,7 @@ KParams base_params(ffst_plan* p) {
   k.part = p->part;
   k.nyq_fwd = p->nyq_fwd; k.nyq_S = p->nyq_S; k.nyq_T = p->nyq_T; k.corr = p->corr; k.nyq_anti = p->nyq_anti; k.nyq_part = p->nyq_part;
   k.n_rowitems = p->n_rowitems;
+  k.nyq_tparts = p->geo.tparts;
   k.rpi = p->rpi;
   k.a_lane_elems = (long long)p->d.batch * (p->n / 2 + 1) * p->n;
   if (const char* d = std::getenv("FFST_DBG")) k.dbg = std::atoi(d);
@@ -826,6 +827,7 @@ ffst_status inverse_impl(ffst_plan* p, const void* coeff, void* img_out, int bat
     k.compact = 1;
     k.nyq_fwd = const_cast<void*>(nyq_gh);
     k.n_rowitems = 1;            // the alternating sums come whole from (G, H)
+    k.nyq_tparts = 1;
   }
   k.units = q->d_units;
   k.chunks = q->d_chunks + q->n_chunks;
@@ -1543,7 +1545,7 @@ static ffst_status plan_create_impl(ffst_plan** out, const ffst_plan_desc* d_in,
   ALLOC(p->W, (size_t)p->W_elems * csz);
   ALLOC(p->nyq_fwd, B * nn * 2 * N * p->rsz);
   ALLOC(p->nyq_S, B * nn * p->n_rowitems * N * p->rsz);
-  ALLOC(p->nyq_T, B * nn * N * p->rsz);
+  ALLOC(p->nyq_T, B * nn * p->geo.tparts * N * p->rsz);
   ALLOC(p->corr, B * 2 * N * p->rsz);
   ALLOC(p->nyq_anti, nn * 2 * N * p->rsz);
   ALLOC(p->nyq_part, B * 2 * std::min<size_t>(nn, 64) * N * csz);

@@ -141,15 +141,20 @@ template <int L, int EM = 16> struct RadixPlan {
   }
 };
 
-// SYNC: 0 = none needed (single pass), 1 = warp, 2 = CTA
-template <int TH> struct SyncOf {
+// Barrier of one line's TH threads: a warp barrier (TH <= 32), else the CTA barrier, or with NAMED
+// the line's own named barrier (id 1 + threadIdx.x / TH, TH threads) -- the lines of a CTA then
+// run out of step with each other (their barrier waits overlap the other lines' work).  NAMED
+// requires every use of the line's scratch to be ordered by the line's own threads only.
+template <int TH, bool NAMED = false> struct SyncOf {
   static __device__ __forceinline__ void sync() {
-    if constexpr (TH <= 32) __syncwarp(); else __syncthreads();
+    if constexpr (TH <= 32) __syncwarp();
+    else if constexpr (NAMED) asm volatile("bar.sync %0, %1;" ::"r"(1 + (int)(threadIdx.x / TH)), "n"(TH) : "memory");
+    else __syncthreads();
   }
 };
 
 // TWS: the twiddle table is in shared memory (plain loads) instead of global (read-only path).
-template <typename T, int L, bool INV, int TWN, bool TWS = false, int EM = 16, bool TW2 = false>
+template <typename T, int L, bool INV, int TWN, bool TWS = false, int EM = 16, bool TW2 = false, bool NAMED = false>
 struct LineFFT {
   using RP = RadixPlan<L, EM>;
   static constexpr int E = RP::E;
@@ -215,7 +220,7 @@ struct LineFFT {
 #pragma unroll
         for (int q = 0; q < R; ++q) r[b + q * NB] = x[b * R + q];
     } else {
-      if constexpr (!FIRST) SyncOf<TH>::sync();      // all reads of this pass done
+      if constexpr (!FIRST) SyncOf<TH, NAMED>::sync();   // all reads of this pass done
 #pragma unroll
       for (int b = 0; b < NB; ++b) {
         const int v = t + b * TH;
@@ -231,7 +236,7 @@ struct LineFFT {
           for (int q = 0; q < R; ++q) sm[PD::at(base + q * NS)] = x[b * R + q];
         }
       }
-      SyncOf<TH>::sync();                            // writes visible to the next pass
+      SyncOf<TH, NAMED>::sync();                     // writes visible to the next pass
       pass<S + 1, NS * R>(r, sm, t, tw);
     }
   }

@@ -62,13 +62,14 @@ struct KParams {
   long long slot_elems;
   void* nyq_fwd;                // [batch][n_nyq][2][n] T: forward Nyquist terms G(m1), H(r)
   void* nyq_S;                  // [batch][n_nyq][n_rowitems][n] T: partial alternating column sums
-  void* nyq_T;                  // [batch][n_nyq][n] T: alternating row sums
+  void* nyq_T;                  // [batch][n_nyq][nyq_tparts][n] T: alternating row sums (partials summed in order)
   void* corr;                   // [batch][2][n] T: inverse Nyquist corrections
   void* nyq_part;               // [batch][2][<=64][n] cpx<T>: partial Nyquist spectra (stage 1 -> 2)
   void* part;                   // small-n fused path: [batch][eta_l][n][n] T partial images of the inverse
   const void* nyq_anti;         // [n_nyq][2][n] T: anti part of each Nyquist plane on the Nyquist row (0) /
                                 //   column (1), natural bin order (plan table)
   int n_rowitems;               // inverse pass-1 items per plane (row groups)
+  int nyq_tparts;               // partial row sums per row in nyq_T (the pair row pass: one per warp of a line)
   int rpi;                      // inverse pass 1: rows per item (a multiple of Geo::GR)
   const ItemDev* items;
   int n_items;
@@ -108,6 +109,7 @@ struct Geometry {
   size_t smem_fwd, smem_inv, smem_aux;   // dynamic shared bytes of the kernels
   int colpad;        // forward intermediate: row stride = ncols rounded up to a multiple of colpad
   int ncpf;          // final column pass (aux kernels, Geo): padded row stride of its output
+  int tparts;        // inv pass 1: partial alternating row sums per row (nyq_T)
 };
 
 // Launchers (defined per dtype in ffst_kern_f32.cu / ffst_kern_f64.cu).

@@ -35,6 +35,9 @@ struct Geo {
   // measured: the pair form wins for the inverse row pass (configs 2-5) and loses for the forward
   // one at n >= 512 (its stores are 8-byte instead of 16-byte per lane): inverse only
   static constexpr bool PAIR_FWD = false, PAIR_INV = PAIR && sizeof(T) == 4;   // float64: registers
+  // partial alternating row sums per row of a Nyquist plane (nyq_T): the pair row pass leaves one per
+  // warp of a line (no cross-warp reduction, no barrier per round); the other row passes one
+  static constexpr int TPARTS = PAIR_INV && THC > 32 ? THC / 32 : 1;
   static constexpr int SCRX = SCR_C > SCR_R ? SCR_C : SCR_R;
   // forward pass 1: columns per item (>= 32-byte row segments of the intermediate)
   static constexpr int GC = LPC > (32 / ESZ) ? LPC : (32 / ESZ);
@@ -270,10 +273,10 @@ struct K {
       return __ldg(tw + kk);
     }
   }
-  template <int L, bool INV>
+  template <int L, bool INV, bool NAMED = false>
   static __device__ __forceinline__ void fft(C (&r)[LineFFT<T, L, INV, N>::E], C* sm, int t, const C* tw) {
-    if constexpr (TW2) LineFFT<T, L, INV, N, true, 16, true>::run(r, sm, t, tw2tab());
-    else LineFFT<T, L, INV, N>::run(r, sm, t, tw);
+    if constexpr (TW2) LineFFT<T, L, INV, N, true, 16, true, NAMED>::run(r, sm, t, tw2tab());
+    else LineFFT<T, L, INV, N, false, 16, false, NAMED>::run(r, sm, t, tw);
   }
 
   // Window sym_i of the CTA's column lines into wbuf[q * NT + tid] (thread tid's element q = row
@@ -502,29 +505,32 @@ struct K {
     constexpr int RPT = G::RPT;                // WCOL: rounds per tile
     const bool stream = MODE == MODE_MAIN && p.ring_stream;
     const unsigned long long pf = policy_evict_first();
-    // WCOL: the TRF rows from tr0 on (column segments of one row block) -> tile rows, asynchronously
-    auto issue_tile = [&](int tr0) {
-      const int rows_here = cnt - tr0 < G::TRF ? cnt - tr0 : G::TRF;
+    // WCOL: each line owns RPT rows of every TRF-row tile (rows tl TRF + line RPT + j, j < RPT) and
+    // gathers them itself (cp.async, column segments of one row block -> its tile rows), so the
+    // lines of the CTA synchronise only with themselves (named barriers) and run out of step.
+    C* ltile = tile + line * RPT * G::TSTR;
+    auto issue_tile = [&](int tl) {
+      const int rb = tl * G::TRF + line * RPT;                 // first row (in the item) of the line's block
 #pragma unroll 4
-      for (int e = tid; e < ncols * G::TRF; e += NT) {
-        const int kk = e / G::TRF, rr = e - kk * G::TRF;
-        if (rr < rows_here) cp_async_el<T>(tile + rr * G::TSTR + kk, src + G::wat(r0 + tr0 + rr, kk, stride), pf, stream);
+      for (int e = t; e < ncols * RPT; e += G::THR) {
+        const int kk = e / RPT, rr = e - kk * RPT;
+        if (rb + rr < cnt) cp_async_el<T>(ltile + rr * G::TSTR + kk, src + G::wat(r0 + rb + rr, kk, stride), pf, stream);
       }
       cp_async_commit();
     };
     if constexpr (G::WCOL) issue_tile(0);
 #pragma unroll 1
     for (int rd = 0; rd < rounds; ++rd) {
-      const int ri = rd * G::LPR + line;
+      const int ri = G::WCOL ? (rd / RPT) * G::TRF + line * RPT + rd % RPT : rd * G::LPR + line;
       const bool act = ri < cnt;
       const int r = r0 + (act ? ri : 0);
       C z[G::ER], zm[G::ER];
       if constexpr (G::WCOL) {
-        if (rd % RPT == 0) {                   // this round's tile has landed
+        if (rd % RPT == 0) {                   // this round's rows have landed
           cp_async_wait_all();
-          __syncthreads();
+          SyncOf<G::THR, true>::sync();
         }
-        const C* trow = tile + ((rd % RPT) * G::LPR + line) * G::TSTR - c_lo;
+        const C* trow = ltile + (rd % RPT) * G::TSTR - c_lo;
 #pragma unroll
         for (int q = 0; q < G::ER; ++q) {
           const int k = t + q * G::THR, km = H - k;
@@ -532,9 +538,9 @@ struct K {
           z[q] = ik ? trow[k] : czero<T>();
           zm[q] = ikm ? trow[km] : czero<T>();
         }
-        if (rd % RPT == RPT - 1 && rd + 1 < rounds) {   // every read of this tile done: the next one
-          __syncthreads();                              // streams in behind this round's FFT
-          issue_tile((rd + 1) * G::LPR);
+        if (rd % RPT == RPT - 1 && rd + 1 < rounds) {   // every read of the line's rows done: the next
+          SyncOf<G::THR, true>::sync();                 // ones stream in behind this round's FFT
+          issue_tile(rd / RPT + 1);
         }
       } else {
         const C* row = src + (size_t)r * stride - c_lo;
@@ -558,7 +564,7 @@ struct K {
         z[q] = mk<T>(a.x - e.y, a.y + e.x);                 // a + i e
       }
       if (rd == 0) FFST_PROBE(p, 0);
-      if (!(p.dbg & 1)) fft<H, true>(z, scr + line * G::SMR, t, tw);
+      if (!(p.dbg & 1)) fft<H, true, true>(z, scr + line * G::SMR, t, tw);
       if (rd == 0) FFST_PROBE(p, 1);
       if (act) {
         const T sr = (r & 1) ? T(-1) : T(1);
@@ -593,7 +599,7 @@ struct K {
           }
         }
       }
-      SyncOf<G::THR>::sync();
+      SyncOf<G::THR, true>::sync();
     }
   }
 
@@ -873,26 +879,14 @@ struct K {
         C* sl = scr + line * G::SMC;
         if (!(p.dbg & 1)) fft<N, false>(z, sl, t, tw);
         if (ti == 0 && rd == 0) FFST_PROBE(p, 1);
-        if (nyq) {   // alternating row sums t(r) = sum_m1 (-1)^m1 Im c(r, m1) over the line's lanes
+        if (nyq) {   // alternating row sums t(r) = sum_m1 (-1)^m1 Im c(r, m1): one partial per warp
 #pragma unroll
           for (int o = (G::THC < 32 ? G::THC : 32) / 2; o > 0; o >>= 1) {
             ta += __shfl_xor_sync(0xffffffffu, ta, o);
             tb += __shfl_xor_sync(0xffffffffu, tb, o);
           }
-          if constexpr (G::THC > 32) {
-            __syncthreads();
-            if ((tid & 31) == 0) { red[(tid >> 5) * 2] = ta; red[(tid >> 5) * 2 + 1] = tb; }
-            __syncthreads();
-            if (t == 0) {
-              ta = tb = T(0);
-              for (int w = 0; w < G::THC / 32; ++w) {
-                ta += red[((line * G::THC) / 32 + w) * 2];
-                tb += red[((line * G::THC) / 32 + w) * 2 + 1];
-              }
-            }
-          }
-          if (t == 0 && act) {
-            T* tt = static_cast<T*>(p.nyq_T) + ((size_t)nyq_b * p.n_nyq + nyq_idx) * N + ra;
+          if ((t & 31) == 0 && act) {          // summed in warp order by nyq_inv_kernel
+            T* tt = static_cast<T*>(p.nyq_T) + (((size_t)nyq_b * p.n_nyq + nyq_idx) * G::TPARTS + (t >> 5)) * N + ra;
             tt[0] = ta;
             tt[1] = tb;
           }
@@ -959,8 +953,18 @@ struct K {
     const int tid = threadIdx.x, line = tid / G::THC, t = tid % G::THC;
     const C* tw = static_cast<const C*>(p.tw);
     constexpr int RPR = 2 * G::LPC;
-    constexpr int ROUNDS = G::GR / RPR > 0 ? G::GR / RPR : 1;
     constexpr int STRIDE = REAL ? 1 : 2;                   // floats per element (real parts only)
+    // rows per tile: as many as the tile region holds for this plane's columns (a power of two from
+    // GR up to 16 dividing the item; row stride ncols | 1), so that each column segment of W is
+    // 64-128 bytes instead of GR x 8 (fewer, fuller L2 writes, fewer store phases)
+    int gr = G::GR, tstr = G::TSTR;
+    if (G::GR < 16) {
+      const int ts = ncols | 1;
+      while (gr < 16 && 2 * gr * ts <= G::TILE_R && cnt % (2 * gr) == 0) gr *= 2;
+      if (gr > G::GR) tstr = ts;
+    }
+    const int lg = 31 - __clz(gr);
+    const int ROUNDS = gr / RPR > 0 ? gr / RPR : 1;
     const T* base = reinterpret_cast<const T*>(src_c);
     const int nrounds = (cnt + RPR - 1) / RPR;
     T ca[G::EC], cb[G::EC];
@@ -992,7 +996,7 @@ struct K {
       }
       const int rd = i % ROUNDS, ti = i / ROUNDS;
       const int ri = rd * RPR + 2 * line;                  // first row of the pair inside the tile
-      const bool act = ti * G::GR + ri < cnt;
+      const bool act = ti * gr + ri < cnt;
       C z[G::EC];
 #pragma unroll
       for (int q = 0; q < G::EC; ++q) z[q] = mk<T>(ca[q], cb[q]);
@@ -1008,22 +1012,22 @@ struct K {
           const int k = c_lo + kk;                         // 0..H
           const C zk = sl[Pad<T>::at(k)];
           const C zm = sl[Pad<T>::at(k == 0 ? 0 : N - k)];
-          tile[ri * G::TSTR + kk] = mk<T>(T(0.5) * (zk.x + zm.x), T(0.5) * (zk.y - zm.y));
-          tile[(ri + 1) * G::TSTR + kk] = mk<T>(T(0.5) * (zk.y + zm.y), T(0.5) * (zm.x - zk.x));
+          tile[ri * tstr + kk] = mk<T>(T(0.5) * (zk.x + zm.x), T(0.5) * (zk.y - zm.y));
+          tile[(ri + 1) * tstr + kk] = mk<T>(T(0.5) * (zk.y + zm.y), T(0.5) * (zm.x - zk.x));
         }
       }
       SyncOf<G::THC>::sync();
       if (rd == ROUNDS - 1 || i + 1 == nrounds) {          // the tile is complete: -> W (column-major)
         if (dep != nullptr && ti == 0 && tid == 0) spin_wait(dep, dep_target);   // slot reuse
         __syncthreads();
-        const int rt0 = r0 + ti * G::GR;
-        const int rows_here = cnt - ti * G::GR < G::GR ? cnt - ti * G::GR : G::GR;
+        const int rt0 = r0 + ti * gr;
+        const int rows_here = cnt - ti * gr < gr ? cnt - ti * gr : gr;
 #pragma unroll 1
-        for (int e = tid; e < (p.dbg & 2 ? 0 : ncols * G::GR); e += NT) {
-          const int kk = e / G::GR, r = e - kk * G::GR;
+        for (int e = tid; e < (p.dbg & 2 ? 0 : ncols << lg); e += NT) {
+          const int kk = e >> lg, r = e & (gr - 1);
           if (r < rows_here) {
-            if (p.ring_stream) st_hint<T>(dst + G::iat(rt0 + r, kk, ncols), tile[r * G::TSTR + kk], pf);
-            else dst[G::iat(rt0 + r, kk, ncols)] = tile[r * G::TSTR + kk];
+            if (p.ring_stream) st_hint<T>(dst + G::iat(rt0 + r, kk, ncols), tile[r * tstr + kk], pf);
+            else dst[G::iat(rt0 + r, kk, ncols)] = tile[r * tstr + kk];
           }
         }
         __syncthreads();
@@ -1088,7 +1092,7 @@ struct K {
         }
         SyncOf<G::THC>::sync();
       }
-      if (act) {
+      if (act && !(p.dbg & 64)) {            // (FFST_DBG bit 64, measurement only: no accumulation)
         C* a = static_cast<C*>(p.A) + (size_t)I.pad1 * p.a_lane_elems + ((size_t)I.b * (H + 1) + cb) * N;
         const unsigned long long pl = policy_evict_last();
 #pragma unroll
@@ -1428,7 +1432,8 @@ __global__ void __launch_bounds__(256) nyq_inv_kernel(KParams p) {
           const T* ps = static_cast<const T*>(p.nyq_S) + ((size_t)b * p.n_nyq + nq) * p.n_rowitems * N + m;
           for (int g = 0; g < p.n_rowitems; ++g) s += ps[(size_t)g * N];
         } else {
-          s = static_cast<const T*>(p.nyq_T)[((size_t)b * p.n_nyq + nq) * N + m];
+          const T* pt = static_cast<const T*>(p.nyq_T) + ((size_t)b * p.n_nyq + nq) * p.nyq_tparts * N + m;
+          for (int w = 0; w < p.nyq_tparts; ++w) s += pt[(size_t)w * N];
         }
       }
       r[q] = mk<T>(s, T(0));

@@ -27,7 +27,7 @@ template <typename T, int N> struct Launch {
     Geometry g{};
     g.nt = G::NT; g.gc = G::GC; g.rp2 = G::RP2; g.rpi = G::RPI; g.gr = G::GR; g.lpc = G::LPC; g.igc = G::IGC;
     g.smem_fwd = G::SMEM_FWD; g.smem_inv = G::SMEM_INV; g.smem_aux = G::SMEM_AUX;
-    g.colpad = G::GC; g.ncpf = G::NCPF;
+    g.colpad = G::GC; g.ncpf = G::NCPF; g.tparts = G::TPARTS;
     return g;
   }
   static cudaError_t spectrum(const KParams& p, int batch, cudaStream_t s) {

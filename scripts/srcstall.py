@@ -3,16 +3,17 @@ import csv, gzip, sys, collections, re
 path = sys.argv[1]; top = int(sys.argv[2]) if len(sys.argv) > 2 else 20
 want = sys.argv[3].split(',') if len(sys.argv) > 3 else ['stall_long_sb', 'stall_short_sb', 'stall_no_inst', 'stall_wait', 'stall_selected']
 rows = list(csv.reader(gzip.open(path, 'rt') if path.endswith('.gz') else open(path)))
-hdr = None; func = None; cur = None; src = ''
+hdr = None; func = None; cur = None; src = ''; fname = ''
 agg = collections.defaultdict(lambda: collections.Counter())
 srcs = {}
 for r in rows:
     if not r: continue
+    if r[0] == 'File Path': fname = r[1].split('/')[-1]; continue
     if r[0] == 'Function Name': func = r[1]; continue
     if r[0] == 'Line No': hdr = r; continue
     if hdr is None: continue
     if r[0].strip().isdigit() and r[1]:
-        cur = (func, r[0]); srcs[cur] = r[1].strip()[:90]; continue
+        cur = (func, fname + ':' + r[0]); srcs[cur] = r[1].strip()[:80]; continue
     d = dict(zip(hdr, r))
     if not d.get('Address'): continue
     for k in hdr:
