@@ -35,9 +35,9 @@ struct Geo {
   // measured: the pair form wins for the inverse row pass (configs 2-5) and loses for the forward
   // one at n >= 512 (its stores are 8-byte instead of 16-byte per lane): inverse only
   static constexpr bool PAIR_FWD = false, PAIR_INV = PAIR && sizeof(T) == 4;   // float64: registers
-  // partial alternating row sums per row of a Nyquist plane (nyq_T): the pair row pass leaves one per
-  // warp of a line (no cross-warp reduction, no barrier per round); the other row passes one
-  static constexpr int TPARTS = PAIR_INV && THC > 32 ? THC / 32 : 1;
+  // partial alternating row sums per row of a Nyquist plane (nyq_T): one per warp of a line (no
+  // cross-warp reduction, no barrier per round)
+  static constexpr int TPARTS = PAIR_INV ? (THC > 32 ? THC / 32 : 1) : (THR > 32 ? THR / 32 : 1);
   static constexpr int SCRX = SCR_C > SCR_R ? SCR_C : SCR_R;
   // forward pass 1: columns per item (>= 32-byte row segments of the intermediate)
   static constexpr int GC = LPC > (32 / ESZ) ? LPC : (32 / ESZ);
@@ -514,11 +514,19 @@ struct K {
 #pragma unroll 4
       for (int e = t; e < ncols * RPT; e += G::THR) {
         const int kk = e / RPT, rr = e - kk * RPT;
-        if (rb + rr < cnt) cp_async_el<T>(ltile + rr * G::TSTR + kk, src + G::wat(r0 + rb + rr, kk, stride), pf, stream);
+        if (rb + rr < cnt) cp_async_el<T>(ltile + rr * G::TSTR + c_lo + kk, src + G::wat(r0 + rb + rr, kk, stride), pf, stream);
       }
       cp_async_commit();
     };
-    if constexpr (G::WCOL) issue_tile(0);
+    if constexpr (G::WCOL) {
+      // the line's tile rows are indexed by the bin k = 0..H: zero outside the plane's bins (the copies
+      // never touch them), so the rounds read them without range tests
+      for (int e = t; line * RPT < G::TRF && e < (G::H + 1 - ncols) * RPT; e += G::THR) {
+        const int rr = e % RPT, j = e / RPT;
+        ltile[rr * G::TSTR + (j < c_lo ? j : j + ncols)] = czero<T>();
+      }
+      issue_tile(0);
+    }
 #pragma unroll 1
     for (int rd = 0; rd < rounds; ++rd) {
       const int ri = G::WCOL ? (rd / RPT) * G::TRF + line * RPT + rd % RPT : rd * G::LPR + line;
@@ -530,13 +538,11 @@ struct K {
           cp_async_wait_all();
           SyncOf<G::THR, true>::sync();
         }
-        const C* trow = ltile + (rd % RPT) * G::TSTR - c_lo;
+        const C* trow = ltile + (rd % RPT) * G::TSTR;
 #pragma unroll
-        for (int q = 0; q < G::ER; ++q) {
-          const int k = t + q * G::THR, km = H - k;
-          const bool ik = act && k >= c_lo && k < c_lo + ncols, ikm = act && km >= c_lo && km < c_lo + ncols;
-          z[q] = ik ? trow[k] : czero<T>();
-          zm[q] = ikm ? trow[km] : czero<T>();
+        for (int q = 0; q < G::ER; ++q) {     // (line-uniform test: lines past the tile read nothing)
+          z[q] = act ? trow[t + q * G::THR] : czero<T>();
+          zm[q] = act ? trow[H - t - q * G::THR] : czero<T>();
         }
         if (rd % RPT == RPT - 1 && rd + 1 < rounds) {   // every read of the line's rows done: the next
           SyncOf<G::THR, true>::sync();                 // ones stream in behind this round's FFT
@@ -616,6 +622,9 @@ struct K {
     const int tid = threadIdx.x, line = tid / G::THR, t = tid % G::THR;
     const C* tw = static_cast<const C*>(p.tw);
     const bool nyq = MODE == MODE_MAIN && nyq_idx >= 0;
+    // MAIN: the lines of the CTA synchronise only with themselves inside a tile (named barriers);
+    // the whole CTA meets at the tile stores
+    constexpr bool NL = MODE == MODE_MAIN;
     T sacc[G::ER][2];
 #pragma unroll
     for (int q = 0; q < G::ER; ++q) sacc[q][0] = sacc[q][1] = T(0);
@@ -660,31 +669,22 @@ struct K {
             z[q] = act ? *reinterpret_cast<const cpx<T>*>(src_r + (size_t)(act ? r : r0) * N + 2 * (t + q * G::THR)) : czero<T>();
         }
         if (ti == 0 && rd == 0) FFST_PROBE(p, 0);
-        fft<H, false>(z, scr + line * G::SMR, t, tw);
+        fft<H, false, NL>(z, scr + line * G::SMR, t, tw);
         if (ti == 0 && rd == 0) FFST_PROBE(p, 1);
         if (nyq) {
-          // alternating row sum t(r) = sum_m1 (-1)^m1 Im c(r, m1), reduced over the line
+          // alternating row sum t(r) = sum_m1 (-1)^m1 Im c(r, m1): one partial per warp of the line
+          // (G::TPARTS, summed in order by nyq_inv_kernel)
           T v = trow;
 #pragma unroll
           for (int o = (G::THR < 32 ? G::THR : 32) / 2; o > 0; o >>= 1) v += __shfl_xor_sync(0xffffffffu, v, o);
-          if constexpr (G::THR > 32) {
-            T* red = reinterpret_cast<T*>(tile + G::TILE_R);   // NT/32 scalars past the tile
-            __syncthreads();
-            if ((tid & 31) == 0) red[tid >> 5] = v;
-            __syncthreads();
-            if (t == 0) {
-              v = T(0);
-              for (int w = 0; w < G::THR / 32; ++w) v += red[(line * G::THR) / 32 + w];
-            }
-          }
-          if (t == 0 && act)
-            static_cast<T*>(p.nyq_T)[((size_t)nyq_b * p.n_nyq + nyq_idx) * N + r] = v;
+          if ((t & 31) == 0 && act)
+            static_cast<T*>(p.nyq_T)[(((size_t)nyq_b * p.n_nyq + nyq_idx) * G::TPARTS + (t >> 5)) * N + r] = v;
         }
         C* sl = scr + line * G::SMR;
-        SyncOf<G::THR>::sync();
+        SyncOf<G::THR, NL>::sync();
 #pragma unroll
         for (int q = 0; q < G::ER; ++q) sl[Pad<T>::at(t + q * G::THR)] = z[q];
-        SyncOf<G::THR>::sync();
+        SyncOf<G::THR, NL>::sync();
         if (act) {
 #pragma unroll 1
           for (int kk = t; kk < ncols; kk += G::THR) {
@@ -693,11 +693,11 @@ struct K {
             const C zm = sl[Pad<T>::at(k == 0 ? 0 : H - k)];
             const C a = mk<T>(zk.x + zm.x, zk.y - zm.y);    // Z[k] + conj(Z[H-k])
             const C d = mk<T>(zk.x - zm.x, zk.y + zm.y);    // Z[k] - conj(Z[H-k])
-            const C e = cmul<T>(d, __ldg(tw + k));           // W^k d
+            const C e = cmul<T>(d, twk(k, tw));              // W^k d
             tile[ri * G::TSTR + kk] = mk<T>(T(0.5) * (a.x + e.y), T(0.5) * (a.y - e.x));   // (a - i e)/2
           }
         }
-        SyncOf<G::THR>::sync();
+        SyncOf<G::THR, NL>::sync();
         if (ti == 0 && rd == 0) FFST_PROBE(p, 2);
       }
       if (dep != nullptr && ti == 0 && tid == 0) spin_wait(dep, dep_target);   // slot reuse: before the first write
