@@ -408,6 +408,27 @@ def test_float64_large(F, n):
         assert plane_err(c[0, i].cpu().numpy(), ref[i], np.max(np.abs(xo[0]))) <= 1e-10, i
 
 
+def test_float32_large_two_images(F):
+    # n = 2048 float32, two images (the forward intermediate in 4-row blocks, the row pass's
+    # per-line tiles with LPR = 4 lines per CTA): one plane of every (kind, j) pair and the first /
+    # last Nyquist planes of both images against the oracle, round trip
+    n = 2048
+    x, xo = images(5, 2, n, torch.float32)
+    plan = F.Plan(n, 2, torch.float32)
+    xd = x.cuda()
+    c = plan.forward(xd)
+    rec = plan.inverse(c)
+    assert float((rec - xd).abs().max() / xd.abs().max()) <= 1e-4
+    base, eta = _kind_scale_planes(n)
+    nyq = plan.nyquist_planes()
+    planes = sorted(set(base) | {nyq[0], nyq[-1]})
+    for b in range(2):
+        x64 = x[b].double().numpy()
+        ref = OP.forward_planes(x64, planes)
+        for i in planes:
+            assert plane_err(c[b, i].cpu().numpy(), ref[i], np.max(np.abs(x64))) <= 1e-4, (b, i)
+
+
 def test_config5_forward_planes(F):
     # configs[4]: 4096x4096 float32 single image; the forward against the oracle on one plane of
     # every (kind, j) pair and on every finest-scale Nyquist plane; round trip and Parseval
