@@ -21,11 +21,14 @@ template <typename T, int N>
 struct Tiny {
   using C = cpx<T>;
   static constexpr int NT = 512;   // (the window and the plane I/O run on all threads, the line FFTs on N * TH)
-  static constexpr int E = RadixPlan<N>::E, TH = N / E;
+  // 8 elements per thread from n = 64 on: the n lines of a pass then occupy all 512 threads (64 x 8)
+  // instead of half of them (radix-8 passes: half the serial work per thread)
+  static constexpr int EM = N >= 64 ? 8 : 16;
+  static constexpr int E = RadixPlan<N, EM>::E, TH = N / E;
   static constexpr int LPR = NT / TH < N ? NT / TH : N;      // lines per round
   static constexpr int ROUNDS = N / LPR;
   static constexpr int LD = N + 1;                          // row stride of the plane in shared memory
-  static constexpr int SCR = Pad<T>::len(N);
+  static constexpr int SCR = Pad<T, EM>::len(N);
   static constexpr size_t SMEM = (size_t)(N * LD + LPR * SCR) * sizeof(C);
 
   // 1-D FFTs of all rows (ROW) or columns of the shared plane, in place; INV: inverse sign.
@@ -43,7 +46,7 @@ struct Tiny {
           const int m = t + q * TH;
           r[q] = ROW ? pl[l * LD + m] : pl[m * LD + l];
         }
-        LineFFT<T, N, INV, N>::run(r, scr + line * SCR, t, tw);
+        LineFFT<T, N, INV, N, false, EM>::run(r, scr + line * SCR, t, tw);
 #pragma unroll
         for (int q = 0; q < E; ++q) {
           const int m = t + q * TH;
@@ -125,7 +128,15 @@ __global__ void __launch_bounds__(256) tiny_sum_kernel(KParams p) {
   if (e >= N * N) return;
   const T* part = static_cast<const T*>(p.part) + (size_t)b * p.eta_l * N * N + e;
   T s = T(0);
-  for (int i = 0; i < p.eta_l; ++i) s += part[(size_t)i * N * N];
+  int i = 0;
+  for (; i + 8 <= p.eta_l; i += 8) {               // eight loads in flight, added in plane order
+    T v[8];
+#pragma unroll
+    for (int u = 0; u < 8; ++u) v[u] = part[(size_t)(i + u) * N * N];
+#pragma unroll
+    for (int u = 0; u < 8; ++u) s += v[u];
+  }
+  for (; i < p.eta_l; ++i) s += part[(size_t)i * N * N];
   static_cast<T*>(p.img_out)[(size_t)b * N * N + e] = s;
 }
 
