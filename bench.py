@@ -530,9 +530,14 @@ def run_gpu(args, cfg):
                       "h2d_bytes_per_step": B * N * N * rsz, "d2h_bytes_per_step": B * N * N * rsz,
                       "launch": "replayed CUDA graph (copies included, one step at a time, L2 flushed between)"
                       if egraph is not None else "eager", "roundtrip_max_rel_err": e2e_rt}
-        e2e = e2e_pipelined(plan, x_pin, out_pin, cube, B, N, dtype, dev, stream, args.steps)
+        streamed = e2e_pipelined(plan, x_pin, out_pin, cube, B, N, dtype, dev, stream, args.steps)
+        streamed["roundtrip_max_rel_err"] = float((out_pin - x_host).abs().max() / x_host.abs().max())
+        # the better of the two user loops (small problems are launch bound: there the graph-replayed
+        # one-step-at-a-time loop wins; large ones overlap the copies with the transforms)
+        e2e = dict(streamed if streamed["value"] >= e2e_serial["value"] else e2e_serial)
+        e2e["mode"] = "streamed" if streamed["value"] >= e2e_serial["value"] else "serial"
+        e2e["streamed"] = {k: v for k, v in streamed.items()}
         e2e["serial"] = e2e_serial
-        e2e["roundtrip_max_rel_err"] = max(e2e_rt, float((out_pin - x_host).abs().max() / x_host.abs().max()))
 
     # compact coefficient format: real parts + Nyquist vectors, half the cube bytes
     compact = None
