@@ -79,8 +79,13 @@ struct Geo {
   static constexpr int GR = GR_ < N ? GR_ : N;
   static constexpr int TSTR = H + 1;           // odd: conflict-free column reads of the tile
   static constexpr int TILE_R = GR * TSTR;
-  static constexpr int RPI_ = (N >= 2048 ? 32 : N / 16) > GR ? (N >= 2048 ? 32 : N / 16) : GR;
+  // (measured at configs 2-5: n = 256 best at 128 rows, 512 and 1024 at 64, 4096 at 32)
+  static constexpr int RPI0 = N >= 2048 ? 32 : (N >= 512 ? 64 : N / 2);
+  static constexpr int RPI_ = RPI0 > GR ? RPI0 : GR;
   static constexpr int RPI = RPI_ < N ? RPI_ : N;
+  // spectrum row pass (spec_rows_kernel): rows per CTA (more, smaller CTAs: one short launch)
+  static constexpr int RPS_ = (N >= 2048 ? 32 : N / 16) > GR ? (N >= 2048 ? 32 : N / 16) : GR;
+  static constexpr int RPS = RPS_ < N ? RPS_ : N;
   // padded row stride of the final column pass output
   static constexpr int NCPF = ((H + 1 + GC - 1) / GC) * GC;
   // inverse pass 2: column groups of LPC columns per round, IG rounds per item (n >= 2048: one
@@ -1291,15 +1296,15 @@ __global__ void __launch_bounds__(256, 2) inv_main_kernel(KParams p) {
 
 // ---------------------------------------------------------------------- auxiliary kernels
 
-// spectrum pass 1: rows of img[b] -> Fscr[b] column-major (all bins 0..H); grid (N/RPI, B)
+// spectrum pass 1: rows of img[b] -> Fscr[b] column-major (all bins 0..H); grid (N/RPS, B)
 template <typename T, int N>
 __global__ void __launch_bounds__(256) spec_rows_kernel(KParams p) {
   extern __shared__ __align__(128) unsigned char smem_raw[];
   K<T, N>::tw2_fill(p);
   using G = Geo<T, N>;
   const int b = blockIdx.y, g = blockIdx.x;
-  const int r0 = g * G::RPI;
-  const int cnt = N - r0 < G::RPI ? N - r0 : G::RPI;
+  const int r0 = g * G::RPS;
+  const int cnt = N - r0 < G::RPS ? N - r0 : G::RPS;
   const T* src = static_cast<const T*>(p.img) + (size_t)b * N * N;
   cpx<T>* dst = static_cast<cpx<T>*>(p.Fscr) + (size_t)b * (N / 2 + 1) * N;
   K<T, N>::template row_r2c<MODE_AUX>(p, nullptr, src, 0, N / 2 + 1, r0, cnt, dst, b, -1, 0,

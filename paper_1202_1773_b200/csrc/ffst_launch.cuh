@@ -32,7 +32,7 @@ template <typename T, int N> struct Launch {
   }
   static cudaError_t spectrum(const KParams& p, int batch, cudaStream_t s) {
     FFST_CHECK(set_smem(spec_rows_kernel<T, N>, G::SMEM_INV));
-    spec_rows_kernel<T, N><<<dim3(N / G::RPI, batch), G::NT, G::SMEM_INV, s>>>(p);
+    spec_rows_kernel<T, N><<<dim3(N / G::RPS, batch), G::NT, G::SMEM_INV, s>>>(p);
     FFST_CHECK(cudaGetLastError());
     FFST_CHECK(set_smem(spec_cols_kernel<T, N>, G::SMEM_AUX));
     spec_cols_kernel<T, N><<<dim3((N / 2 + 1 + G::LPC - 1) / G::LPC, batch), G::NT, G::SMEM_AUX, s>>>(p);
