@@ -56,10 +56,11 @@ struct Geo {
   // block (DRAM locality: plain column-major would read 32-byte segments 32 KB apart at n = 4096).
   static constexpr bool WCOL = DIRECT;
   static constexpr int TILE_CE = DIRECT ? 0 : TILE_C;     // tile elements allocated (pass 1)
-  // forward pass 2 / final rows: rows per item (~128 KB of output)
-  // (n >= 2048: at least 16 rows -- per-item overhead and the Nyquist-term staging amortised)
-  static constexpr int RP2_A = (131072 / (N * ESZ)) > LPR ? (131072 / (N * ESZ)) : LPR;
-  static constexpr int RP2_ = (N >= 2048 && RP2_A < 16) ? 16 : RP2_A;
+  // forward pass 2: rows per item (per-item overhead and the Nyquist-term staging amortised)
+  // (measured sweep: ~256 KB of output per item up to n = 512, 512 KB at n = 1024, 64 rows from n = 2048)
+  static constexpr int RP2_B = (N >= 1024 ? 524288 : 262144) / (N * ESZ);
+  static constexpr int RP2_A = RP2_B > LPR ? RP2_B : LPR;
+  static constexpr int RP2_ = (N >= 2048 && RP2_A < 64) ? 64 : RP2_A;
   static constexpr int RP2 = RP2_ < N ? RP2_ : N;
   // column-major row pass (WCOL): rows per shared tile
   static constexpr int TRF_ = LPR > 4 ? LPR : 4;
