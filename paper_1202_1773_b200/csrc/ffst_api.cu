@@ -1497,8 +1497,11 @@ static ffst_status plan_create_impl(ffst_plan** out, const ffst_plan_desc* d_in,
   const char* env = std::getenv("FFST_SLOT_KB");
   // chunk byte budget: 4 MB; 16 MB from n = 1024 (planes of ~1.6 MB: longer chunks shorten the
   // inverse's accumulation chains; measured config 4: 868 -> 943 images/s at 12 MB, 1173 -> 1202 at
-  // 16 MB (24-32 MB no further gain), config 3 no gain)
-  const long long budget_bytes = (env ? std::atoll(env) : (d->n >= 1024 ? 16384 : 4096)) * 1024LL;
+  // 16 MB (24-128 MB no further gain), config 3 no gain); 256 MB from n = 2048, where the ring is in
+  // HBM anyway (config 5: chunks of ~9 planes instead of one, the adjoint accumulating them in
+  // registers: 31.5 -> 30.1 ms per step; 64 / 128 / 512 MB: 31.1 / 30.4 / 30.5 ms)
+  const long long budget_kb = d->n >= 2048 ? 262144 : (d->n >= 1024 ? 16384 : 4096);
+  const long long budget_bytes = (env ? std::atoll(env) : budget_kb) * 1024LL;
   p->slot_budget = std::max(maxplane, budget_bytes / (long long)csz);
   {
     // accumulator lanes: as many as keep the lanes of A L2-sized (<= 32 MB), at most 4 (16 for
