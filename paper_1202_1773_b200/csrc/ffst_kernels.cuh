@@ -80,8 +80,8 @@ struct Geo {
   static constexpr int GR = GR_ < N ? GR_ : N;
   static constexpr int TSTR = H + 1;           // odd: conflict-free column reads of the tile
   static constexpr int TILE_R = GR * TSTR;
-  // (measured at configs 2-5: n = 256 best at 128 rows, 512 and 1024 at 64, 4096 at 32)
-  static constexpr int RPI0 = N >= 2048 ? 32 : (N >= 512 ? 64 : N / 2);
+  // (measured at configs 2-5: n = 256 best at 128 rows, 512 to 4096 at 64)
+  static constexpr int RPI0 = N >= 512 ? 64 : N / 2;
   static constexpr int RPI_ = RPI0 > GR ? RPI0 : GR;
   static constexpr int RPI = RPI_ < N ? RPI_ : N;
   // spectrum row pass (spec_rows_kernel): rows per CTA (more, smaller CTAs: one short launch)
