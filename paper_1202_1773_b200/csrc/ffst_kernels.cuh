@@ -72,6 +72,10 @@ struct Geo {
   // each tile as one contiguous chunk (config 5 inverse pass 1 12.7 -> 11.5 ms), but the column pass
   // then loads 32-byte pieces of eight lines per warp instruction (pass 2 4.5 -> 8.0 ms).
   static constexpr bool WBLK_INV = false;
+  // inverse pass 1 (row pairs): the extraction stores each column's row pair straight to W instead
+  // of staging a tile of rows in shared memory (measured, 20-step A/B twice: n = 256 inverse 0.239 -> 0.227 ms, n = 512 3.42 -> 3.33 ms,
+  // n = 1024 even, n = 4096 +15 %: there the tile's 64-128-byte column segments win)
+  static constexpr bool DIRW = N <= 512;
   static FFST_HD size_t iat(int r, int c, int ncols) { return WBLK_INV ? wat(r, c, ncols) : (size_t)c * N + r; }
   static constexpr int RPF_ = WCOL ? TRF : LPR;      // final row pass: one tile / round per CTA (more CTAs)
   static constexpr int RPF = RPF_ < N ? RPF_ : N;
@@ -149,6 +153,16 @@ template <> __device__ __forceinline__ void st_hint<float>(float2* dst, float2 v
 }
 template <> __device__ __forceinline__ void st_hint<double>(double2* dst, double2 v, unsigned long long pol) {
   asm volatile("st.global.cg.L2::cache_hint.v2.f64 [%0], {%1, %2}, %3;" ::"l"(dst), "d"(v.x), "d"(v.y), "l"(pol) : "memory");
+}
+// two adjacent complex values in one store (float32: 16 bytes) with an L2 policy
+template <typename T> __device__ __forceinline__ void store_pair_hint(cpx<T>* dst, cpx<T> a, cpx<T> b, unsigned long long pol);
+template <> __device__ __forceinline__ void store_pair_hint<float>(float2* dst, float2 a, float2 b, unsigned long long pol) {
+  asm volatile("st.global.cg.L2::cache_hint.v4.f32 [%0], {%1, %2, %3, %4}, %5;" ::"l"(dst), "f"(a.x), "f"(a.y), "f"(b.x),
+               "f"(b.y), "l"(pol) : "memory");
+}
+template <> __device__ __forceinline__ void store_pair_hint<double>(double2* dst, double2 a, double2 b, unsigned long long pol) {
+  st_hint<double>(dst, a, pol);
+  st_hint<double>(dst + 1, b, pol);
 }
 template <typename T> __device__ __forceinline__ cpx<T> ld_hint(const cpx<T>* src, unsigned long long pol);
 template <> __device__ __forceinline__ float2 ld_hint<float>(const float2* src, unsigned long long pol) {
@@ -830,6 +844,12 @@ struct K {
     for (int q = 0; q < G::EC; ++q) sacc[q] = T(0);
     constexpr int ROUNDS = G::GR / RPR > 0 ? G::GR / RPR : 1;
     const int ntiles = (cnt + G::GR - 1) / G::GR;
+    const bool direct = G::DIRW ^ ((p.dbg & 128) != 0);    // (see row_r2c_pair_pipe)
+    const unsigned long long pfd = policy_evict_first();
+    if (direct && dep != nullptr) {
+      if (tid == 0) spin_wait(dep, dep_target);           // slot reuse: before the first write
+      __syncthreads();
+    }
 #pragma unroll 1
     for (int ti = 0; ti < ntiles; ++ti) {
       const int rt0 = r0 + ti * G::GR;
@@ -901,7 +921,21 @@ struct K {
 #pragma unroll
         for (int q = 0; q < G::EC; ++q) sl[Pad<T>::at(t + q * G::THC)] = z[q];
         SyncOf<G::THC>::sync();
-        if (act) {
+        if (act && direct) {
+#pragma unroll 2
+          for (int kk = t; kk < ncols; kk += G::THC) {
+            const int k = c_lo + kk;                         // 0..H
+            const C zk = sl[Pad<T>::at(k)];
+            const C zm = sl[Pad<T>::at(k == 0 ? 0 : N - k)];
+            const C xa = mk<T>(T(0.5) * (zk.x + zm.x), T(0.5) * (zk.y - zm.y));
+            const C xb = mk<T>(T(0.5) * (zk.y + zm.y), T(0.5) * (zm.x - zk.x));
+            C* d = dst + G::iat(ra, kk, ncols);
+            if (!(p.dbg & 2)) {
+              if (p.ring_stream) store_pair_hint<T>(d, xa, xb, pfd);
+              else store_pair_cg<T>(d, xa, xb);
+            }
+          }
+        } else if (act) {
 #pragma unroll 2
           for (int kk = t; kk < ncols; kk += G::THC) {
             const int k = c_lo + kk;                         // 0..H
@@ -914,6 +948,7 @@ struct K {
         SyncOf<G::THC>::sync();
         if (ti == 0 && rd == 0) FFST_PROBE(p, 2);
       }
+      if (direct) continue;          // (each line reuses only its own scratch: no CTA barrier per tile)
       if (dep != nullptr && ti == 0 && tid == 0) spin_wait(dep, dep_target);   // slot reuse: before the first write
       __syncthreads();
       const int rows_here = cnt - ti * G::GR < G::GR ? cnt - ti * G::GR : G::GR;
@@ -931,6 +966,7 @@ struct K {
     }
     if (nyq) {
       // partial alternating column sums s(m1) over this item's rows: lines summed in fixed order
+      if (direct) __syncthreads();                          // (every line done with its scratch)
       T* rs = reinterpret_cast<T*>(scr);                    // [LPC][N] scalars (fits SCR_C)
 #pragma unroll
       for (int q = 0; q < G::EC; ++q) rs[line * N + t + q * G::THC] = sacc[q];
@@ -986,6 +1022,14 @@ struct K {
       }
     }
     const unsigned long long pf = policy_evict_first();
+    // Direct stores (Geo::DIRW; FFST_DBG bit 128 flips it, measurement only): the pair extraction
+    // stores each column's two rows straight to W (one 16-byte store per column and row pair,
+    // column-major: rows ra, ra + 1 are adjacent), no shared tile and no CTA-wide store phase
+    const bool direct = G::DIRW ^ ((p.dbg & 128) != 0);
+    if (direct && dep != nullptr) {
+      if (tid == 0) spin_wait(dep, dep_target);           // slot reuse: before the first write
+      __syncthreads();
+    }
 #pragma unroll 1
     for (int i = 0; i < nrounds; ++i) {
       T na[G::EC], nb[G::EC];
@@ -1012,7 +1056,25 @@ struct K {
 #pragma unroll
       for (int q = 0; q < G::EC; ++q) sl[Pad<T>::at(t + q * G::THC)] = z[q];
       SyncOf<G::THC>::sync();
-      if (act) {
+      if (act && direct) {
+        const int ra = r0 + ti * gr + ri;
+#pragma unroll 2
+        for (int kk = t; kk < ncols; kk += G::THC) {
+          const int k = c_lo + kk;                         // 0..H
+          const C zk = sl[Pad<T>::at(k)];
+          const C zm = sl[Pad<T>::at(k == 0 ? 0 : N - k)];
+          const C xa = mk<T>(T(0.5) * (zk.x + zm.x), T(0.5) * (zk.y - zm.y));
+          const C xb = mk<T>(T(0.5) * (zk.y + zm.y), T(0.5) * (zm.x - zk.x));
+          C* d = dst + G::iat(ra, kk, ncols);
+          if (!(p.dbg & 2)) {
+            if (p.ring_stream) {
+              store_pair_hint<T>(d, xa, xb, pf);
+            } else {
+              store_pair_cg<T>(d, xa, xb);
+            }
+          }
+        }
+      } else if (act) {
 #pragma unroll 2
         for (int kk = t; kk < ncols; kk += G::THC) {
           const int k = c_lo + kk;                         // 0..H
@@ -1023,7 +1085,7 @@ struct K {
         }
       }
       SyncOf<G::THC>::sync();
-      if (rd == ROUNDS - 1 || i + 1 == nrounds) {          // the tile is complete: -> W (column-major)
+      if (!direct && (rd == ROUNDS - 1 || i + 1 == nrounds)) {   // the tile is complete: -> W (column-major)
         if (dep != nullptr && ti == 0 && tid == 0) spin_wait(dep, dep_target);   // slot reuse
         __syncthreads();
         const int rt0 = r0 + ti * gr;

@@ -51,7 +51,7 @@ case "$task" in
     echo "ncu traffic exit $?" ;;
   env) IFS=';' read -ra SETS <<< "$1"; cfgs=$2
     for e in "${SETS[@]}"; do for c in $cfgs; do
-      env $e timeout 600 python bench.py --config "$c" --steps 5 --warmup 3 --no-cpu-baseline --no-cufft \
+      env $e timeout 600 python bench.py --config "$c" --steps ${STEPS:-5} --warmup 3 --no-cpu-baseline --no-cufft \
         > gpurun_out/b.json 2> gpurun_out/b.err || tail -2 gpurun_out/b.err
       echo -n "[$e] "; summ gpurun_out/b.json
     done; done ;;
