@@ -195,6 +195,19 @@ template <> __device__ __forceinline__ void load_pair_cs<double>(const double2* 
 }
 
 // Asynchronous global -> shared copies (LDGSTS): no registers held while in flight.
+// Loads of the small vectors an item re-reads for every row (the Nyquist terms G, H): read-only path,
+// kept in L1 against the streaming traffic (L1::evict_last).
+template <typename T> __device__ __forceinline__ cpx<T> ldg_keep2(const cpx<T>* src);
+template <> __device__ __forceinline__ float2 ldg_keep2<float>(const float2* src) {
+  float2 v;
+  asm("ld.global.nc.L1::evict_last.v2.f32 {%0, %1}, [%2];" : "=f"(v.x), "=f"(v.y) : "l"(src));
+  return v;
+}
+template <> __device__ __forceinline__ double2 ldg_keep2<double>(const double2* src) {
+  double2 v;
+  asm("ld.global.nc.L1::evict_last.v2.f64 {%0, %1}, [%2];" : "=d"(v.x), "=d"(v.y) : "l"(src));
+  return v;
+}
 template <typename T> __device__ __forceinline__ void cp_async_el(cpx<T>* dst_smem, const cpx<T>* src, unsigned long long pol,
                                                                  bool hint) {
   const unsigned d = (unsigned)__cvta_generic_to_shared(dst_smem);
@@ -607,7 +620,11 @@ struct K {
           if (MODE != MODE_COMPACT && nyqG != nullptr) {
             T g0, g1;
             if constexpr (G::WCOL) {
+              #ifdef FFST_EXP_GL1
+              const cpx<T> gg = ldg_keep2<T>(reinterpret_cast<const cpx<T>*>(gsafe + m1));
+#else
               const cpx<T> gg = __ldg(reinterpret_cast<const cpx<T>*>(gsafe + m1));
+#endif
               g0 = gg.x; g1 = gg.y;
             } else {
               g0 = sG[m1]; g1 = sG[m1 + 1];
