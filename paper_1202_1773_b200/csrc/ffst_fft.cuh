@@ -41,6 +41,9 @@ template <typename T, int M, bool INV> FFST_HD cpx<T> mul_w16(cpx<T> a) {
                               -1.0, -0.92387953251128675613, -0.70710678118654752440, -0.38268343236508977173};
     const T c = T(C[m]);
     const T s = INV ? T(S[m]) : T(-S[m]);      // exp(-+ i theta) = cos -+ i sin
+#ifdef FFST_HAVE_F2
+    if constexpr (sizeof(T) == 4) return cmul<T>(a, mk<T>(c, s));
+#endif
     return mk<T>(a.x * c - a.y * s, a.x * s + a.y * c);
   }
 }
@@ -52,6 +55,17 @@ template <typename T, bool INV> FFST_HD void dft2(cpx<T>& a0, cpx<T>& a1) {
 
 template <typename T, bool INV> FFST_HD void dft4(cpx<T>& a0, cpx<T>& a1, cpx<T>& a2, cpx<T>& a3) {
   const cpx<T> s0 = cadd<T>(a0, a2), d0 = csub<T>(a0, a2);
+#ifdef FFST_HAVE_F2
+  if constexpr (sizeof(T) == 4) {   // d0 +- (-+ i) e as fused multiply-adds on the swapped pair
+    const float2 s1 = f2_add(a1, a3), e = f2_sub(a1, a3);
+    const float2 es = make_float2(e.y, e.x);
+    const float sg = INV ? -1.f : 1.f;                  // * (-+ i): (e.y, -e.x) / (-e.y, e.x)
+    a0 = f2_add(s0, s1); a2 = f2_sub(s0, s1);
+    a1 = f2_fma(es, make_float2(sg, -sg), d0);
+    a3 = f2_fma(es, make_float2(-sg, sg), d0);
+    return;
+  }
+#endif
   const cpx<T> s1 = cadd<T>(a1, a3), d1 = mul_mi<T, INV>(csub<T>(a1, a3));
   a0 = cadd<T>(s0, s1); a2 = csub<T>(s0, s1);
   a1 = cadd<T>(d0, d1); a3 = csub<T>(d0, d1);

@@ -195,19 +195,6 @@ template <> __device__ __forceinline__ void load_pair_cs<double>(const double2* 
 }
 
 // Asynchronous global -> shared copies (LDGSTS): no registers held while in flight.
-// Loads of the small vectors an item re-reads for every row (the Nyquist terms G, H): read-only path,
-// kept in L1 against the streaming traffic (L1::evict_last).
-template <typename T> __device__ __forceinline__ cpx<T> ldg_keep2(const cpx<T>* src);
-template <> __device__ __forceinline__ float2 ldg_keep2<float>(const float2* src) {
-  float2 v;
-  asm("ld.global.nc.L1::evict_last.v2.f32 {%0, %1}, [%2];" : "=f"(v.x), "=f"(v.y) : "l"(src));
-  return v;
-}
-template <> __device__ __forceinline__ double2 ldg_keep2<double>(const double2* src) {
-  double2 v;
-  asm("ld.global.nc.L1::evict_last.v2.f64 {%0, %1}, [%2];" : "=d"(v.x), "=d"(v.y) : "l"(src));
-  return v;
-}
 template <typename T> __device__ __forceinline__ void cp_async_el(cpx<T>* dst_smem, const cpx<T>* src, unsigned long long pol,
                                                                  bool hint) {
   const unsigned d = (unsigned)__cvta_generic_to_shared(dst_smem);
@@ -597,10 +584,10 @@ struct K {
       for (int q = 0; q < G::ER; ++q) {
         const int k = t + q * G::THR;
         const C xk = z[q], xm = zm[q];
-        const C a = mk<T>(xk.x + xm.x, xk.y - xm.y);      // xk + conj(xm)
-        const C d = mk<T>(xk.x - xm.x, xk.y + xm.y);      // xk - conj(xm)
+        const C a = cadd_conj<T>(xk, xm);                   // xk + conj(xm)
+        const C d = csub_conj<T>(xk, xm);                   // xk - conj(xm)
         const C e = cmulc<T>(d, twk(k, tw));                // d * exp(+2 pi i k / N)
-        z[q] = mk<T>(a.x - e.y, a.y + e.x);                 // a + i e
+        z[q] = cadd_i<T>(a, e);                             // a + i e
       }
       if (rd == 0) FFST_PROBE(p, 0);
       if (!(p.dbg & 1)) fft<H, true, true>(z, scr + line * G::SMR, t, tw);
@@ -615,22 +602,20 @@ struct K {
 #pragma unroll
         for (int q = 0; q < G::ER; ++q) {
           const int m1 = 2 * (t + q * G::THR);
-          const T x0 = z[q].x * scale, x1 = z[q].y * scale;
+          const C xs = cscale<T>(z[q], scale);
+          const T x0 = xs.x, x1 = xs.y;
           T c0 = T(0), c1 = T(0);
           if (MODE != MODE_COMPACT && nyqG != nullptr) {
             T g0, g1;
             if constexpr (G::WCOL) {
-              #ifdef FFST_EXP_GL1
-              const cpx<T> gg = ldg_keep2<T>(reinterpret_cast<const cpx<T>*>(gsafe + m1));
-#else
-              const cpx<T> gg = __ldg(reinterpret_cast<const cpx<T>*>(gsafe + m1));
-#endif
+                            const cpx<T> gg = __ldg(reinterpret_cast<const cpx<T>*>(gsafe + m1));
               g0 = gg.x; g1 = gg.y;
             } else {
               g0 = sG[m1]; g1 = sG[m1 + 1];
             }
-            c0 = sr * g0 + hr;
-            c1 = sr * g1 - hr;
+            const C cc = cfma_real<T>(sr, mk<T>(g0, g1), mk<T>(hr, -hr));
+            c0 = cc.x;
+            c1 = cc.y;
           }
           if constexpr (MODE == MODE_MAIN) {
             if (!(p.dbg & 2)) store_pair_cs<T>(out_c + (size_t)r * N + m1, mk<T>(x0, c0), mk<T>(x1, c1));
@@ -944,8 +929,8 @@ struct K {
             const int k = c_lo + kk;                         // 0..H
             const C zk = sl[Pad<T>::at(k)];
             const C zm = sl[Pad<T>::at(k == 0 ? 0 : N - k)];
-            const C xa = mk<T>(T(0.5) * (zk.x + zm.x), T(0.5) * (zk.y - zm.y));
-            const C xb = mk<T>(T(0.5) * (zk.y + zm.y), T(0.5) * (zm.x - zk.x));
+            const C xa = cscale<T>(cadd_conj<T>(zk, zm), T(0.5));
+            const C xb = cscale_mi<T>(csub_conj<T>(zk, zm), T(0.5));
             C* d = dst + G::iat(ra, kk, ncols);
             if (!(p.dbg & 2)) {
               if (p.ring_stream) store_pair_hint<T>(d, xa, xb, pfd);
@@ -958,8 +943,8 @@ struct K {
             const int k = c_lo + kk;                         // 0..H
             const C zk = sl[Pad<T>::at(k)];
             const C zm = sl[Pad<T>::at(k == 0 ? 0 : N - k)];
-            tile[ri * G::TSTR + kk] = mk<T>(T(0.5) * (zk.x + zm.x), T(0.5) * (zk.y - zm.y));
-            tile[(ri + 1) * G::TSTR + kk] = mk<T>(T(0.5) * (zk.y + zm.y), T(0.5) * (zm.x - zk.x));
+            tile[ri * G::TSTR + kk] = cscale<T>(cadd_conj<T>(zk, zm), T(0.5));
+            tile[(ri + 1) * G::TSTR + kk] = cscale_mi<T>(csub_conj<T>(zk, zm), T(0.5));
           }
         }
         SyncOf<G::THC>::sync();
@@ -971,6 +956,21 @@ struct K {
       const int rows_here = cnt - ti * G::GR < G::GR ? cnt - ti * G::GR : G::GR;
       const unsigned long long pf = policy_evict_first();
 #pragma unroll 1
+#ifdef FFST_EXP_ST16
+      // two rows of a column per thread: one 16-byte store (rows r, r + 1 are adjacent in W, r even)
+      static_assert(!G::WBLK_INV && G::GR % 2 == 0, "pair stores need the plain column-major W");
+      for (int e = tid; e < (p.dbg & 2 ? 0 : ncols * (G::GR / 2)); e += NT) {
+        const int kk = e / (G::GR / 2), ri = 2 * (e - kk * (G::GR / 2));
+        if (ri + 1 < rows_here) {
+          C* d = dst + G::iat(rt0 + ri, kk, ncols);
+          const C a = tile[ri * G::TSTR + kk], b = tile[(ri + 1) * G::TSTR + kk];
+          if (p.ring_stream) store_pair_hint<T>(d, a, b, pf);
+          else store_pair_cg<T>(d, a, b);
+        } else if (ri < rows_here) {
+          dst[G::iat(rt0 + ri, kk, ncols)] = tile[ri * G::TSTR + kk];
+        }
+      }
+#else
       for (int e = tid; e < (p.dbg & 2 ? 0 : ncols * G::GR); e += NT) {
         const int kk = e / G::GR, ri = e - kk * G::GR;
         if (ri < rows_here) {
@@ -978,6 +978,7 @@ struct K {
           else dst[G::iat(rt0 + ri, kk, ncols)] = tile[ri * G::TSTR + kk];
         }
       }
+#endif
       __syncthreads();
       if (ti == 0) FFST_PROBE(p, 3);
     }
@@ -1080,8 +1081,8 @@ struct K {
           const int k = c_lo + kk;                         // 0..H
           const C zk = sl[Pad<T>::at(k)];
           const C zm = sl[Pad<T>::at(k == 0 ? 0 : N - k)];
-          const C xa = mk<T>(T(0.5) * (zk.x + zm.x), T(0.5) * (zk.y - zm.y));
-          const C xb = mk<T>(T(0.5) * (zk.y + zm.y), T(0.5) * (zm.x - zk.x));
+          const C xa = cscale<T>(cadd_conj<T>(zk, zm), T(0.5));
+          const C xb = cscale_mi<T>(csub_conj<T>(zk, zm), T(0.5));
           C* d = dst + G::iat(ra, kk, ncols);
           if (!(p.dbg & 2)) {
             if (p.ring_stream) {
@@ -1097,8 +1098,8 @@ struct K {
           const int k = c_lo + kk;                         // 0..H
           const C zk = sl[Pad<T>::at(k)];
           const C zm = sl[Pad<T>::at(k == 0 ? 0 : N - k)];
-          tile[ri * tstr + kk] = mk<T>(T(0.5) * (zk.x + zm.x), T(0.5) * (zk.y - zm.y));
-          tile[(ri + 1) * tstr + kk] = mk<T>(T(0.5) * (zk.y + zm.y), T(0.5) * (zm.x - zk.x));
+          tile[ri * tstr + kk] = cscale<T>(cadd_conj<T>(zk, zm), T(0.5));
+          tile[(ri + 1) * tstr + kk] = cscale_mi<T>(csub_conj<T>(zk, zm), T(0.5));
         }
       }
       SyncOf<G::THC>::sync();
@@ -1108,6 +1109,19 @@ struct K {
         const int rt0 = r0 + ti * gr;
         const int rows_here = cnt - ti * gr < gr ? cnt - ti * gr : gr;
 #pragma unroll 1
+#ifdef FFST_EXP_ST16
+        for (int e = tid; e < (p.dbg & 2 ? 0 : ncols << (lg - 1)); e += NT) {   // (gr >= 4: row pairs, 16-byte stores)
+          const int kk = e >> (lg - 1), r = 2 * (e & ((gr >> 1) - 1));
+          if (r + 1 < rows_here) {
+            C* d = dst + G::iat(rt0 + r, kk, ncols);
+            const C a = tile[r * tstr + kk], b = tile[(r + 1) * tstr + kk];
+            if (p.ring_stream) store_pair_hint<T>(d, a, b, pf);
+            else store_pair_cg<T>(d, a, b);
+          } else if (r < rows_here) {
+            dst[G::iat(rt0 + r, kk, ncols)] = tile[r * tstr + kk];
+          }
+        }
+#else
         for (int e = tid; e < (p.dbg & 2 ? 0 : ncols << lg); e += NT) {
           const int kk = e >> lg, r = e & (gr - 1);
           if (r < rows_here) {
@@ -1115,6 +1129,7 @@ struct K {
             else dst[G::iat(rt0 + r, kk, ncols)] = tile[r * tstr + kk];
           }
         }
+#endif
         __syncthreads();
       }
 #pragma unroll
@@ -1171,8 +1186,7 @@ struct K {
 #pragma unroll
           for (int q = 0; q < G::EC; ++q) {
             const T w = wbuf[q * NT + tid];
-            acc[q].x += w * r[q].x;
-            acc[q].y += w * r[q].y;
+            acc[q] = cfma_real<T>(w, r[q], acc[q]);
           }
         }
         SyncOf<G::THC>::sync();

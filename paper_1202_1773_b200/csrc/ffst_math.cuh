@@ -41,6 +41,68 @@ template <typename T> FFST_HD cpx<T> cmulc(cpx<T> a, cpx<T> b) {
 template <typename T> FFST_HD cpx<T> conj_(cpx<T> a) { return mk<T>(a.x, -a.y); }
 template <typename T> FFST_HD cpx<T> cscale(cpx<T> a, T s) { return mk<T>(a.x * s, a.y * s); }
 template <typename T> FFST_HD cpx<T> czero() { return mk<T>(T(0), T(0)); }
+// a + conj(b), a - conj(b), a + i b, -i s a, acc + w r (w real): the Hermitian split / merge steps of the
+// real-data row passes and the window accumulation
+template <typename T> FFST_HD cpx<T> cadd_conj(cpx<T> a, cpx<T> b) { return mk<T>(a.x + b.x, a.y - b.y); }
+template <typename T> FFST_HD cpx<T> csub_conj(cpx<T> a, cpx<T> b) { return mk<T>(a.x - b.x, a.y + b.y); }
+template <typename T> FFST_HD cpx<T> cadd_i(cpx<T> a, cpx<T> b) { return mk<T>(a.x - b.y, a.y + b.x); }
+template <typename T> FFST_HD cpx<T> cscale_mi(cpx<T> a, T s) { return mk<T>(s * a.y, -s * a.x); }
+template <typename T> FFST_HD cpx<T> cfma_real(T w, cpx<T> r, cpx<T> acc) { return mk<T>(acc.x + w * r.x, acc.y + w * r.y); }
+
+// Packed float32 pairs (sm_100a FADD2 / FMUL2 / FFMA2: one instruction for both halves of a complex
+// value; ptxas folds the half swaps, broadcasts and per-half signs into operand modifiers).  Same
+// IEEE operations as the scalar forms (a product rounded, then one fused multiply-add).
+// (-DFFST_NO_F32X2 builds the scalar forms: A/B measurements.)
+#if defined(__CUDA_ARCH__) && !defined(FFST_NO_F32X2)
+#define FFST_HAVE_F2 1
+__device__ __forceinline__ float2 f2_add(float2 a, float2 b) {
+  float2 r;
+  asm("{.reg .b64 ra, rb, rc; mov.b64 ra, {%2,%3}; mov.b64 rb, {%4,%5}; add.rn.f32x2 rc, ra, rb; mov.b64 {%0,%1}, rc;}"
+      : "=f"(r.x), "=f"(r.y) : "f"(a.x), "f"(a.y), "f"(b.x), "f"(b.y));
+  return r;
+}
+__device__ __forceinline__ float2 f2_sub(float2 a, float2 b) {
+  float2 r;
+  asm("{.reg .b64 ra, rb, rc; mov.b64 ra, {%2,%3}; mov.b64 rb, {%4,%5}; sub.rn.f32x2 rc, ra, rb; mov.b64 {%0,%1}, rc;}"
+      : "=f"(r.x), "=f"(r.y) : "f"(a.x), "f"(a.y), "f"(b.x), "f"(b.y));
+  return r;
+}
+__device__ __forceinline__ float2 f2_mul(float2 a, float2 b) {
+  float2 r;
+  asm("{.reg .b64 ra, rb, rc; mov.b64 ra, {%2,%3}; mov.b64 rb, {%4,%5}; mul.rn.f32x2 rc, ra, rb; mov.b64 {%0,%1}, rc;}"
+      : "=f"(r.x), "=f"(r.y) : "f"(a.x), "f"(a.y), "f"(b.x), "f"(b.y));
+  return r;
+}
+__device__ __forceinline__ float2 f2_fma(float2 a, float2 b, float2 c) {
+  float2 r;
+  asm("{.reg .b64 ra, rb, rc, rd; mov.b64 ra, {%2,%3}; mov.b64 rb, {%4,%5}; mov.b64 rc, {%6,%7}; "
+      "fma.rn.f32x2 rd, ra, rb, rc; mov.b64 {%0,%1}, rd;}"
+      : "=f"(r.x), "=f"(r.y) : "f"(a.x), "f"(a.y), "f"(b.x), "f"(b.y), "f"(c.x), "f"(c.y));
+  return r;
+}
+template <> __device__ __forceinline__ float2 cadd<float>(float2 a, float2 b) { return f2_add(a, b); }
+template <> __device__ __forceinline__ float2 csub<float>(float2 a, float2 b) { return f2_sub(a, b); }
+template <> __device__ __forceinline__ float2 cmul<float>(float2 a, float2 b) {
+  const float2 t = f2_mul(make_float2(a.y, a.y), make_float2(b.y, b.x));
+  return f2_fma(make_float2(a.x, a.x), b, make_float2(-t.x, t.y));
+}
+template <> __device__ __forceinline__ float2 cmulc<float>(float2 a, float2 b) {
+  const float2 t = f2_mul(make_float2(a.y, a.y), make_float2(b.y, b.x));
+  return f2_fma(make_float2(a.x, a.x), make_float2(b.x, -b.y), t);
+}
+template <> __device__ __forceinline__ float2 cscale<float>(float2 a, float s) { return f2_mul(a, make_float2(s, s)); }
+template <> __device__ __forceinline__ float2 cadd_conj<float>(float2 a, float2 b) { return f2_fma(b, make_float2(1.f, -1.f), a); }
+template <> __device__ __forceinline__ float2 csub_conj<float>(float2 a, float2 b) { return f2_fma(b, make_float2(-1.f, 1.f), a); }
+template <> __device__ __forceinline__ float2 cadd_i<float>(float2 a, float2 b) {
+  return f2_fma(make_float2(b.y, b.x), make_float2(-1.f, 1.f), a);
+}
+template <> __device__ __forceinline__ float2 cscale_mi<float>(float2 a, float s) {
+  return f2_mul(make_float2(a.y, a.x), make_float2(s, -s));
+}
+template <> __device__ __forceinline__ float2 cfma_real<float>(float w, float2 r, float2 acc) {
+  return f2_fma(make_float2(w, w), r, acc);
+}
+#endif
 
 // ---------------------------------------------------------------- window math
 
