@@ -956,7 +956,6 @@ struct K {
       const int rows_here = cnt - ti * G::GR < G::GR ? cnt - ti * G::GR : G::GR;
       const unsigned long long pf = policy_evict_first();
 #pragma unroll 1
-#ifdef FFST_EXP_ST16
       // two rows of a column per thread: one 16-byte store (rows r, r + 1 are adjacent in W, r even)
       static_assert(!G::WBLK_INV && G::GR % 2 == 0, "pair stores need the plain column-major W");
       for (int e = tid; e < (p.dbg & 2 ? 0 : ncols * (G::GR / 2)); e += NT) {
@@ -970,15 +969,6 @@ struct K {
           dst[G::iat(rt0 + ri, kk, ncols)] = tile[ri * G::TSTR + kk];
         }
       }
-#else
-      for (int e = tid; e < (p.dbg & 2 ? 0 : ncols * G::GR); e += NT) {
-        const int kk = e / G::GR, ri = e - kk * G::GR;
-        if (ri < rows_here) {
-          if (p.ring_stream) st_hint<T>(dst + G::iat(rt0 + ri, kk, ncols), tile[ri * G::TSTR + kk], pf);
-          else dst[G::iat(rt0 + ri, kk, ncols)] = tile[ri * G::TSTR + kk];
-        }
-      }
-#endif
       __syncthreads();
       if (ti == 0) FFST_PROBE(p, 3);
     }
@@ -1109,7 +1099,6 @@ struct K {
         const int rt0 = r0 + ti * gr;
         const int rows_here = cnt - ti * gr < gr ? cnt - ti * gr : gr;
 #pragma unroll 1
-#ifdef FFST_EXP_ST16
         for (int e = tid; e < (p.dbg & 2 ? 0 : ncols << (lg - 1)); e += NT) {   // (gr >= 4: row pairs, 16-byte stores)
           const int kk = e >> (lg - 1), r = 2 * (e & ((gr >> 1) - 1));
           if (r + 1 < rows_here) {
@@ -1121,15 +1110,6 @@ struct K {
             dst[G::iat(rt0 + r, kk, ncols)] = tile[r * tstr + kk];
           }
         }
-#else
-        for (int e = tid; e < (p.dbg & 2 ? 0 : ncols << lg); e += NT) {
-          const int kk = e >> lg, r = e & (gr - 1);
-          if (r < rows_here) {
-            if (p.ring_stream) st_hint<T>(dst + G::iat(rt0 + r, kk, ncols), tile[r * tstr + kk], pf);
-            else dst[G::iat(rt0 + r, kk, ncols)] = tile[r * tstr + kk];
-          }
-        }
-#endif
         __syncthreads();
       }
 #pragma unroll
