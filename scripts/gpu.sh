@@ -37,7 +37,7 @@ case "$task" in
       --log-file gpurun_out/launches_$tag.csv $CMD > gpurun_out/launches_$tag.log 2>&1; echo "ncu launches exit $?" ;;
   prof) c=$1; tag=$2; kr=${3:-main_kernel}; s=${4:-2}; cnt=${5:-2}
     CMD="python bench.py --config $c --steps 1 --warmup 1 --no-cpu-baseline --no-cufft"
-    $CMD > gpurun_out/plain_$tag.log 2>&1 && timeout 1800 ncu --set full --clock-control none --import-source on \
+    $CMD > gpurun_out/plain_$tag.log 2>&1 && timeout 1800 ncu -f --set full --clock-control none --import-source on \
       -k regex:$kr -s $s -c $cnt -o /tmp/prof_$tag $CMD > /tmp/ncu_$tag.log 2>&1; echo "ncu exit $?"
     tail -2 /tmp/ncu_$tag.log
     ncu -i /tmp/prof_$tag.ncu-rep --page raw --csv > gpurun_out/prof_${tag}_raw.csv 2>&1
