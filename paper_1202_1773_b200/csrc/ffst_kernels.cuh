@@ -590,15 +590,6 @@ struct K {
         z[q] = cadd_i<T>(a, e);                             // a + i e
       }
       if (rd == 0) FFST_PROBE(p, 0);
-#ifdef FFST_EXP_PFG
-      if constexpr (G::WCOL && MODE == MODE_MAIN) {   // the Nyquist terms this round adds: into L1 behind the FFT
-        if (nyqG != nullptr) {
-#pragma unroll
-          for (int q = 0; q < G::ER; ++q)                  // (the addresses the store loop reads)
-            asm volatile("prefetch.global.L1 [%0];" ::"l"(nyqG + 2 * (t + q * G::THR)));
-        }
-      }
-#endif
       if (!(p.dbg & 1)) fft<H, true, true>(z, scr + line * G::SMR, t, tw);
       if (rd == 0) FFST_PROBE(p, 1);
       if (act) {
