@@ -825,43 +825,6 @@ struct K {
     }
   }
 
-  // Inverse pass 1, n = 4096 (one line per CTA; FFST_EXP_QUAD): the two rounds of a 4-row segment
-  // keep their FFT results in two scratch lines (the second one in the tile region), and the
-  // extraction stores rows ra .. ra + 3 of each column straight to W (two 16-byte stores, one full
-  // 32-byte run): no shared tile, no CTA-wide store phase.
-#ifdef FFST_EXP_QUAD
-  static constexpr bool QUAD = G::LPC == 1 && !G::DIRW && !G::WBLK_INV && G::GR == 4 && sizeof(T) == 4;
-#else
-  static constexpr bool QUAD = false;
-#endif
-  static __device__ __forceinline__ void quad_extract(const KParams& p, const C* A_, const C* B_, bool two, int c_lo,
-                                                      int ncols, int ra, C* dst, int t, unsigned long long pf) {
-#pragma unroll 2
-    for (int kk = t; kk < ncols; kk += G::THC) {
-      const int k = c_lo + kk;                         // 0..H
-      const int ik = Pad<T>::at(k), im = Pad<T>::at(k == 0 ? 0 : N - k);
-      C* d = dst + G::iat(ra, kk, ncols);
-      {
-        const C zk = A_[ik], zm = A_[im];
-        const C xa = cscale<T>(cadd_conj<T>(zk, zm), T(0.5));
-        const C xb = cscale_mi<T>(csub_conj<T>(zk, zm), T(0.5));
-        if (!(p.dbg & 2)) {
-          if (p.ring_stream) store_pair_hint<T>(d, xa, xb, pf);
-          else store_pair_cg<T>(d, xa, xb);
-        }
-      }
-      if (two) {
-        const C zk = B_[ik], zm = B_[im];
-        const C xa = cscale<T>(cadd_conj<T>(zk, zm), T(0.5));
-        const C xb = cscale_mi<T>(csub_conj<T>(zk, zm), T(0.5));
-        if (!(p.dbg & 2)) {
-          if (p.ring_stream) store_pair_hint<T>(d + 2, xa, xb, pf);
-          else store_pair_cg<T>(d + 2, xa, xb);
-        }
-      }
-    }
-  }
-
   // Inverse pass 1 (PAIR): Z = Re c(ra, .) + i Re c(ra+1, .), one forward FFT; the rows' spectra
   // Xa[k] = (Z[k] + conj Z[N-k])/2, Xb[k] = (Z[k] - conj Z[N-k])/(2i) for the plane's bins -> tile
   // -> W (column-major), plus the alternating sums of Im c for Nyquist planes.  Same results as
@@ -885,7 +848,7 @@ struct K {
     const int ntiles = (cnt + G::GR - 1) / G::GR;
     const bool direct = G::DIRW ^ ((p.dbg & 128) != 0);    // (see row_r2c_pair_pipe)
     const unsigned long long pfd = policy_evict_first();
-    if ((direct || QUAD) && dep != nullptr) {
+    if (direct && dep != nullptr) {
       if (tid == 0) spin_wait(dep, dep_target);           // slot reuse: before the first write
       __syncthreads();
     }
@@ -941,7 +904,7 @@ struct K {
           }
         }
         if (ti == 0 && rd == 0) FFST_PROBE(p, 0);
-        C* sl = (QUAD && rd == 1) ? tile : scr + line * G::SMC;
+        C* sl = scr + line * G::SMC;
         if (!(p.dbg & 1)) fft<N, false>(z, sl, t, tw);
         if (ti == 0 && rd == 0) FFST_PROBE(p, 1);
         if (nyq) {   // alternating row sums t(r) = sum_m1 (-1)^m1 Im c(r, m1): one partial per warp
@@ -960,9 +923,7 @@ struct K {
 #pragma unroll
         for (int q = 0; q < G::EC; ++q) sl[Pad<T>::at(t + q * G::THC)] = z[q];
         SyncOf<G::THC>::sync();
-        if constexpr (QUAD) {
-          if (rd == 1) quad_extract(p, scr, tile, act, c_lo, ncols, rt0, dst, t, pfd);
-        } else if (act && direct) {
+        if (act && direct) {
 #pragma unroll 2
           for (int kk = t; kk < ncols; kk += G::THC) {
             const int k = c_lo + kk;                         // 0..H
@@ -989,7 +950,7 @@ struct K {
         SyncOf<G::THC>::sync();
         if (ti == 0 && rd == 0) FFST_PROBE(p, 2);
       }
-      if (direct || QUAD) continue;  // (each line reuses only its own scratch: no CTA barrier per tile)
+      if (direct) continue;          // (each line reuses only its own scratch: no CTA barrier per tile)
       if (dep != nullptr && ti == 0 && tid == 0) spin_wait(dep, dep_target);   // slot reuse: before the first write
       __syncthreads();
       const int rows_here = cnt - ti * G::GR < G::GR ? cnt - ti * G::GR : G::GR;
@@ -1013,7 +974,7 @@ struct K {
     }
     if (nyq) {
       // partial alternating column sums s(m1) over this item's rows: lines summed in fixed order
-      if (direct || QUAD) __syncthreads();                  // (every line done with its scratch)
+      if (direct) __syncthreads();                          // (every line done with its scratch)
       T* rs = reinterpret_cast<T*>(scr);                    // [LPC][N] scalars (fits SCR_C)
 #pragma unroll
       for (int q = 0; q < G::EC; ++q) rs[line * N + t + q * G::THC] = sacc[q];
@@ -1047,7 +1008,7 @@ struct K {
     // GR up to 16 dividing the item; row stride ncols | 1), so that each column segment of W is
     // 64-128 bytes instead of GR x 8 (fewer, fuller L2 writes, fewer store phases)
     int gr = G::GR, tstr = G::TSTR;
-    if (G::GR < 16 && !QUAD) {
+    if (G::GR < 16) {
       const int ts = ncols | 1;
       while (gr < 16 && 2 * gr * ts <= G::TILE_R && cnt % (2 * gr) == 0) gr *= 2;
       if (gr > G::GR) tstr = ts;
@@ -1073,7 +1034,7 @@ struct K {
     // stores each column's two rows straight to W (one 16-byte store per column and row pair,
     // column-major: rows ra, ra + 1 are adjacent), no shared tile and no CTA-wide store phase
     const bool direct = G::DIRW ^ ((p.dbg & 128) != 0);
-    if ((direct || QUAD) && dep != nullptr) {
+    if (direct && dep != nullptr) {
       if (tid == 0) spin_wait(dep, dep_target);           // slot reuse: before the first write
       __syncthreads();
     }
@@ -1097,15 +1058,13 @@ struct K {
       C z[G::EC];
 #pragma unroll
       for (int q = 0; q < G::EC; ++q) z[q] = mk<T>(ca[q], cb[q]);
-      C* sl = (QUAD && rd == 1) ? tile : scr + line * G::SMC;
+      C* sl = scr + line * G::SMC;
       if (!(p.dbg & 1)) fft<N, false>(z, sl, t, tw);
       SyncOf<G::THC>::sync();
 #pragma unroll
       for (int q = 0; q < G::EC; ++q) sl[Pad<T>::at(t + q * G::THC)] = z[q];
       SyncOf<G::THC>::sync();
-      if constexpr (QUAD) {
-        if (rd == 1 || i + 1 == nrounds) quad_extract(p, scr, tile, rd == 1, c_lo, ncols, r0 + ti * gr, dst, t, pf);
-      } else if (act && direct) {
+      if (act && direct) {
         const int ra = r0 + ti * gr + ri;
 #pragma unroll 2
         for (int kk = t; kk < ncols; kk += G::THC) {
@@ -1134,7 +1093,7 @@ struct K {
         }
       }
       SyncOf<G::THC>::sync();
-      if (!direct && !QUAD && (rd == ROUNDS - 1 || i + 1 == nrounds)) {   // the tile is complete: -> W (column-major)
+      if (!direct && (rd == ROUNDS - 1 || i + 1 == nrounds)) {   // the tile is complete: -> W (column-major)
         if (dep != nullptr && ti == 0 && tid == 0) spin_wait(dep, dep_target);   // slot reuse
         __syncthreads();
         const int rt0 = r0 + ti * gr;
